@@ -1,0 +1,164 @@
+/*
+ * mst.h — C ABI of the B200-native Mini-Sequence Transformer (MsT) hot path.
+ *
+ * The reference (arxiv 2407.15892, mounted at /root/reference) specifies the
+ * operator API of module `miniseq` in prose and ships no
+ * implementation.  Each entry point below replaces one SPEC operation; the
+ * citation is given per function.  All compute runs on sm_100a kernels from
+ * libmst.so; there is no CPU fallback.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Device pointers are CUDA device memory;
+ *    `stream` is a cudaStream_t (NULL = legacy default stream).
+ *  - Activations/weights are bf16 (uint16 storage), row-major, in the SPEC
+ *    orientation: X[N,H]; W_gate, W_up [H,I]; W_down [I,H]; W_out [H,V]
+ *    (SPEC.md:179-185).  Weight gradients are fp32 row-major, same shapes.
+ *    Labels are int32 [N] with ignore value -100.
+ *  - The caller owns every buffer, including the scratch `workspace`
+ *    (size from the matching *_workspace query).  Calls are asynchronous on
+ *    `stream`; results are valid after the stream is synchronised.
+ *  - Errors: every function returns an mst_status; mst_last_error() gives a
+ *    thread-local message.  Codes map 1:1 onto the reference's error
+ *    taxonomy (proj/include/minitrain/error.hpp:14-20).
+ */
+#ifndef MST_MST_H_
+#define MST_MST_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MST_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define MST_API __attribute__((visibility("default")))
+#else
+#define MST_API
+#endif
+
+typedef enum mst_status {
+  MST_OK = 0,
+  MST_ERR_SHAPE = 1,     /* minitrain::ShapeError      error.hpp:14 */
+  MST_ERR_BOUNDS = 2,    /* minitrain::BoundsError     error.hpp:15 */
+  MST_ERR_DTYPE = 3,     /* minitrain::DtypeError      error.hpp:16 */
+  MST_ERR_CONFIG = 4,    /* minitrain::ConfigError     error.hpp:17 */
+  MST_ERR_DATA = 5,      /* minitrain::DataError       error.hpp:18 */
+  MST_ERR_STATE = 6,     /* minitrain::StateError      error.hpp:19 */
+  MST_ERR_NONFINITE = 7, /* minitrain::NonFiniteError  error.hpp:20 */
+  MST_ERR_CUDA = 8,      /* CUDA runtime / driver failure (no reference analogue) */
+  MST_ERR_INTERNAL = 9
+} mst_status;
+
+/* Loss reduction over mini-sequences. */
+typedef enum mst_loss_mode {
+  MST_LOSS_TOKEN_WEIGHTED = 0, /* sum(loss_sum_i) / sum(valid_i)  (default) */
+  MST_LOSS_PAPER_MEAN = 1      /* (sum_i mean_i) / M  (Alg. 2 line 8 literal) */
+} mst_loss_mode;
+
+typedef struct mst_ctx mst_ctx;
+
+/* Layout of the device `stats` buffer written by mst_lmhead_forward.
+ * MST_STATS_LEN(M) floats: [0] loss_sum, [1] valid count, [2] loss,
+ * [3] invalid-label count, [4..4+M) per-chunk loss sums,
+ * [4+M..4+2M) per-chunk valid counts.  Entries 0..1 are additive across
+ * sequence shards (all-reduce SUM them for the global token-weighted loss). */
+#define MST_STATS_LEN(M) (4 + 2 * (M))
+
+/* Saved state between forward and backward.
+ * Filled by the forward call; the backward call checks the fingerprint and
+ * raises MST_ERR_STATE on a stale or mismatched record. */
+typedef struct mst_mlp_saved {
+  const void* x;
+  const void* w_gate;
+  const void* w_up;
+  const void* w_down;
+  int64_t n, h, i, m;
+  uint64_t fingerprint;
+} mst_mlp_saved;
+
+typedef struct mst_lmhead_saved {
+  const void* x;
+  const int32_t* labels;
+  const void* w_out;
+  float* lse;   /* device [n] fp32: log-sum-exp per row (the only saved activation) */
+  float* stats; /* device MST_STATS_LEN(m) */
+  int64_t n, h, v, m;
+  int32_t loss_mode;
+  int32_t _pad;
+  uint64_t fingerprint;
+} mst_lmhead_saved;
+
+MST_API int mst_abi_version(void);
+MST_API const char* mst_last_error(void);
+
+/* Context: one per host thread per device (SPEC.md:99 threading contract). */
+MST_API int mst_ctx_create(int device, mst_ctx** out);
+MST_API void mst_ctx_destroy(mst_ctx* ctx);
+/* Number of CTA pairs a grouped launch uses (diagnostics / tests). */
+MST_API int mst_ctx_num_pairs(const mst_ctx* ctx);
+/* Kernel launches issued by this context since creation (bench evidence). */
+MST_API int64_t mst_ctx_launch_count(const mst_ctx* ctx);
+
+/* make_chunk_plan(N, M) — SPEC.md:286-294.  Writes min(M,N)+1 row bounds
+ * into `bounds` (capacity >= min(M,N)+1): chunk c is [bounds[c], bounds[c+1]).
+ * Balanced rule: the first N mod M chunks hold ceil(N/M) rows. */
+MST_API int mst_make_chunk_plan(int64_t n, int64_t m, int64_t* bounds, int64_t* num_chunks);
+
+/* Scratch sizes (bytes) for each operation. */
+MST_API int mst_mlp_workspace(int64_t n, int64_t h, int64_t i, int64_t m, size_t* bytes);
+MST_API int mst_lmhead_workspace(int64_t n, int64_t h, int64_t v, int64_t m, size_t* bytes);
+MST_API int mst_block_workspace(int64_t n, int64_t h, int64_t i, int64_t v, int64_t m_mlp, int64_t m_head, size_t* bytes);
+
+/* miniseq_mlp_forward(X, w, plan) -> (O, saved) — SPEC.md:295-303, Alg. 1.
+ * O = (silu(X W_gate) * (X W_up)) W_down per chunk; only X is retained. */
+MST_API int mst_mlp_forward(mst_ctx* ctx, void* stream, const void* x, const void* w_gate, const void* w_up,
+                    const void* w_down, void* out, int64_t n, int64_t h, int64_t i, int64_t m,
+                    void* workspace, size_t workspace_bytes, mst_mlp_saved* saved);
+
+/* miniseq_mlp_backward(dO, saved, w, plan) -> (dX, dW) — SPEC.md:304-312, Alg. 3.
+ * Per chunk: recompute G,U,h; dX concatenated; dW accumulated in fp32 in
+ * ascending chunk order.  accumulate=0 overwrites dW, 1 adds onto it. */
+MST_API int mst_mlp_backward(mst_ctx* ctx, void* stream, const void* grad_out, const mst_mlp_saved* saved,
+                     const void* w_gate, const void* w_up, const void* w_down, void* grad_x,
+                     float* grad_w_gate, float* grad_w_up, float* grad_w_down, int accumulate,
+                     void* workspace, size_t workspace_bytes);
+
+/* miniseq_lmhead_forward(X, L, w, plan, mode) -> (loss, saved) — SPEC.md:313-321, Alg. 2.
+ * Logits are never written to HBM: the GEMM epilogue keeps an online
+ * softmax.  `stats` receives the loss (see MST_STATS_LEN); `lse` [n]. */
+MST_API int mst_lmhead_forward(mst_ctx* ctx, void* stream, const void* x, const int32_t* labels, const void* w_out,
+                       int64_t n, int64_t h, int64_t v, int64_t m, int loss_mode, float* stats, float* lse,
+                       void* workspace, size_t workspace_bytes, mst_lmhead_saved* saved);
+
+/* miniseq_lmhead_backward(saved, w, plan, mode) -> (dX, dW_out) — SPEC.md:322-330, Alg. 4.
+ * `global_stats` may be the forward's stats or an all-reduced copy (sequence
+ * sharding); token-weighted scaling uses global_stats[1] as the count.
+ * grad_loss is the scalar upstream gradient. */
+MST_API int mst_lmhead_backward(mst_ctx* ctx, void* stream, const mst_lmhead_saved* saved, const void* w_out,
+                        const float* global_stats, float grad_loss, void* grad_x, float* grad_w_out,
+                        int accumulate, void* workspace, size_t workspace_bytes);
+
+/* One fused MLP -> LM-Head block, forward + backward (the bench unit):
+ * O = mlp(X); loss = CE(O W_out, L); then dW_out, dO, dX, dW_{gate,up,down}.
+ * `stats` as in mst_lmhead_forward (device, MST_STATS_LEN(m_head) floats). */
+MST_API int mst_block_step(mst_ctx* ctx, void* stream, const void* x, const int32_t* labels, const void* w_gate,
+                   const void* w_up, const void* w_down, const void* w_out, int64_t n, int64_t h, int64_t i,
+                   int64_t v, int64_t m_mlp, int64_t m_head, int loss_mode, float grad_loss, float* stats,
+                   void* grad_x, float* grad_w_gate, float* grad_w_up, float* grad_w_down, float* grad_w_out,
+                   int accumulate, void* workspace, size_t workspace_bytes);
+
+/* Diagnostic single GEMM through the same engine: C[M,N] = A[M,K] B[K,N].
+ * a_mn=0: A row-major [M,K]; a_mn=1: A given as row-major [K,M] (A^T).
+ * b_mn=1: B row-major [K,N]; b_mn=0: B given as row-major [N,K] (B^T).
+ * out_f32=0: C bf16; 1: C fp32 with C = beta*C + A B (beta in {0,1}). */
+MST_API int mst_debug_gemm(mst_ctx* ctx, void* stream, const void* a, const void* b, void* c, int64_t m, int64_t n,
+                   int64_t k, int a_mn, int b_mn, int out_f32, int beta);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MST_MST_H_ */

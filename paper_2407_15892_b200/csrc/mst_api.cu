@@ -1,0 +1,908 @@
+// C-ABI implementation of the MsT hot path (include/mst/mst.h).
+//
+// Host responsibilities: argument validation with the reference's error
+// taxonomy, TMA tensor-map encoding, the mini-sequence chunk loop
+// (SPEC.md:271-361), grouping independent GEMMs of a chunk into one
+// persistent launch, and an LPT (longest-processing-time-first) tile
+// schedule per launch so CTA pairs finish together.  All arithmetic runs in
+// the sm_100a kernels of gemm.cuh and the small kernels below.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <mutex>
+#include <queue>
+#include <string>
+#include <vector>
+
+#include "gemm.cuh"
+#include "mst/mst.h"
+
+using mst::GemmParams;
+using mst::PhaseDesc;
+using mst::ProblemDesc;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Status {
+  int code = MST_OK;
+};
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define MST_CUDA(expr)                                                                        \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess) return fail(MST_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define MST_TRY(expr)              \
+  do {                             \
+    int s_ = (expr);               \
+    if (s_ != MST_OK) return s_;   \
+  } while (0)
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+uint64_t fnv1a(const void* data, size_t n, uint64_t h = 0xcbf29ce484222325ull) {
+  const unsigned char* p = static_cast<const unsigned char*>(data);
+  for (size_t k = 0; k < n; ++k) {
+    h ^= p[k];
+    h *= 0x100000001b3ull;
+  }
+  return h;
+}
+
+int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Sequential bump allocator over the caller's workspace.
+struct Carve {
+  char* base;
+  size_t cap;
+  size_t used = 0;
+  bool dry;  // size query only
+  void* take(size_t bytes) {
+    used = align_up(used, 256);
+    void* p = dry ? nullptr : base + used;
+    used += bytes;
+    return p;
+  }
+};
+
+}  // namespace
+
+struct SchedEntry {
+  int32_t* dev = nullptr;  // [off (pairs+1) | tiles]
+  int32_t num_pairs = 0;
+};
+
+struct mst_ctx {
+  int device = 0;
+  int num_sms = 0;
+  int num_pairs = 0;
+  EncodeTiledFn encode = nullptr;
+  std::map<std::string, SchedEntry> sched_cache;
+  int64_t launches = 0;
+  float* scratch_dev = nullptr;  // small persistent device scratch
+};
+
+namespace {
+
+// ------------------------------------------------------------ tensor maps
+int tmap_2d(mst_ctx* c, CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t ld_elems,
+            uint32_t box_inner, uint32_t box_outer) {
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0)
+    return fail(MST_ERR_CONFIG, "tensor base %p is not 16-byte aligned", base);
+  if ((ld_elems * 2) % 16 != 0) return fail(MST_ERR_CONFIG, "row stride %llu elems not a multiple of 8", (unsigned long long)ld_elems);
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld_elems * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = c->encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(MST_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) dims=%llu x %llu box=%u x %u", (int)r,
+                (unsigned long long)inner, (unsigned long long)outer, box_inner, box_outer);
+  return MST_OK;
+}
+
+// Operand of a GEMM, as stored in global memory (row-major, ld elements).
+//   K-major : element (row, k) at base[row*ld + k]      -> map dims {K, rows}
+//   MN-major: element (k, mn)  at base[k*ld + mn]       -> map dims {MN, K}
+struct Operand {
+  const void* base;
+  int64_t mn;  // rows (M for A, N for B)
+  int64_t k;
+  int64_t ld;
+  bool mn_major;
+};
+
+// Builder for one launch: collects tensor maps and problems.
+struct Launch {
+  GemmParams p;
+  int nmaps = 0;
+  int acc_cols = 0;
+  Launch() { std::memset(&p, 0, sizeof(p)); }
+};
+
+int add_map(mst_ctx* c, Launch& L, const Operand& o, int box_mn) {
+  if (L.nmaps >= mst::kMaxMaps) return fail(MST_ERR_INTERNAL, "too many tensor maps in one launch");
+  CUtensorMap* m = &L.p.maps[L.nmaps];
+  int s = o.mn_major ? tmap_2d(c, m, o.base, o.mn, o.k, o.ld, 64, 64) : tmap_2d(c, m, o.base, o.k, o.mn, o.ld, 64, box_mn);
+  if (s != MST_OK) return s;
+  return -(L.nmaps++) - 100;  // encoded index (negative to distinguish from status)
+}
+
+int map_index(int encoded) { return -(encoded + 100); }
+
+struct PhaseSpec {
+  Operand a;
+  Operand b0, b1;  // B source for CTA rank 0 / 1
+  int umma_n;
+  int tmem_col;
+  int b_off0, b_off1;
+  bool acc_continue;
+};
+
+int add_phase(mst_ctx* c, Launch& L, ProblemDesc& P, const PhaseSpec& s) {
+  PhaseDesc& d = P.ph[P.num_phases++];
+  int ea = add_map(c, L, s.a, 128);
+  if (ea >= 0) return ea;
+  const int nh = s.umma_n / 2;
+  int eb0 = add_map(c, L, s.b0, nh);
+  if (eb0 >= 0) return eb0;
+  int eb1 = eb0;
+  if (s.b1.base != s.b0.base || s.b1.mn != s.b0.mn) {
+    eb1 = add_map(c, L, s.b1, nh);
+    if (eb1 >= 0) return eb1;
+  }
+  d.map_a = map_index(ea);
+  d.map_b0 = map_index(eb0);
+  d.map_b1 = map_index(eb1);
+  d.a_mn = s.a.mn_major ? 1 : 0;
+  d.b_mn = s.b0.mn_major ? 1 : 0;
+  d.umma_n = s.umma_n;
+  d.tmem_col = s.tmem_col;
+  d.k_blocks = static_cast<int32_t>(cdiv(s.a.k, mst::kBK));
+  d.b_off0 = s.b_off0;
+  d.b_off1 = s.b_off1;
+  d.acc_continue = s.acc_continue ? 1 : 0;
+  L.acc_cols = std::max(L.acc_cols, s.tmem_col + s.umma_n);
+  return MST_OK;
+}
+
+// Estimated tile cost in SM cycles (for LPT scheduling only).
+double tile_cost(const ProblemDesc& P) {
+  double mma = 0;
+  for (int i = 0; i < P.num_phases; ++i) mma += double(P.ph[i].k_blocks) * P.ph[i].umma_n * 2.0;
+  double bytes = 0;
+  switch (P.epi) {
+    case mst::kEpiStoreBf16: bytes = 256.0 * P.ph[0].umma_n * 2; break;
+    case mst::kEpiAccF32: bytes = 256.0 * P.ph[0].umma_n * 4 * (P.beta ? 2 : 1); break;
+    case mst::kEpiSwiglu: bytes = 256.0 * 128 * 2; break;
+    case mst::kEpiMlpBwd: bytes = 3 * 256.0 * 128 * 2; break;
+    case mst::kEpiCeFwd: bytes = 256.0 * 16; break;
+    case mst::kEpiCeBwd: bytes = 256.0 * 256 * 2; break;
+  }
+  const double epi = bytes / 46.0;
+  return std::max(mma, epi) + 800.0;
+}
+
+int get_schedule(mst_ctx* c, const GemmParams& p, const int32_t** sched, const int32_t** off) {
+  std::string key;
+  for (int i = 0; i < p.num_problems; ++i) {
+    const ProblemDesc& P = p.prob[i];
+    char buf[160];
+    snprintf(buf, sizeof(buf), "%d:%d:%d:%d:%d:%d:%d|", P.m_tiles, P.n_tiles, P.epi, P.beta, P.num_phases,
+             P.ph[0].k_blocks * 1000 + P.ph[0].umma_n, P.num_phases > 1 ? P.ph[1].k_blocks * 1000 + P.ph[1].umma_n : 0);
+    key += buf;
+  }
+  auto it = c->sched_cache.find(key);
+  if (it == c->sched_cache.end()) {
+    struct T {
+      double cost;
+      int32_t code;
+      int order;
+    };
+    std::vector<T> tiles;
+    for (int i = 0; i < p.num_problems; ++i) {
+      const ProblemDesc& P = p.prob[i];
+      const double cst = tile_cost(P);
+      const int nt = P.m_tiles * P.n_tiles;
+      for (int t = 0; t < nt; ++t) tiles.push_back({cst, (i << 24) | t, (int)tiles.size()});
+    }
+    std::stable_sort(tiles.begin(), tiles.end(), [](const T& a, const T& b) { return a.cost > b.cost; });
+    const int np = c->num_pairs;
+    using Q = std::pair<double, int>;
+    std::priority_queue<Q, std::vector<Q>, std::greater<Q>> heap;
+    for (int q = 0; q < np; ++q) heap.push({0.0, q});
+    std::vector<std::vector<int32_t>> per(np);
+    for (const T& t : tiles) {
+      Q top = heap.top();
+      heap.pop();
+      per[top.second].push_back(t.code);
+      heap.push({top.first + t.cost, top.second});
+    }
+    std::vector<int32_t> host(np + 1 + tiles.size());
+    int32_t acc = 0;
+    for (int q = 0; q < np; ++q) {
+      host[q] = acc;
+      acc += (int32_t)per[q].size();
+    }
+    host[np] = acc;
+    size_t w = np + 1;
+    for (int q = 0; q < np; ++q)
+      for (int32_t code : per[q]) host[w++] = code;
+    SchedEntry e;
+    e.num_pairs = np;
+    MST_CUDA(cudaMalloc(&e.dev, host.size() * sizeof(int32_t)));
+    MST_CUDA(cudaMemcpy(e.dev, host.data(), host.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    it = c->sched_cache.emplace(key, e).first;
+  }
+  *off = it->second.dev;
+  *sched = it->second.dev + c->num_pairs + 1;
+  return MST_OK;
+}
+
+int launch(mst_ctx* c, cudaStream_t st, Launch& L) {
+  GemmParams& p = L.p;
+  if (L.acc_cols > mst::kTmemCols) return fail(MST_ERR_INTERNAL, "accumulator needs %d TMEM columns", L.acc_cols);
+  int tiles = 0;
+  for (int i = 0; i < p.num_problems; ++i) tiles += p.prob[i].m_tiles * p.prob[i].n_tiles;
+  if (tiles == 0) return MST_OK;
+  if (L.acc_cols <= 256) {
+    p.acc_stages = 2;
+    p.acc_stride = 256;
+  } else {
+    p.acc_stages = 1;
+    p.acc_stride = 0;
+  }
+  MST_TRY(get_schedule(c, p, &p.sched, &p.sched_off));
+  cudaLaunchConfig_t cfg;
+  std::memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3(2 * c->num_pairs);
+  cfg.blockDim = dim3(mst::kThreads);
+  cfg.dynamicSmemBytes = mst::kSmemBytes;
+  cfg.stream = st;
+  MST_CUDA(cudaLaunchKernelEx(&cfg, mst::mst_grouped_gemm_kernel, p));
+  c->launches++;
+  return MST_OK;
+}
+
+// ------------------------------------------------------------ small kernels
+// Combine the per-128-column softmax partials of one row into lse and the
+// row loss (loss = lse - z_label for non-ignored rows).
+__global__ void ce_combine_kernel(const float2* __restrict__ part, int nparts, const float* __restrict__ ztarget,
+                                  const int32_t* __restrict__ labels, int rows, int vocab, float* __restrict__ lse,
+                                  float* __restrict__ loss_row, float* __restrict__ bad) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const float2* pr = part + static_cast<int64_t>(warp) * nparts;
+  float m = -INFINITY;
+  for (int j = lane; j < nparts; j += 32) m = fmaxf(m, pr[j].x);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffff, m, o));
+  float s = 0.f;
+  for (int j = lane; j < nparts; j += 32) s += pr[j].y * exp2f(pr[j].x - m);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffff, s, o);
+  if (lane == 0) {
+    const float l2 = m + log2f(s);
+    lse[warp] = l2 * 0.69314718055994531f;
+    const int lab = labels[warp];
+    const bool valid = lab >= 0 && lab < vocab;
+    if (lab != -100 && !valid) atomicAdd(bad, 1.0f);
+    loss_row[warp] = valid ? l2 * 0.69314718055994531f - ztarget[warp] : 0.0f;
+  }
+}
+
+// Per-chunk (loss_sum, valid) with a fixed-order block reduction
+// (deterministic; SPEC.md:90 bitwise reruns).
+__global__ void chunk_reduce_kernel(const float* __restrict__ loss_row, const int32_t* __restrict__ labels, int rows,
+                                    int vocab, float* __restrict__ out_sum, float* __restrict__ out_valid) {
+  __shared__ float ss[32], sv[32];
+  float s = 0.f, v = 0.f;
+  for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+    s += loss_row[r];
+    const int lab = labels[r];
+    v += (lab >= 0 && lab < vocab) ? 1.f : 0.f;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffff, s, o);
+    v += __shfl_xor_sync(0xffffffff, v, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    ss[threadIdx.x >> 5] = s;
+    sv[threadIdx.x >> 5] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float a = 0.f, b = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      a += ss[w];
+      b += sv[w];
+    }
+    *out_sum = a;
+    *out_valid = b;
+  }
+}
+
+// stats[0..3] from the per-chunk entries (SPEC.md:316-317 loss modes).
+__global__ void finalize_loss_kernel(float* stats, int m, int mode) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s = 0, v = 0, pm = 0;
+  int nonempty = 0;
+  for (int c = 0; c < m; ++c) {
+    const double cs = stats[4 + c], cv = stats[4 + m + c];
+    s += cs;
+    v += cv;
+    if (cv > 0) {
+      pm += cs / cv;
+      ++nonempty;
+    }
+  }
+  stats[0] = (float)s;
+  stats[1] = (float)v;
+  stats[2] = mode == MST_LOSS_PAPER_MEAN ? (float)(pm / m) : (float)(s / v);
+}
+
+// Per-chunk dlogits scale: grad_loss / valid_global (token-weighted) or
+// grad_loss / (M * valid_chunk) (paper-mean).
+__global__ void grad_scale_kernel(const float* global_stats, const float* local_stats, int m, int mode,
+                                  float grad_loss, float* scales) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= m) return;
+  float sc;
+  if (mode == MST_LOSS_PAPER_MEAN) {
+    const float cv = local_stats[4 + m + c];
+    sc = cv > 0 ? grad_loss / (float(m) * cv) : 0.f;
+  } else {
+    const float gv = global_stats[1];
+    sc = gv > 0 ? grad_loss / gv : 0.f;
+  }
+  scales[c] = sc;
+}
+
+// ------------------------------------------------------------ validation
+int check_dims(int64_t n, int64_t h, int64_t x, int64_t m, const char* xname) {
+  if (n <= 0) return fail(MST_ERR_DATA, "N must be >= 1 (SPEC.md:290), got %lld", (long long)n);
+  if (m <= 0) return fail(MST_ERR_CONFIG, "M must be >= 1, got %lld", (long long)m);
+  if (h <= 0 || x <= 0) return fail(MST_ERR_SHAPE, "extents must be positive (H=%lld %s=%lld)", (long long)h, xname, (long long)x);
+  if (h % 8 || x % 8)
+    return fail(MST_ERR_SHAPE, "H and %s must be multiples of 8 for 16-byte TMA rows (H=%lld %s=%lld)", xname,
+                (long long)h, xname, (long long)x);
+  if (n > (int64_t(1) << 30) || h > 65536 * 4 || x > (int64_t(1) << 24))
+    return fail(MST_ERR_BOUNDS, "extent too large");
+  return MST_OK;
+}
+
+std::vector<int64_t> plan_bounds(int64_t n, int64_t m) {
+  const int64_t c = std::min(n, m);
+  std::vector<int64_t> b(c + 1);
+  const int64_t q = n / c, r = n % c;
+  b[0] = 0;
+  for (int64_t i = 0; i < c; ++i) b[i + 1] = b[i] + q + (i < r ? 1 : 0);
+  return b;
+}
+
+int64_t max_chunk(int64_t n, int64_t m) { return cdiv(n, std::min(n, m)); }
+
+const char* bptr(const void* p, int64_t off_elems) { return static_cast<const char*>(p) + off_elems * 2; }
+
+// ------------------------------------------------------------ problem builders
+// K1: h = silu(X W_g) * (X W_u) for one chunk.
+int build_k1(mst_ctx* c, Launch& L, const void* x, const void* wg, const void* wu, void* h, int64_t rows, int64_t H,
+             int64_t I) {
+  ProblemDesc& P = L.p.prob[L.p.num_problems++];
+  PhaseSpec s{};
+  s.a = {x, rows, H, H, false};
+  s.b0 = {wg, I, H, I, true};
+  s.b1 = {wu, I, H, I, true};
+  s.umma_n = 256;
+  s.tmem_col = 0;
+  MST_TRY(add_phase(c, L, P, s));
+  P.m_tiles = (int)cdiv(rows, 256);
+  P.tile_n = 128;
+  P.n_tiles = (int)cdiv(I, 128);
+  P.rows = (int)rows;
+  P.cols = (int)I;
+  P.epi = mst::kEpiSwiglu;
+  P.out0 = h;
+  P.ld0 = I;
+  return MST_OK;
+}
+
+// Plain C[rows, cols] = A B with B split {0,128} over the pair; STORE_BF16 or ACC_F32.
+int build_plain(mst_ctx* c, Launch& L, const Operand& a, const Operand& b, void* out, int64_t ld_out, int epi,
+                int beta) {
+  ProblemDesc& P = L.p.prob[L.p.num_problems++];
+  PhaseSpec s{};
+  s.a = a;
+  s.b0 = b;
+  s.b1 = b;
+  s.umma_n = 256;
+  s.b_off0 = 0;
+  s.b_off1 = 128;
+  MST_TRY(add_phase(c, L, P, s));
+  P.m_tiles = (int)cdiv(a.mn, 256);
+  P.tile_n = 256;
+  P.n_tiles = (int)cdiv(b.mn, 256);
+  P.rows = (int)a.mn;
+  P.cols = (int)b.mn;
+  P.epi = epi;
+  P.beta = beta;
+  P.out0 = P.out1 = out;
+  P.ld0 = P.ld1 = ld_out;
+  P.col_off0 = 0;
+  P.col_off1 = 128;
+  return MST_OK;
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+int mst_abi_version(void) { return MST_ABI_VERSION; }
+const char* mst_last_error(void) { return g_last_error.c_str(); }
+
+int mst_ctx_create(int device, mst_ctx** out) {
+  if (!out) return fail(MST_ERR_CONFIG, "out is NULL");
+  *out = nullptr;
+  int ndev = 0;
+  MST_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(MST_ERR_CONFIG, "device %d out of range (%d devices)", device, ndev);
+  MST_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  MST_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(MST_ERR_CONFIG, "libmst is built for sm_100a (B200); device %d is sm_%d%d", device, prop.major,
+                prop.minor);
+  mst_ctx* c = new mst_ctx();
+  c->device = device;
+  c->num_sms = prop.multiProcessorCount;
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || fn == nullptr) {
+    delete c;
+    return fail(MST_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  }
+  c->encode = reinterpret_cast<EncodeTiledFn>(fn);
+  e = cudaFuncSetAttribute(mst::mst_grouped_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           mst::kSmemBytes);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(MST_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+  }
+  // Co-resident CTA pairs (persistent grid size).
+  cudaLaunchConfig_t cfg;
+  std::memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3(2 * (c->num_sms / 2));
+  cfg.blockDim = dim3(mst::kThreads);
+  cfg.dynamicSmemBytes = mst::kSmemBytes;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = 2;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  int clusters = 0;
+  e = cudaOccupancyMaxActiveClusters(&clusters, mst::mst_grouped_gemm_kernel, &cfg);
+  if (e != cudaSuccess || clusters <= 0) clusters = c->num_sms / 2;
+  c->num_pairs = std::min(clusters, c->num_sms / 2);
+  e = cudaMalloc(&c->scratch_dev, 4096);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(MST_ERR_CUDA, "cudaMalloc: %s", cudaGetErrorString(e));
+  }
+  *out = c;
+  return MST_OK;
+}
+
+void mst_ctx_destroy(mst_ctx* c) {
+  if (!c) return;
+  for (auto& kv : c->sched_cache) cudaFree(kv.second.dev);
+  cudaFree(c->scratch_dev);
+  delete c;
+}
+
+int mst_ctx_num_pairs(const mst_ctx* c) { return c ? c->num_pairs : 0; }
+int64_t mst_ctx_launch_count(const mst_ctx* c) { return c ? c->launches : 0; }
+
+int mst_make_chunk_plan(int64_t n, int64_t m, int64_t* bounds, int64_t* num_chunks) {
+  if (n <= 0) return fail(MST_ERR_DATA, "make_chunk_plan: N must be >= 1 (SPEC.md:290)");
+  if (m <= 0) return fail(MST_ERR_CONFIG, "make_chunk_plan: M must be >= 1");
+  std::vector<int64_t> b = plan_bounds(n, m);
+  if (num_chunks) *num_chunks = (int64_t)b.size() - 1;
+  if (bounds) std::memcpy(bounds, b.data(), b.size() * sizeof(int64_t));
+  return MST_OK;
+}
+
+// ---- workspace layouts (shared by size query and execution)
+static int carve_mlp(Carve& cv, int64_t n, int64_t h, int64_t i, int64_t m, void** hbuf, void** dg, void** du) {
+  (void)h;
+  const int64_t nc = max_chunk(n, m);
+  const size_t hb = size_t(nc) * i * 2;
+  // forward uses two h buffers (ping-pong across chunks); backward h,dG,dU.
+  *hbuf = cv.take(hb);
+  *dg = cv.take(hb);
+  *du = cv.take(hb);
+  return MST_OK;
+}
+
+static void carve_head(Carve& cv, int64_t n, int64_t v, int64_t m, float2** part, float** zt, float** lrow,
+                       void** dl, float** scales) {
+  const int64_t nc = max_chunk(n, m);
+  const int64_t nparts = 2 * cdiv(v, 256);
+  *part = static_cast<float2*>(cv.take(size_t(nc) * nparts * sizeof(float2)));
+  *zt = static_cast<float*>(cv.take(size_t(nc) * 4));
+  *lrow = static_cast<float*>(cv.take(size_t(nc) * 4));
+  *dl = cv.take(size_t(nc) * v * 2);
+  *scales = static_cast<float*>(cv.take(size_t(std::min(n, m)) * 4 + 64));
+}
+
+int mst_mlp_workspace(int64_t n, int64_t h, int64_t i, int64_t m, size_t* bytes) {
+  MST_TRY(check_dims(n, h, i, m, "I"));
+  Carve cv{nullptr, 0, 0, true};
+  void *a, *b, *d;
+  carve_mlp(cv, n, h, i, m, &a, &b, &d);
+  *bytes = align_up(cv.used, 256);
+  return MST_OK;
+}
+
+int mst_lmhead_workspace(int64_t n, int64_t h, int64_t v, int64_t m, size_t* bytes) {
+  MST_TRY(check_dims(n, h, v, m, "V"));
+  Carve cv{nullptr, 0, 0, true};
+  float2* part;
+  float *zt, *lr, *sc;
+  void* dl;
+  carve_head(cv, n, v, m, &part, &zt, &lr, &dl, &sc);
+  *bytes = align_up(cv.used, 256);
+  return MST_OK;
+}
+
+static size_t block_fixed_bytes(int64_t n, int64_t h) { return align_up(size_t(n) * h * 2, 256) * 2 + align_up(size_t(n) * 4, 256); }
+
+int mst_block_workspace(int64_t n, int64_t h, int64_t i, int64_t v, int64_t m_mlp, int64_t m_head, size_t* bytes) {
+  size_t a = 0, b = 0;
+  MST_TRY(mst_mlp_workspace(n, h, i, m_mlp, &a));
+  MST_TRY(mst_lmhead_workspace(n, h, v, m_head, &b));
+  *bytes = block_fixed_bytes(n, h) + 256 + std::max(a, b);
+  return MST_OK;
+}
+
+static uint64_t mlp_fp(const mst_mlp_saved* s) { return fnv1a(s, offsetof(mst_mlp_saved, fingerprint)) ^ 0x4d4c50ull; }
+static uint64_t head_fp(const mst_lmhead_saved* s) {
+  return fnv1a(s, offsetof(mst_lmhead_saved, fingerprint)) ^ 0x48454144ull;
+}
+
+int mst_mlp_forward(mst_ctx* c, void* stream, const void* x, const void* wg, const void* wu, const void* wd, void* out,
+                    int64_t n, int64_t h, int64_t i, int64_t m, void* ws, size_t ws_bytes, mst_mlp_saved* saved) {
+  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  MST_TRY(check_dims(n, h, i, m, "I"));
+  if (!x || !wg || !wu || !wd || !out) return fail(MST_ERR_CONFIG, "NULL tensor pointer");
+  size_t need = 0;
+  MST_TRY(mst_mlp_workspace(n, h, i, m, &need));
+  if (!ws || ws_bytes < need) return fail(MST_ERR_CONFIG, "workspace too small (%zu < %zu)", ws_bytes, need);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Carve cv{static_cast<char*>(ws), ws_bytes, 0, false};
+  void *hb[2], *unused;
+  carve_mlp(cv, n, h, i, m, &hb[0], &hb[1], &unused);
+  const std::vector<int64_t> b = plan_bounds(n, m);
+  const int nch = (int)b.size() - 1;
+  // Software pipeline over chunks: launch j runs K2(j-1) and K1(j) together
+  // (independent: different h buffers), so the long-K down GEMM of one chunk
+  // fills the tail of the next chunk's gate/up GEMM (Alg. 1 loop).
+  for (int j = 0; j <= nch; ++j) {
+    Launch L;
+    if (j >= 1) {
+      const int64_t r0 = b[j - 1], rows = b[j] - b[j - 1];
+      Operand a{hb[(j - 1) & 1], rows, i, i, false};
+      Operand bw{wd, h, i, h, true};
+      MST_TRY(build_plain(c, L, a, bw, const_cast<char*>(bptr(out, r0 * h)), h, mst::kEpiStoreBf16, 0));
+    }
+    if (j < nch) {
+      const int64_t r0 = b[j], rows = b[j + 1] - b[j];
+      MST_TRY(build_k1(c, L, bptr(x, r0 * h), wg, wu, hb[j & 1], rows, h, i));
+    }
+    MST_TRY(launch(c, st, L));
+  }
+  MST_CUDA(cudaGetLastError());
+  if (saved) {
+    saved->x = x;
+    saved->w_gate = wg;
+    saved->w_up = wu;
+    saved->w_down = wd;
+    saved->n = n;
+    saved->h = h;
+    saved->i = i;
+    saved->m = m;
+    saved->fingerprint = mlp_fp(saved);
+  }
+  return MST_OK;
+}
+
+int mst_mlp_backward(mst_ctx* c, void* stream, const void* dout, const mst_mlp_saved* s, const void* wg, const void* wu,
+                     const void* wd, void* dx, float* dwg, float* dwu, float* dwd, int accumulate, void* ws,
+                     size_t ws_bytes) {
+  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  if (!s || s->fingerprint != mlp_fp(s)) return fail(MST_ERR_STATE, "stale or corrupted MLP saved state (SPEC.md:308)");
+  if (s->w_gate != wg || s->w_up != wu || s->w_down != wd)
+    return fail(MST_ERR_STATE, "MLP saved state was produced with different weights");
+  if (!dout || !dx || !dwg || !dwu || !dwd) return fail(MST_ERR_CONFIG, "NULL tensor pointer");
+  const int64_t n = s->n, h = s->h, i = s->i, m = s->m;
+  size_t need = 0;
+  MST_TRY(mst_mlp_workspace(n, h, i, m, &need));
+  if (!ws || ws_bytes < need) return fail(MST_ERR_CONFIG, "workspace too small (%zu < %zu)", ws_bytes, need);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Carve cv{static_cast<char*>(ws), ws_bytes, 0, false};
+  void *hb, *dg, *du;
+  carve_mlp(cv, n, h, i, m, &hb, &dg, &du);
+  const std::vector<int64_t> b = plan_bounds(n, m);
+  const int nch = (int)b.size() - 1;
+  for (int j = 0; j < nch; ++j) {
+    const int64_t r0 = b[j], rows = b[j + 1] - b[j];
+    const int beta = (j > 0 || accumulate) ? 1 : 0;
+    const void* xj = bptr(s->x, r0 * h);
+    const void* doj = bptr(dout, r0 * h);
+    {  // K7: recompute G,U and dh = dO W_d^T; emit h, dG, dU.
+      Launch L;
+      ProblemDesc& P = L.p.prob[L.p.num_problems++];
+      PhaseSpec p0{};
+      p0.a = {xj, rows, h, h, false};
+      p0.b0 = {wg, i, h, i, true};
+      p0.b1 = {wu, i, h, i, true};
+      p0.umma_n = 256;
+      MST_TRY(add_phase(c, L, P, p0));
+      PhaseSpec p1{};
+      p1.a = {doj, rows, h, h, false};
+      p1.b0 = {wd, i, h, h, false};  // B[k=h, n=i] = W_d[i, h]: K-major
+      p1.b1 = p1.b0;
+      p1.umma_n = 128;
+      p1.tmem_col = 256;
+      p1.b_off0 = 0;
+      p1.b_off1 = 64;
+      MST_TRY(add_phase(c, L, P, p1));
+      P.m_tiles = (int)cdiv(rows, 256);
+      P.tile_n = 128;
+      P.n_tiles = (int)cdiv(i, 128);
+      P.rows = (int)rows;
+      P.cols = (int)i;
+      P.epi = mst::kEpiMlpBwd;
+      P.out0 = hb;
+      P.out1 = dg;
+      P.out2 = du;
+      P.ld0 = P.ld1 = P.ld2 = i;
+      MST_TRY(launch(c, st, L));
+    }
+    {  // K8 + K9 + K10 in one grouped launch (mutually independent).
+      Launch L;
+      // K9 first: its 64 long-K tiles get scheduled first by LPT anyway.
+      {
+        ProblemDesc& P = L.p.prob[L.p.num_problems++];
+        PhaseSpec q0{};
+        q0.a = {dg, rows, i, i, false};
+        q0.b0 = {wg, h, i, i, false};  // B[k=i, n=h] = W_g[h, i]: K-major
+        q0.b1 = q0.b0;
+        q0.umma_n = 256;
+        q0.b_off1 = 128;
+        MST_TRY(add_phase(c, L, P, q0));
+        PhaseSpec q1 = q0;
+        q1.a = {du, rows, i, i, false};
+        q1.b0 = {wu, h, i, i, false};
+        q1.b1 = q1.b0;
+        q1.acc_continue = true;
+        MST_TRY(add_phase(c, L, P, q1));
+        P.m_tiles = (int)cdiv(rows, 256);
+        P.tile_n = 256;
+        P.n_tiles = (int)cdiv(h, 256);
+        P.rows = (int)rows;
+        P.cols = (int)h;
+        P.epi = mst::kEpiStoreBf16;
+        P.out0 = P.out1 = const_cast<char*>(bptr(dx, r0 * h));
+        P.ld0 = P.ld1 = h;
+        P.col_off0 = 0;
+        P.col_off1 = 128;
+      }
+      // K8: dW_d[I,H] += h^T dO_j
+      MST_TRY(build_plain(c, L, Operand{hb, i, rows, i, true}, Operand{doj, h, rows, h, true}, dwd, h,
+                          mst::kEpiAccF32, beta));
+      // K10: [dW_g | dW_u][H, I] += X_j^T [dG | dU]
+      {
+        ProblemDesc& P = L.p.prob[L.p.num_problems++];
+        PhaseSpec q{};
+        q.a = {xj, h, rows, h, true};
+        q.b0 = {dg, i, rows, i, true};
+        q.b1 = {du, i, rows, i, true};
+        q.umma_n = 256;
+        MST_TRY(add_phase(c, L, P, q));
+        P.m_tiles = (int)cdiv(h, 256);
+        P.tile_n = 128;
+        P.n_tiles = (int)cdiv(i, 128);
+        P.rows = (int)h;
+        P.cols = (int)i;
+        P.epi = mst::kEpiAccF32;
+        P.beta = beta;
+        P.out0 = dwg;
+        P.out1 = dwu;
+        P.ld0 = P.ld1 = i;
+        P.col_off0 = P.col_off1 = 0;
+      }
+      MST_TRY(launch(c, st, L));
+    }
+  }
+  MST_CUDA(cudaGetLastError());
+  return MST_OK;
+}
+
+int mst_lmhead_forward(mst_ctx* c, void* stream, const void* x, const int32_t* labels, const void* wout, int64_t n,
+                       int64_t h, int64_t v, int64_t m, int loss_mode, float* stats, float* lse, void* ws,
+                       size_t ws_bytes, mst_lmhead_saved* saved) {
+  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  MST_TRY(check_dims(n, h, v, m, "V"));
+  if (loss_mode != MST_LOSS_TOKEN_WEIGHTED && loss_mode != MST_LOSS_PAPER_MEAN)
+    return fail(MST_ERR_CONFIG, "unknown loss mode %d", loss_mode);
+  if (!x || !labels || !wout || !stats || !lse) return fail(MST_ERR_CONFIG, "NULL tensor pointer");
+  size_t need = 0;
+  MST_TRY(mst_lmhead_workspace(n, h, v, m, &need));
+  if (!ws || ws_bytes < need) return fail(MST_ERR_CONFIG, "workspace too small (%zu < %zu)", ws_bytes, need);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Carve cv{static_cast<char*>(ws), ws_bytes, 0, false};
+  float2* part;
+  float *zt, *lrow, *scales;
+  void* dl;
+  carve_head(cv, n, v, m, &part, &zt, &lrow, &dl, &scales);
+  const std::vector<int64_t> b = plan_bounds(n, m);
+  const int nch = (int)b.size() - 1;
+  const int nparts = (int)(2 * cdiv(v, 256));
+  MST_CUDA(cudaMemsetAsync(stats, 0, sizeof(float) * MST_STATS_LEN(nch), st));
+  for (int j = 0; j < nch; ++j) {
+    const int64_t r0 = b[j], rows = b[j + 1] - b[j];
+    Launch L;  // K3: logits GEMM + online-softmax partials
+    MST_TRY(build_plain(c, L, Operand{bptr(x, r0 * h), rows, h, h, false}, Operand{wout, v, h, v, true}, nullptr, 0,
+                        mst::kEpiCeFwd, 0));
+    ProblemDesc& P = L.p.prob[0];
+    P.labels = labels + r0;
+    P.part = part;
+    P.ztarget = zt;
+    P.nparts = nparts;
+    MST_TRY(launch(c, st, L));
+    const int threads = 256;
+    const int blocks = (int)cdiv(rows * 32, threads);
+    ce_combine_kernel<<<blocks, threads, 0, st>>>(part, nparts, zt, labels + r0, (int)rows, (int)v, lse + r0, lrow,
+                                                   stats + 3);
+    chunk_reduce_kernel<<<1, 1024, 0, st>>>(lrow, labels + r0, (int)rows, (int)v, stats + 4 + j, stats + 4 + nch + j);
+    c->launches += 2;
+  }
+  finalize_loss_kernel<<<1, 32, 0, st>>>(stats, nch, loss_mode);
+  c->launches += 1;
+  MST_CUDA(cudaGetLastError());
+  if (saved) {
+    saved->x = x;
+    saved->labels = labels;
+    saved->w_out = wout;
+    saved->lse = lse;
+    saved->stats = stats;
+    saved->n = n;
+    saved->h = h;
+    saved->v = v;
+    saved->m = m;
+    saved->loss_mode = loss_mode;
+    saved->_pad = 0;
+    saved->fingerprint = head_fp(saved);
+  }
+  return MST_OK;
+}
+
+int mst_lmhead_backward(mst_ctx* c, void* stream, const mst_lmhead_saved* s, const void* wout,
+                        const float* global_stats, float grad_loss, void* dx, float* dwout, int accumulate, void* ws,
+                        size_t ws_bytes) {
+  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  if (!s || s->fingerprint != head_fp(s)) return fail(MST_ERR_STATE, "stale or corrupted LM-Head saved state (SPEC.md:308)");
+  if (s->w_out != wout) return fail(MST_ERR_STATE, "LM-Head saved state was produced with different weights");
+  if (!dx || !dwout) return fail(MST_ERR_CONFIG, "NULL tensor pointer");
+  const int64_t n = s->n, h = s->h, v = s->v, m = s->m;
+  size_t need = 0;
+  MST_TRY(mst_lmhead_workspace(n, h, v, m, &need));
+  if (!ws || ws_bytes < need) return fail(MST_ERR_CONFIG, "workspace too small (%zu < %zu)", ws_bytes, need);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Carve cv{static_cast<char*>(ws), ws_bytes, 0, false};
+  float2* part;
+  float *zt, *lrow, *scales;
+  void* dl;
+  carve_head(cv, n, v, m, &part, &zt, &lrow, &dl, &scales);
+  const std::vector<int64_t> b = plan_bounds(n, m);
+  const int nch = (int)b.size() - 1;
+  grad_scale_kernel<<<(nch + 255) / 256, 256, 0, st>>>(global_stats ? global_stats : s->stats, s->stats, nch,
+                                                           s->loss_mode, grad_loss, scales);
+  c->launches += 1;
+  for (int j = 0; j < nch; ++j) {
+    const int64_t r0 = b[j], rows = b[j + 1] - b[j];
+    const int beta = (j > 0 || accumulate) ? 1 : 0;
+    const void* xj = bptr(s->x, r0 * h);
+    {  // K4: recompute logits, dlogits = (softmax - onehot) * scale -> bf16
+      Launch L;
+      MST_TRY(build_plain(c, L, Operand{xj, rows, h, h, false}, Operand{wout, v, h, v, true}, dl, v,
+                          mst::kEpiCeBwd, 0));
+      ProblemDesc& P = L.p.prob[0];
+      P.labels = s->labels + r0;
+      P.lse = s->lse + r0;
+      P.scale = scales + j;
+      MST_TRY(launch(c, st, L));
+    }
+    {  // K5 (dX = dl W_out^T) + K6 (dW_out += X^T dl), grouped.
+      Launch L;
+      MST_TRY(build_plain(c, L, Operand{dl, rows, v, v, false}, Operand{wout, h, v, v, false},
+                          const_cast<char*>(bptr(dx, r0 * h)), h, mst::kEpiStoreBf16, 0));
+      MST_TRY(build_plain(c, L, Operand{xj, h, rows, h, true}, Operand{dl, v, rows, v, true}, dwout, v,
+                          mst::kEpiAccF32, beta));
+      MST_TRY(launch(c, st, L));
+    }
+  }
+  MST_CUDA(cudaGetLastError());
+  return MST_OK;
+}
+
+int mst_block_step(mst_ctx* c, void* stream, const void* x, const int32_t* labels, const void* wg, const void* wu,
+                   const void* wd, const void* wout, int64_t n, int64_t h, int64_t i, int64_t v, int64_t m_mlp,
+                   int64_t m_head, int loss_mode, float grad_loss, float* stats, void* dx, float* dwg, float* dwu,
+                   float* dwd, float* dwout, int accumulate, void* ws, size_t ws_bytes) {
+  size_t need = 0;
+  MST_TRY(mst_block_workspace(n, h, i, v, m_mlp, m_head, &need));
+  if (!ws || ws_bytes < need) return fail(MST_ERR_CONFIG, "workspace too small (%zu < %zu)", ws_bytes, need);
+  char* base = static_cast<char*>(ws);
+  const size_t ob = align_up(size_t(n) * h * 2, 256);
+  void* o = base;
+  void* dO = base + ob;
+  float* lse = reinterpret_cast<float*>(base + 2 * ob);
+  const size_t fixed = block_fixed_bytes(n, h) + 256;
+  void* rest = base + fixed;
+  const size_t rest_bytes = ws_bytes - fixed;
+  mst_mlp_saved ms;
+  mst_lmhead_saved hs;
+  MST_TRY(mst_mlp_forward(c, stream, x, wg, wu, wd, o, n, h, i, m_mlp, rest, rest_bytes, &ms));
+  MST_TRY(mst_lmhead_forward(c, stream, o, labels, wout, n, h, v, m_head, loss_mode, stats, lse, rest, rest_bytes, &hs));
+  MST_TRY(mst_lmhead_backward(c, stream, &hs, wout, stats, grad_loss, dO, dwout, accumulate, rest, rest_bytes));
+  MST_TRY(mst_mlp_backward(c, stream, dO, &ms, wg, wu, wd, dx, dwg, dwu, dwd, accumulate, rest, rest_bytes));
+  return MST_OK;
+}
+
+int mst_debug_gemm(mst_ctx* c, void* stream, const void* a, const void* b, void* out, int64_t m, int64_t n, int64_t k,
+                   int a_mn, int b_mn, int out_f32, int beta) {
+  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  if (m <= 0 || n <= 0 || k <= 0) return fail(MST_ERR_SHAPE, "extents must be positive");
+  if (m % 8 || n % 8 || k % 8) return fail(MST_ERR_SHAPE, "extents must be multiples of 8");
+  Launch L;
+  Operand oa = a_mn ? Operand{a, m, k, m, true} : Operand{a, m, k, k, false};
+  Operand ob = b_mn ? Operand{b, n, k, n, true} : Operand{b, n, k, k, false};
+  MST_TRY(build_plain(c, L, oa, ob, out, n, out_f32 ? mst::kEpiAccF32 : mst::kEpiStoreBf16, beta));
+  MST_TRY(launch(c, static_cast<cudaStream_t>(stream), L));
+  MST_CUDA(cudaGetLastError());
+  return MST_OK;
+}
+
+}  // extern "C"
