@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""Benchmark of the MsT hot path: one MLP -> LM-Head block forward+backward.
+
+Workload (BASELINE.json config 2): Llama3-8B widths H=4096, I=14336,
+V=128256, S=8192 tokens per GPU, M=8 mini-sequences for both blocks, bf16
+compute with fp32 accumulation, synthetic random-init weights and tokens.
+A "step" is the whole block fwd+bwd over S tokens: loss, dX, dW_gate,
+dW_up, dW_down, dW_out (the unit the paper times).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N>1 runs under torchrun (one process per GPU, NCCL): sequence sharding with
+S tokens per GPU (weak scaling), global token-weighted loss and SUM
+all-reduce of the weight gradients (paper_2407_15892_b200/parallel.py).
+Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "MLP+LM-Head fwd+bwd tokens/s at Llama3-8B shape; peak activation GB; max seq len"
+UNIT = "tokens/s"
+H, I, V = 4096, 14336, 128256
+
+
+def flops_per_token(h=H, i=I, v=V) -> float:
+    """Canonical executed FLOPs per token of MsT with per-chunk recompute
+    (SURVEY.md 8d): MLP 6HI fwd + 4HI recompute + 12HI bwd; head 2HV fwd +
+    2HV recompute + 4HV bwd."""
+    return 22.0 * h * i + 8.0 * h * v
+
+
+def model_flops_per_token(h=H, i=I, v=V) -> float:
+    return 18.0 * h * i + 6.0 * h * v
+
+
+def load_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return dict(tflops=d["bf16_tflops"], tflops_sustained=d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                    hbm=d["hbm_gbs"], source="measured (MEASURED_PEAKS.json)")
+    return dict(tflops=1590.0, tflops_sustained=1400.0, hbm=6650.0, source="fallback (B200_PROFILING.md)")
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clock and throttle reasons via NVML while the timed region runs."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device_index: int, interval: float = 0.02):
+        self.samples: list[int] = []
+        self.reasons: set[str] = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # pragma: no cover - NVML missing
+            self.nv = None
+        self.interval = interval
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.interval)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+
+    def summary(self) -> dict:
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------- helpers
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def emit(obj: dict) -> None:
+    print(json.dumps(obj), flush=True)
+
+
+def ncu_traffic_per_launch():
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
+    --set full capture summary (profiles/ncu_summary.json), or None."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+        return d.get("dominant_kernel", {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------------------- CPU (reference arm)
+def cpu_block(tokens: int, m: int, nthreads: int, seed: int = 0):
+    """Builds the CPU port of the block at Llama3-8B widths for `tokens` rows."""
+    import numpy as np
+    import torch
+
+    from oracle import oracle
+
+    g = torch.Generator().manual_seed(seed)
+    X = torch.randn(tokens, H, generator=g).numpy()
+    Wg = (0.02 * torch.randn(H, I, generator=g)).numpy()
+    Wu = (0.02 * torch.randn(H, I, generator=g)).numpy()
+    Wd = (0.02 * torch.randn(I, H, generator=g)).numpy()
+    Wo = (0.02 * torch.randn(H, V, generator=g)).numpy()
+    L = torch.randint(0, V, (tokens,), generator=g).to(torch.int32).numpy()
+    L[::20] = -100
+    return oracle.CpuBlock(X, L, Wg, Wu, Wd, Wo, min(m, tokens), min(m, tokens), nthreads), np
+
+
+def cpu_baseline(m: int, budget_s: float = 20.0) -> dict:
+    """The reference path (CPU port of SPEC.md:271-361, f32, sequential-K
+    matmuls, OpenMP over output rows) on all host threads, on a bounded sample
+    of the same workload (Llama3-8B widths, fewer tokens; cost per token is
+    independent of S)."""
+    from oracle import oracle
+
+    nth = oracle.host_threads()
+    probe_tokens = 16
+    blk, _ = cpu_block(probe_tokens, m, nth)
+    blk.step()  # warm (page-in)
+    t0 = time.perf_counter()
+    blk.step()
+    t_probe = time.perf_counter() - t0
+    tokens = int(max(16, min(256, probe_tokens * budget_s / max(t_probe, 1e-3))))
+    tokens = (tokens // 8) * 8
+    del blk
+    blk, _ = cpu_block(tokens, m, nth)
+    t0 = time.perf_counter()
+    loss = blk.step()
+    dt = time.perf_counter() - t0
+    return {"value": tokens / dt, "unit": UNIT, "cores": nth, "kind": "port",
+            "sample": f"{tokens} tokens (H=4096 I=14336 V=128256, M={min(m, tokens)}) fwd+bwd in {dt:.1f} s, f32, "
+                      f"oracle/mst_oracle.c orc_block_step_f32 (loss {loss:.4f})",
+            "tflops": tokens * flops_per_token() / dt / 1e12}
+
+
+def run_reference(args) -> None:
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle
+
+    nth = oracle.host_threads()
+    # size one step so the whole --steps K --warmup W run takes ~2-3 minutes
+    per_step_budget = max(3.0, min(15.0, 150.0 / max(1, args.steps + args.warmup)))
+    probe, _ = cpu_block(16, args.m_mlp, nth)
+    probe.step()
+    t0 = time.perf_counter()
+    probe.step()
+    t_probe = time.perf_counter() - t0
+    del probe
+    tokens = int(max(16, min(512, 16 * per_step_budget / max(t_probe, 1e-3)))) // 8 * 8
+    blk, _ = cpu_block(tokens, args.m_mlp, nth)
+    for _ in range(args.warmup):
+        blk.step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        blk.step()
+    dt = (time.perf_counter() - t0) / args.steps
+    value = tokens / dt
+    sample = (f"{tokens} tokens per step at Llama3-8B widths (H=4096 I=14336 V=128256), M={min(args.m_mlp, tokens)}, "
+              f"f32 CPU port of the reference path (oracle/mst_oracle.c), {nth} threads")
+    emit({"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+          "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+          "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+          "config": {"workload": "config 2 (Llama3-8B MLP+LM-Head widths), bounded CPU sample", "tokens_per_step": tokens,
+                     "M_mlp": args.m_mlp, "M_head": args.m_head, "parallelism": "cpu"},
+          "cpu_baseline": {"value": value, "unit": UNIT, "cores": nth, "kind": "port", "sample": sample},
+          "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+
+
+# --------------------------------------------------------------------------- GPU arm
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--seq", type=int, default=8192, help="tokens per GPU")
+    ap.add_argument("--m-mlp", type=int, default=8)
+    ap.add_argument("--m-head", type=int, default=8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2407_15892_b200 import miniseq as ms
+    from paper_2407_15892_b200.parallel import GpuOps, sp_block_step
+
+    world, rank, local = dist_env()
+    if world != args.gpus and rank == 0:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    S, Mm, Mh = args.seq, args.m_mlp, args.m_head
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    gw = torch.Generator(device=dev).manual_seed(42)  # identical replicated weights on every rank
+    X = torch.randn(S, H, device=dev, generator=g).bfloat16()
+    Wg = (0.02 * torch.randn(H, I, device=dev, generator=gw)).bfloat16()
+    Wu = (0.02 * torch.randn(H, I, device=dev, generator=gw)).bfloat16()
+    Wd = (0.02 * torch.randn(I, H, device=dev, generator=gw)).bfloat16()
+    Wo = (0.02 * torch.randn(H, V, device=dev, generator=gw)).bfloat16()
+    L = torch.randint(0, V, (S,), device=dev, generator=g, dtype=torch.int32)
+    L[torch.rand(S, device=dev, generator=g) < 0.05] = -100
+    mlp, head = ms.MlpWeights(Wg, Wu, Wd), ms.LmHeadWeights(Wo)
+    ctx = ms.Context.get(local)
+    grads = ms.alloc_block_grads(S, H, I, V, dev)
+    nch = min(S, Mh)
+    stats = torch.empty(ms.stats_len(nch), dtype=torch.float32, device=dev)
+    ws = torch.empty(ms.block_workspace_bytes(S, H, I, V, Mm, Mh), dtype=torch.uint8, device=dev)
+
+    if world == 1:
+        def step():
+            ms.block_step(X, L, mlp, head, Mm, Mh, grads=grads, stats=stats, workspace=ws)
+    else:
+        ops = GpuOps()
+        gtuple = (grads.W_gate, grads.W_up, grads.W_down, grads.W_out)
+
+        def step():
+            sp_block_step(ops, X, L, (Wg, Wu, Wd), Wo, Mm, Mh, gtuple)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    stream = torch.cuda.current_stream(dev)
+    torch.cuda.reset_peak_memory_stats(dev)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    peak_alloc = torch.cuda.max_memory_allocated(dev)
+
+    # ---------------- timed region (device events on the launching stream)
+    ctx.take_timing()
+    ctx.set_timing(True)
+    launches0 = ctx.launch_count
+    barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    barrier()
+    ctx.set_timing(False)
+    gemm_ms, gemm_flops, gemm_launches = ctx.take_timing()
+    launches = ctx.launch_count - launches0
+    ms_total = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t)
+    ms_step = ms_total / args.steps
+    tokens_step = S * world
+    value = tokens_step / (ms_step / 1e3)
+
+    # ---------------- end-to-end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        Xh = X.cpu().pin_memory()
+        Lh = L.cpu().pin_memory()
+        loss_h = torch.empty(1, dtype=torch.float32).pin_memory()
+
+        def step_e2e():
+            X.copy_(Xh, non_blocking=True)
+            L.copy_(Lh, non_blocking=True)
+            step()
+            loss_h.copy_(stats[2:3] if world == 1 else stats[2:3], non_blocking=True)
+
+        for _ in range(2):
+            step_e2e()
+        torch.cuda.synchronize(dev)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            step_e2e()
+        torch.cuda.synchronize(dev)
+        barrier()
+        dt = (time.perf_counter() - t0) / args.steps
+        if world > 1:
+            t = torch.tensor([dt], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t)
+        e2e = {"value": tokens_step / dt, "unit": UNIT, "h2d_bytes_per_step": Xh.numel() * 2 + Lh.numel() * 4,
+               "d2h_bytes_per_step": 4, "ms_per_step": dt * 1e3,
+               "path": "pinned host X/labels -> H2D, miniseq.block_step (C ABI mst_block_step) "
+                       "[sp_block_step + NCCL for N>1], loss D2H; wall clock with synchronize"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peaks = load_peaks()
+    achieved = gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
+    traffic = ncu_traffic_per_launch()
+    tflops_step = tokens_step / world * flops_per_token() / (ms_step / 1e3) / 1e12
+    ws_m1 = ms.block_workspace_bytes(S, H, I, V, 1, 1)
+    nc = lambda n, m: math.ceil(n / min(n, m))  # noqa: E731
+    inter = lambda mm, mh: max(3 * nc(S, mm) * I * 2, nc(S, mh) * V * 2)  # noqa: E731
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights N(0,0.02^2), X~N(0,1), 5% ignored labels)",
+        "config": {"workload": "config 2: Llama3-8B MLP+LM-Head block fwd+bwd, H=4096 I=14336 V=128256, "
+                               f"S={S} tokens/GPU, M_mlp={Mm} M_head={Mh}",
+                   "H": H, "I": I, "V": V, "seq_len": S, "global_tokens": tokens_step, "M_mlp": Mm, "M_head": Mh,
+                   "parallelism": f"sp{world}" if world > 1 else "single",
+                   "l2": "no flush: every step streams 1.4 GB of bf16 weights and 2.8 GB of fp32 dW (>> 126 MB L2)"},
+        "tflops_per_gpu": tflops_step,
+        "mfu_model_flops": tokens_step / world * model_flops_per_token() / (ms_step / 1e3) / 1e12 / peaks["tflops"],
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peaks["tflops_sustained"], "unit": "TFLOP/s",
+                     "frac": achieved / peaks["tflops_sustained"] if achieved else None, "traffic": traffic,
+                     "kernel": "mst_grouped_gemm_kernel (all GEMM launches K1..K10)",
+                     "algorithmic_flops_per_launch": gemm_flops / max(1, gemm_launches),
+                     "avg_launch_ms": gemm_ms / max(1, gemm_launches), "launches": gemm_launches,
+                     "share_of_step": gemm_ms / ms_total if ms_total > 0 else None,
+                     "peak_source": peaks["source"] + " bf16_tflops_sustained (kernel timed inside a long step)",
+                     "peak_burst": peaks["tflops"], "frac_of_burst": achieved / peaks["tflops"] if achieved else None},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "memory": {"workspace_gb": ws.numel() / 1e9, "workspace_gb_at_M1": ws_m1 / 1e9,
+                   "peak_intermediate_gb": inter(Mm, Mh) / 1e9, "peak_intermediate_gb_at_M1": inter(1, 1) / 1e9,
+                   "peak_activation_gb": (ws.numel() + S * H * 2 + stats.numel() * 4) / 1e9,
+                   "peak_activation_gb_at_M1": (ws_m1 + S * H * 2 + stats.numel() * 4) / 1e9,
+                   "device_peak_allocated_gb": peak_alloc / 1e9},
+        "e2e": e2e,
+    }
+    if e2e is None:
+        out["e2e"] = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            out["cpu_baseline"] = cpu_baseline(Mm)
+        except Exception as exc:  # pragma: no cover
+            out["cpu_baseline"] = {"value": None, "error": repr(exc)}
+    emit(out)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

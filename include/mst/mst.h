@@ -102,6 +102,15 @@ MST_API int mst_ctx_num_pairs(const mst_ctx* ctx);
 /* Kernel launches issued by this context since creation (bench evidence). */
 MST_API int64_t mst_ctx_launch_count(const mst_ctx* ctx);
 
+/* Per-launch device timing of the grouped tcgen05 GEMM kernel (the
+ * dominant kernel): when enabled, CUDA events are recorded on the launch
+ * stream around every launch.  mst_ctx_take_timing() synchronises on them
+ * and returns, for the launches since the previous call, the summed device
+ * time (ms), their algorithmic FLOPs (2*M*N*K of the valid extents) and the
+ * launch count, then resets. */
+MST_API int mst_ctx_set_timing(mst_ctx* ctx, int enable);
+MST_API int mst_ctx_take_timing(mst_ctx* ctx, double* gemm_ms, double* gemm_flops, int64_t* gemm_launches);
+
 /* make_chunk_plan(N, M) — SPEC.md:286-294.  Writes min(M,N)+1 row bounds
  * into `bounds` (capacity >= min(M,N)+1): chunk c is [bounds[c], bounds[c+1]).
  * Balanced rule: the first N mod M chunks hold ceil(N/M) rows. */

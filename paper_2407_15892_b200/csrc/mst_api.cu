@@ -103,6 +103,11 @@ struct mst_ctx {
   std::map<std::string, SchedEntry> sched_cache;
   int64_t launches = 0;
   float* scratch_dev = nullptr;  // small persistent device scratch
+  // per-launch event timing (mst_ctx_set_timing)
+  bool timing = false;
+  std::vector<cudaEvent_t> ev;  // pairs: start, end
+  std::vector<double> ev_flops;
+  size_t ev_used = 0;
 };
 
 namespace {
@@ -142,6 +147,7 @@ struct Launch {
   GemmParams p;
   int nmaps = 0;
   int acc_cols = 0;
+  double flops = 0;  // algorithmic 2*M*N*K over the valid extents
   Launch() { std::memset(&p, 0, sizeof(p)); }
 };
 
@@ -284,7 +290,22 @@ int launch(mst_ctx* c, cudaStream_t st, Launch& L) {
   cfg.blockDim = dim3(mst::kThreads);
   cfg.dynamicSmemBytes = mst::kSmemBytes;
   cfg.stream = st;
+  if (c->timing) {
+    if (c->ev_used + 2 > c->ev.size()) {
+      for (int k = 0; k < 64; ++k) {
+        cudaEvent_t e;
+        MST_CUDA(cudaEventCreate(&e));
+        c->ev.push_back(e);
+      }
+    }
+    MST_CUDA(cudaEventRecord(c->ev[c->ev_used], st));
+  }
   MST_CUDA(cudaLaunchKernelEx(&cfg, mst::mst_grouped_gemm_kernel, p));
+  if (c->timing) {
+    MST_CUDA(cudaEventRecord(c->ev[c->ev_used + 1], st));
+    c->ev_used += 2;
+    c->ev_flops.push_back(L.flops);
+  }
   c->launches++;
   return MST_OK;
 }
@@ -431,6 +452,7 @@ int build_k1(mst_ctx* c, Launch& L, const void* x, const void* wg, const void* w
   P.epi = mst::kEpiSwiglu;
   P.out0 = h;
   P.ld0 = I;
+  L.flops += 2.0 * rows * (2.0 * I) * H;
   return MST_OK;
 }
 
@@ -457,6 +479,7 @@ int build_plain(mst_ctx* c, Launch& L, const Operand& a, const Operand& b, void*
   P.ld0 = P.ld1 = ld_out;
   P.col_off0 = 0;
   P.col_off1 = 128;
+  L.flops += 2.0 * a.mn * b.mn * a.k;
   return MST_OK;
 }
 
@@ -526,8 +549,34 @@ int mst_ctx_create(int device, mst_ctx** out) {
 void mst_ctx_destroy(mst_ctx* c) {
   if (!c) return;
   for (auto& kv : c->sched_cache) cudaFree(kv.second.dev);
+  for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   cudaFree(c->scratch_dev);
   delete c;
+}
+
+int mst_ctx_set_timing(mst_ctx* c, int enable) {
+  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  c->timing = enable != 0;
+  return MST_OK;
+}
+
+int mst_ctx_take_timing(mst_ctx* c, double* ms_out, double* flops_out, int64_t* n_out) {
+  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  double ms = 0, fl = 0;
+  const int64_t n = (int64_t)(c->ev_used / 2);
+  for (int64_t k = 0; k < n; ++k) {
+    MST_CUDA(cudaEventSynchronize(c->ev[2 * k + 1]));
+    float t = 0;
+    MST_CUDA(cudaEventElapsedTime(&t, c->ev[2 * k], c->ev[2 * k + 1]));
+    ms += t;
+    fl += c->ev_flops[k];
+  }
+  c->ev_used = 0;
+  c->ev_flops.clear();
+  if (ms_out) *ms_out = ms;
+  if (flops_out) *flops_out = fl;
+  if (n_out) *n_out = n;
+  return MST_OK;
 }
 
 int mst_ctx_num_pairs(const mst_ctx* c) { return c ? c->num_pairs : 0; }
@@ -697,6 +746,7 @@ int mst_mlp_backward(mst_ctx* c, void* stream, const void* dout, const mst_mlp_s
       P.out1 = dg;
       P.out2 = du;
       P.ld0 = P.ld1 = P.ld2 = i;
+      L.flops += 2.0 * rows * (2.0 * i) * h + 2.0 * rows * i * h;
       MST_TRY(launch(c, st, L));
     }
     {  // K8 + K9 + K10 in one grouped launch (mutually independent).
@@ -727,6 +777,7 @@ int mst_mlp_backward(mst_ctx* c, void* stream, const void* dout, const mst_mlp_s
         P.ld0 = P.ld1 = h;
         P.col_off0 = 0;
         P.col_off1 = 128;
+        L.flops += 2.0 * 2.0 * rows * h * i;
       }
       // K8: dW_d[I,H] += h^T dO_j
       MST_TRY(build_plain(c, L, Operand{hb, i, rows, i, true}, Operand{doj, h, rows, h, true}, dwd, h,
@@ -751,6 +802,7 @@ int mst_mlp_backward(mst_ctx* c, void* stream, const void* dout, const mst_mlp_s
         P.out1 = dwu;
         P.ld0 = P.ld1 = i;
         P.col_off0 = P.col_off1 = 0;
+        L.flops += 2.0 * h * (2.0 * i) * rows;
       }
       MST_TRY(launch(c, st, L));
     }

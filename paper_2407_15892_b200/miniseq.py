@@ -92,6 +92,9 @@ _SIGS = {
     "mst_ctx_destroy": ([_VP], None),
     "mst_ctx_num_pairs": ([_VP], ctypes.c_int),
     "mst_ctx_launch_count": ([_VP], ctypes.c_int64),
+    "mst_ctx_set_timing": ([_VP, _I32], ctypes.c_int),
+    "mst_ctx_take_timing": ([_VP, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                             ctypes.POINTER(_I64)], ctypes.c_int),
     "mst_make_chunk_plan": ([_I64, _I64, ctypes.POINTER(_I64), ctypes.POINTER(_I64)], ctypes.c_int),
     "mst_mlp_workspace": ([_I64, _I64, _I64, _I64, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
     "mst_lmhead_workspace": ([_I64, _I64, _I64, _I64, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
@@ -149,8 +152,7 @@ class Context:
         self.lib = load_library()
         self.device = device
         h = ctypes.c_void_p()
-        with torch.cuda.device(device):
-            _check(self.lib.mst_ctx_create(device, ctypes.byref(h)))
+        _check(self.lib.mst_ctx_create(device, ctypes.byref(h)))
         self.handle = h
         self._ws: Optional[torch.Tensor] = None
 
@@ -176,6 +178,15 @@ class Context:
     @property
     def launch_count(self) -> int:
         return self.lib.mst_ctx_launch_count(self.handle)
+
+    def set_timing(self, enable: bool) -> None:
+        _check(self.lib.mst_ctx_set_timing(self.handle, int(enable)))
+
+    def take_timing(self) -> tuple[float, float, int]:
+        """(gemm device ms, algorithmic gemm FLOPs, launches) since the last call."""
+        ms_, fl, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+        _check(self.lib.mst_ctx_take_timing(self.handle, ctypes.byref(ms_), ctypes.byref(fl), ctypes.byref(n)))
+        return ms_.value, fl.value, n.value
 
 
 def _stream(t: torch.Tensor) -> int:

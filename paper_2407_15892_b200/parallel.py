@@ -1,0 +1,100 @@
+"""Sequence-parallel MsT step across ranks (SPEC.md:606-657 made real).
+
+Tokens are independent through the MLP and LM-Head blocks, so each rank owns
+a contiguous sequence shard (WorkerState) and runs the full
+mini-sequence pipeline on it.  The only cross-rank traffic is:
+
+  1. the LM-Head statistics (loss sum, valid-token count): all-reduce SUM of
+     two floats between the head forward and backward, so every rank scales
+     its dlogits by the GLOBAL valid count (token-weighted loss,
+     SPEC.md:647-648) — the per-rank gradients then already sum to the
+     P=1 gradient;
+  2. the weight gradients: all-reduce SUM.  dW_out is final after the head
+     backward and is reduced on a side stream while the MLP backward runs;
+     dW_{gate,up,down} are reduced at the end.
+
+The collective backend is whatever torch.distributed was initialised with:
+NCCL over NVLink on B200 boxes, gloo in the CPU tests.  The compute is an
+`ops` object; `GpuOps` (libmst, sm_100a) is the only product implementation.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+import torch
+import torch.distributed as dist
+
+
+def shard_rows(total: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous, balanced sequence shard of `rank` (first total % world ranks get one more row)."""
+    if total < world:
+        raise ValueError(f"cannot shard {total} rows over {world} ranks")
+    q, r = divmod(total, world)
+    start = rank * q + min(rank, r)
+    return start, start + q + (1 if rank < r else 0)
+
+
+@dataclass
+class StepResult:
+    loss: torch.Tensor       # 0-d global loss (device of the ops)
+    stats: torch.Tensor      # all-reduced stats (loss_sum, valid, ...)
+    dX: torch.Tensor
+    dW_gate: torch.Tensor
+    dW_up: torch.Tensor
+    dW_down: torch.Tensor
+    dW_out: torch.Tensor
+
+
+class GpuOps:
+    """libmst-backed compute for one rank (CUDA tensors)."""
+
+    def __init__(self):
+        from . import miniseq as ms
+
+        self.ms = ms
+
+    def mlp_forward(self, X, w, M):
+        return self.ms.miniseq_mlp_forward(X, self.ms.MlpWeights(*w), self.ms.make_chunk_plan(X.shape[0], M))
+
+    def lmhead_forward(self, O, L, Wout, M):
+        plan = self.ms.make_chunk_plan(O.shape[0], M)
+        _, saved = self.ms.miniseq_lmhead_forward(O, L, self.ms.LmHeadWeights(Wout), plan)
+        return saved.stats, saved
+
+    def lmhead_backward(self, saved, Wout, global_stats, dW_out):
+        return self.ms.miniseq_lmhead_backward(saved, self.ms.LmHeadWeights(Wout), saved.plan,
+                                               global_stats=global_stats, dW_out=dW_out)[0]
+
+    def mlp_backward(self, dO, saved, w, grads):
+        g = self.ms.MlpGrads(*grads)
+        return self.ms.miniseq_mlp_backward(dO, saved, self.ms.MlpWeights(*w), saved.plan, grads=g)[0]
+
+
+def sp_block_step(ops, X: torch.Tensor, L: torch.Tensor, w: tuple, Wout: torch.Tensor, M_mlp: int, M_head: int,
+                  grads: tuple, group=None, overlap: bool = True) -> StepResult:
+    """One sequence-parallel MLP -> LM-Head forward+backward on this rank's shard.
+
+    w = (W_gate, W_up, W_down); grads = (dW_gate, dW_up, dW_down, dW_out) buffers
+    (overwritten).  Returns global loss and SUM-reduced gradients."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    O, msaved = ops.mlp_forward(X, w, M_mlp)
+    stats, hsaved = ops.lmhead_forward(O, L, Wout, M_head)
+    gstats = stats.clone()
+    if world > 1:
+        head = gstats[:2].contiguous()
+        dist.all_reduce(head, op=dist.ReduceOp.SUM, group=group)
+        gstats[:2] = head
+    dWg, dWu, dWd, dWo = grads
+    dO = ops.lmhead_backward(hsaved, Wout, gstats, dWo)
+    work = None
+    if world > 1:
+        # The process group runs the collective on its own stream, ordered
+        # after the head backward; the MLP backward below overlaps it.
+        work = dist.all_reduce(dWo, op=dist.ReduceOp.SUM, group=group, async_op=overlap)
+    dX = ops.mlp_backward(dO, msaved, w, (dWg, dWu, dWd))
+    if world > 1:
+        for t in (dWg, dWu, dWd):
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        if work is not None:
+            work.wait()
+    loss = gstats[0] / gstats[1]
+    return StepResult(loss=loss, stats=gstats, dX=dX, dW_gate=dWg, dW_up=dWu, dW_down=dWd, dW_out=dWo)
