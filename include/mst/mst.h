@@ -110,6 +110,15 @@ MST_API int64_t mst_ctx_launch_count(const mst_ctx* ctx);
  * launch count, then resets. */
 MST_API int mst_ctx_set_timing(mst_ctx* ctx, int enable);
 MST_API int mst_ctx_take_timing(mst_ctx* ctx, double* gemm_ms, double* gemm_flops, int64_t* gemm_launches);
+/* Same, per launch: fills up to `cap` (ms, flops) records, returns the count
+ * in *n and resets. */
+MST_API int mst_ctx_take_timing_records(mst_ctx* ctx, int64_t cap, double* ms, double* flops, int64_t* n);
+
+/* Tuning builds (-DMST_PROFILE) only: device buffer of 64 x 8 uint64 counters;
+ * grouped-GEMM launch k (counted from this call) accumulates per-role
+ * barrier-wait cycles into slot k % 64 (layout in csrc/gemm.cuh).  NULL
+ * disables.  No effect in product builds. */
+MST_API int mst_ctx_set_profile_buffer(mst_ctx* ctx, void* dev_counters);
 
 /* make_chunk_plan(N, M) — SPEC.md:286-294.  Writes min(M,N)+1 row bounds
  * into `bounds` (capacity >= min(M,N)+1): chunk c is [bounds[c], bounds[c+1]).

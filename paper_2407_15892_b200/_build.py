@@ -40,16 +40,19 @@ def needs_rebuild(out: Path, inputs: list[Path]) -> bool:
     return any(p.stat().st_mtime > t for p in inputs)
 
 
-def build_lib(force: bool = False, verbose: bool = False) -> Path:
+def build_lib(force: bool = False, verbose: bool = False, out: Path | None = None,
+              defines: tuple[str, ...] = ()) -> Path:
+    """Compile libmst.so (or a tuning variant at `out` with extra -D defines)."""
     LIB_DIR.mkdir(parents=True, exist_ok=True)
-    if not force and not needs_rebuild(LIB_PATH, lib_inputs()):
-        return LIB_PATH
-    tmp = LIB_PATH.with_suffix(".so.tmp")
+    target = out or LIB_PATH
+    if not force and not defines and not needs_rebuild(target, lib_inputs()):
+        return target
+    tmp = target.with_suffix(".so.tmp")
     cmd = [
         nvcc(), *ARCH_FLAGS, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
         "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
         "-I", str(ROOT / "include"), "-I", str(CSRC),
-        "-Xptxas", "-v" if verbose else "-O3",
+        "-Xptxas", "-v" if verbose else "-O3", *[f"-D{d}" for d in defines],
         "-o", str(tmp), *map(str, lib_sources()),
     ]
     res = subprocess.run(cmd, capture_output=True, text=True)
@@ -57,8 +60,8 @@ def build_lib(force: bool = False, verbose: bool = False) -> Path:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
     if verbose:
         print(res.stderr)
-    os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

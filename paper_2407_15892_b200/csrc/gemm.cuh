@@ -1,81 +1,95 @@
 // Persistent, warp-specialised, CTA-pair (cta_group::2) tcgen05 GEMM that
 // executes a *group* of independent GEMM problems in one launch, each with a
 // fused epilogue.  This is the single compute engine behind every MsT
-// kernel K1..K10:
+// kernel:
 //
 //   K1  gate+up GEMM, SiLU(G)*U epilogue            (Alg. 1)
 //   K2  down GEMM, bf16 store                        (Alg. 1)
 //   K3  LM-Head GEMM, online-softmax CE partials     (Alg. 2)
 //   K4  LM-Head GEMM recompute, dlogits epilogue     (Alg. 4)
 //   K5  dX = dlogits * W_out^T                       (Alg. 4)
-//   K6  dW_out += X^T dlogits (fp32 accumulate)      (Alg. 4)
-//   K7  G,U,dh recompute, SwiGLU-backward epilogue   (Alg. 3)
+//   K6  dW_out += X^T dlogits (fp32, TMA reduce-add) (Alg. 4)
+//   K7a dh = dO W_down^T (fp32 store)                (Alg. 3)
+//   K7b G,U recompute, SwiGLU-backward epilogue      (Alg. 3)
 //   K8  dW_down += h^T dO                            (Alg. 3)
 //   K9  dX = dG W_g^T + dU W_u^T (two-phase K loop)  (Alg. 3)
 //   K10 dW_gate|up += X^T [dG|dU]                    (Alg. 3)
 //
 // Tile geometry: a CTA pair owns a 256-row output tile (128 rows per CTA,
-// UMMA M=256) and an N extent of up to 256 accumulator columns.  Operands
-// are staged by TMA with 128-byte swizzle, one 64-deep K block per stage.
-// Each CTA of the pair loads its own 128 rows of A and its half of B; the
-// leader CTA issues tcgen05.mma for both.  Accumulators live in TMEM
-// (512 columns, double-buffered when a tile needs <= 256 columns) so the
-// epilogue of tile i overlaps the main loop of tile i+1.
+// UMMA M=256) and up to 256 fp32 accumulator columns.  Operands are staged
+// by TMA with 128-byte swizzle, one 64-deep K block per stage.  Each CTA of
+// the pair loads its own 128 rows of A and its half of B; the leader CTA
+// issues tcgen05.mma for both.  Accumulators live in TMEM (512 columns,
+// double-buffered) so the epilogue of tile i overlaps the main loop of tile
+// i+1.  Epilogues go TMEM -> registers -> swizzled smem -> TMA store (bf16 /
+// fp32) or TMA reduce-add (fp32 weight-gradient accumulation in L2), so no
+// epilogue thread ever waits on a global store.
 //
-// Warp roles (384 threads): w0 TMA producer, w1 MMA issuer (leader only),
-// w2 TMEM allocator, w3 idle, w4..w11 epilogue (two column groups of four
-// warps; warp w reads TMEM lanes 32*(w%4) .. +31).
+// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer (leader CTA
+// only), w2 TMEM allocator, w3 idle, w4..w7 epilogue (warp w owns TMEM lanes
+// 32*(w%4) .. +31, i.e. 32 output rows, and all accumulator columns).
 #pragma once
+
+#include <cuda_bf16.h>
 
 #include "ptx.cuh"
 
 namespace mst {
 
-constexpr int kStages = 6;
+#ifndef MST_STAGES
+#define MST_STAGES 6
+#endif
+#ifndef MST_EPI_BUFS
+#define MST_EPI_BUFS 2
+#endif
+constexpr int kStages = MST_STAGES;
 constexpr int kBK = 64;                      // K elements per stage (128 B rows)
 constexpr int kABytes = 128 * kBK * 2;       // per-CTA A tile (16 KB)
 constexpr int kBBytes = 128 * kBK * 2;       // per-CTA B tile, max (16 KB)
 constexpr int kStageBytes = kABytes + kBBytes;
-constexpr int kNumEpiWarps = 8;
+constexpr int kNumEpiWarps = 4;
 constexpr int kThreads = 128 + 32 * kNumEpiWarps;
+constexpr int kEpiBufBytes = 4096;           // one 32-row x 128-byte TMA box
+constexpr int kEpiBufs = MST_EPI_BUFS;       // per epilogue warp (>= 2)
+constexpr int kEpiBytes = kNumEpiWarps * kEpiBufs * kEpiBufBytes;
 constexpr int kMaxProblems = 4;
 constexpr int kMaxMaps = 16;
 constexpr int kTmemCols = 512;
-constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
 
 enum EpiKind : int32_t {
-  kEpiStoreBf16 = 0,  // out{g}[row, col] = bf16(acc)
-  kEpiSwiglu = 1,     // h = silu(G) * U
-  kEpiMlpBwd = 2,     // h, dG, dU from G, U, dh
-  kEpiAccF32 = 3,     // out{g}[row, col] (+)= acc  (fp32)
-  kEpiCeFwd = 4,      // per-row (max, sumexp) partials + target logit
-  kEpiCeBwd = 5,      // dlogits = (softmax - onehot) * scale
+  kEpiStoreBf16 = 0,  // out{g}[row, col] = bf16(acc)                     (TMA store)
+  kEpiSwiglu = 1,     // h = silu(G) * U                                   (TMA store)
+  kEpiSwigluBwd = 2,  // h, dG, dU from G, U (TMEM) and dh (global fp32)   (3 TMA stores)
+  kEpiAccF32 = 3,     // out{g}[row, col] (+)= acc  fp32                   (TMA store / reduce-add)
+  kEpiCeFwd = 4,      // per-row (max, sumexp) partial + target logit
+  kEpiCeBwd = 5,      // dlogits = (softmax - onehot) * scale              (TMA store)
 };
 
 struct PhaseDesc {
   int32_t map_a, map_b0, map_b1;  // tensor-map indices; B map per CTA rank
   int32_t a_mn, b_mn;             // 1 = MN-major operand in smem
-  int32_t umma_n;                 // MMA N across the pair (64..256, %32 == 0)
+  int32_t umma_n;                 // MMA N across the pair (128 or 256)
   int32_t tmem_col;               // accumulator column offset for this phase
   int32_t k_blocks;               // number of 64-deep K blocks
   int32_t b_off0, b_off1;         // per-rank B column offset (added to tn*tile_n)
   int32_t acc_continue;           // 1: keep accumulating onto the previous phase
+  int32_t a_pol, b_pol;           // L2 policy of the operand loads: 0 normal, 1 evict_last, 2 evict_first
 };
 
 struct ProblemDesc {
   int32_t num_phases;
   PhaseDesc ph[2];
   int32_t m_tiles, n_tiles, tile_n;
-  int32_t rows, cols;  // valid output rows / columns (masking)
+  int32_t rows, cols;  // valid output rows / columns
   int32_t epi;
-  int32_t beta;        // kEpiAccF32: 1 = accumulate onto the existing value
+  int32_t beta;        // kEpiAccF32: 1 = reduce-add onto the existing value
   int32_t col_off0, col_off1;
   int32_t nparts;      // kEpiCeFwd: partials per row
+  int32_t map_out0, map_out1, map_out2;  // output tensor maps (TMA store boxes)
   int32_t _pad;
-  void* out0;
-  void* out1;
-  void* out2;
-  int64_t ld0, ld1, ld2;
+  int64_t ld_aux;
+  const float* aux;    // kEpiSwigluBwd: dh [rows, ld_aux] fp32
   const int32_t* labels;
   const float* lse;    // kEpiCeBwd: log-sum-exp per row (natural log)
   const float* scale;  // kEpiCeBwd: device scalar gradient scale
@@ -92,7 +106,35 @@ struct GemmParams {
   int32_t _pad;
   const int32_t* sched;      // encoded tiles (problem << 24 | tile), grouped per pair
   const int32_t* sched_off;  // [num_pairs + 1]
+  unsigned long long* prof;  // MST_PROFILE builds: per-role wait-cycle counters (else unused)
 };
+
+// Instrumentation (tuning builds only, -DMST_PROFILE): clock64 spent in
+// barrier waits, summed per role into p.prof:
+//  [0] producer waiting for free smem stages   [1] producer total cycles
+//  [2] MMA waiting for TMA data (full)          [3] MMA waiting for TMEM (tempty)
+//  [4] MMA total cycles                         [5] epilogue waiting for tfull
+//  [6] epilogue busy cycles                     [7] epilogue total cycles
+#ifdef MST_PROFILE
+#define MST_PROF_DECL unsigned long long prof_t0 = clock64(), prof_acc[3] = {0, 0, 0};
+#define MST_PROF_WAIT(idx, expr)              \
+  do {                                         \
+    const unsigned long long t_ = clock64();  \
+    expr;                                      \
+    prof_acc[idx] += clock64() - t_;           \
+  } while (0)
+#define MST_PROF_FLUSH(base, n)                                                     \
+  do {                                                                             \
+    if (p.prof) {                                                                  \
+      for (int i_ = 0; i_ < (n); ++i_) atomicAdd(p.prof + (base) + i_, prof_acc[i_]); \
+      atomicAdd(p.prof + (base) + (n), clock64() - prof_t0);                        \
+    }                                                                              \
+  } while (0)
+#else
+#define MST_PROF_DECL
+#define MST_PROF_WAIT(idx, expr) expr
+#define MST_PROF_FLUSH(base, n)
+#endif
 
 __device__ __forceinline__ void decode_tile(const GemmParams& p, int32_t code, int& prob, int& tm, int& tn) {
   prob = code >> 24;
@@ -109,47 +151,6 @@ constexpr float kLog2e = 1.4426950408889634f;
 
 __device__ __forceinline__ float sigmoid(float x) { return __frcp_rn(1.0f + __expf(-x)); }
 
-__device__ __forceinline__ void store_bf16_row32(__nv_bfloat16* dst, const float* v, int valid) {
-  if (valid >= 32 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-    uint4* d4 = reinterpret_cast<uint4*>(dst);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint4 w;
-      w.x = ptx::pack_bf16(v[8 * q + 0], v[8 * q + 1]);
-      w.y = ptx::pack_bf16(v[8 * q + 2], v[8 * q + 3]);
-      w.z = ptx::pack_bf16(v[8 * q + 4], v[8 * q + 5]);
-      w.w = ptx::pack_bf16(v[8 * q + 6], v[8 * q + 7]);
-      d4[q] = w;
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (j < valid) dst[j] = __float2bfloat16_rn(v[j]);
-  }
-}
-
-__device__ __forceinline__ void acc_f32_row32(float* dst, const float* v, int valid, int beta) {
-  if (valid >= 32 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-    float4* d4 = reinterpret_cast<float4*>(dst);
-    if (beta) {
-      float4 old[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) old[q] = d4[q];
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        d4[q] = make_float4(old[q].x + v[4 * q], old[q].y + v[4 * q + 1], old[q].z + v[4 * q + 2],
-                            old[q].w + v[4 * q + 3]);
-    } else {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) d4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (j < valid) dst[j] = beta ? dst[j] + v[j] : v[j];
-  }
-}
-
 __device__ __forceinline__ void load32(uint32_t taddr, float (&v)[32]) {
   uint32_t r[32];
   ptx::tmem_ld_32x32b_x32(taddr, r);
@@ -158,91 +159,190 @@ __device__ __forceinline__ void load32(uint32_t taddr, float (&v)[32]) {
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
 }
 
+// Per-warp staging buffers: 32 rows x 128 B, SWIZZLE_128B layout (16-byte
+// chunk j of row r lives at chunk j ^ (r & 7)), matching the output tensor
+// maps so one thread per row writes conflict-free and TMA stores a box.
+struct Stager {
+  uint8_t* base;  // kEpiBufs buffers of kEpiBufBytes, 1024-aligned
+  int lane;
+  int next;       // round-robin buffer index
+
+  __device__ __forceinline__ uint8_t* buf(int b) const { return base + b * kEpiBufBytes; }
+
+  // Claim the next buffer: the group that last read it was issued kEpiBufs
+  // groups ago, so at most kEpiBufs-1 may still be pending.
+  __device__ __forceinline__ int acquire() {
+    if (lane == 0) ptx::bulk_wait_read<kEpiBufs - 1>();
+    __syncwarp();
+    const int b = next;
+    next = next + 1 == kEpiBufs ? 0 : next + 1;
+    return b;
+  }
+  // Claim the next buffer while one claimed buffer is not yet issued: one
+  // group fewer may be pending.
+  __device__ __forceinline__ int acquire_second() {
+    if (lane == 0) ptx::bulk_wait_read<kEpiBufs - 2>();
+    __syncwarp();
+    const int b = next;
+    next = next + 1 == kEpiBufs ? 0 : next + 1;
+    return b;
+  }
+  // 8 x 16-byte chunks of this thread's row, chunk j at logical column 16*j bytes.
+  __device__ __forceinline__ void put_chunk(int b, int j, uint4 w) const {
+    *reinterpret_cast<uint4*>(buf(b) + lane * 128 + ((j ^ (lane & 7)) << 4)) = w;
+  }
+  __device__ __forceinline__ void put_f32x32(int b, const float* v) const {
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      put_chunk(b, j,
+                make_uint4(__float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]), __float_as_uint(v[4 * j + 2]),
+                           __float_as_uint(v[4 * j + 3])));
+  }
+  // 32 bf16 values into chunks [4*half, 4*half + 4) of the 128-byte row.
+  __device__ __forceinline__ void put_bf16x32(int b, int half, const float* v) const {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      put_chunk(b, 4 * half + j,
+                make_uint4(ptx::pack_bf16(v[8 * j], v[8 * j + 1]), ptx::pack_bf16(v[8 * j + 2], v[8 * j + 3]),
+                           ptx::pack_bf16(v[8 * j + 4], v[8 * j + 5]), ptx::pack_bf16(v[8 * j + 6], v[8 * j + 7])));
+  }
+  // Publish buffer b to the async proxy and store (or reduce-add) it at
+  // tensor coordinates (col, row).  One bulk group per issue.
+  __device__ __forceinline__ void issue(int b, const CUtensorMap* m, int col, int row, bool reduce) const {
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      const uint32_t src = ptx::smem_u32(buf(b));
+      if (reduce)
+        ptx::tma_reduce_add_2d(m, src, col, row);
+      else
+        ptx::tma_store_2d(m, src, col, row);
+      ptx::bulk_commit();
+    }
+  }
+};
+
 }  // namespace epi
 
-// Runs the epilogue of one tile for this thread's row.
+// Runs the epilogue of one tile for the 32 rows of this warp.
 //   taddr : TMEM address of this warp's lane quadrant at accumulator column 0
-//   g     : column group (0/1) of this epilogue warp
-__device__ __forceinline__ void run_epilogue(const ProblemDesc& P, int tm, int tn, int row, uint32_t taddr,
-                                             int g) {
+//   row0  : first output row of the warp (tile-relative rows are row0 + lane)
+__device__ __forceinline__ void run_epilogue(const GemmParams& p, const ProblemDesc& P, int tn, int row0,
+                                             uint32_t taddr, epi::Stager& st) {
+  const int lane = st.lane;
+  const int row = row0 + lane;
   const bool row_ok = row < P.rows;
   switch (P.epi) {
-    case kEpiStoreBf16:
+    case kEpiStoreBf16: {
+      const int half = P.ph[0].umma_n >> 1;
+      for (int g = 0; g < 2; ++g) {
+        const CUtensorMap* m = &p.maps[g ? P.map_out1 : P.map_out0];
+        const int col0 = tn * P.tile_n + (g ? P.col_off1 : P.col_off0);
+        for (int c = 0; c < half; c += 64) {
+          const int b = st.acquire();
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            float v[32];
+            epi::load32(taddr + g * half + c + 32 * s, v);
+            st.put_bf16x32(b, s, v);
+          }
+          st.issue(b, m, col0 + c, row0, false);
+        }
+      }
+      break;
+    }
     case kEpiAccF32: {
-      const int half = P.ph[0].umma_n >> 1;  // D columns per group
-      void* out = g ? P.out1 : P.out0;
-      const int64_t ld = g ? P.ld1 : P.ld0;
-      const int col0 = tn * P.tile_n + (g ? P.col_off1 : P.col_off0);
-      for (int c = 0; c < half; c += 32) {
-        float v[32];
-        epi::load32(taddr + g * half + c, v);
-        const int col = col0 + c;
-        const int valid = P.cols - col;
-        if (row_ok && valid > 0) {
-          if (P.epi == kEpiStoreBf16)
-            epi::store_bf16_row32(static_cast<__nv_bfloat16*>(out) + row * ld + col, v, valid);
-          else
-            epi::acc_f32_row32(static_cast<float*>(out) + row * ld + col, v, valid, P.beta);
+      const int half = P.ph[0].umma_n >> 1;
+      for (int g = 0; g < 2; ++g) {
+        const CUtensorMap* m = &p.maps[g ? P.map_out1 : P.map_out0];
+        const int col0 = tn * P.tile_n + (g ? P.col_off1 : P.col_off0);
+        for (int c = 0; c < half; c += 32) {
+          const int b = st.acquire();
+          float v[32];
+          epi::load32(taddr + g * half + c, v);
+          st.put_f32x32(b, v);
+          st.issue(b, m, col0 + c, row0, P.beta != 0);
         }
       }
       break;
     }
     case kEpiSwiglu: {
-      // D = [G (128) | U (128)], output 128 columns; group g owns 64.
-      for (int c = 0; c < 64; c += 32) {
-        float gv[32], uv[32];
-        epi::load32(taddr + 64 * g + c, gv);
-        epi::load32(taddr + 128 + 64 * g + c, uv);
-        const int col = tn * 128 + 64 * g + c;
-        const int valid = P.cols - col;
-        if (row_ok && valid > 0) {
-          float h[32];
+      // D = [G (128) | U (128)] -> h (128 columns)
+      const CUtensorMap* m = &p.maps[P.map_out0];
+      for (int c = 0; c < 128; c += 64) {
+        const int b = st.acquire();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float s = epi::sigmoid(gv[j]);
-            h[j] = (gv[j] * s) * uv[j];
-          }
-          epi::store_bf16_row32(static_cast<__nv_bfloat16*>(P.out0) + row * P.ld0 + col, h, valid);
+        for (int s = 0; s < 2; ++s) {
+          float gv[32], uv[32];
+          epi::load32(taddr + c + 32 * s, gv);
+          epi::load32(taddr + 128 + c + 32 * s, uv);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) gv[j] = (gv[j] * epi::sigmoid(gv[j])) * uv[j];
+          st.put_bf16x32(b, s, gv);
         }
+        st.issue(b, m, tn * 128 + c, row0, false);
       }
       break;
     }
-    case kEpiMlpBwd: {
-      // D = [G (128) | U (128) | dh (128)] -> h, dG, dU (128 columns).
-      for (int c = 0; c < 64; c += 32) {
-        float gv[32], uv[32], dh[32];
-        epi::load32(taddr + 64 * g + c, gv);
-        epi::load32(taddr + 128 + 64 * g + c, uv);
-        epi::load32(taddr + 256 + 64 * g + c, dh);
-        const int col = tn * 128 + 64 * g + c;
-        const int valid = P.cols - col;
-        if (row_ok && valid > 0) {
+    case kEpiSwigluBwd: {
+      // D = [G (128) | U (128)], dh from global -> h, dG, dU (128 columns).
+      // h and dG are staged per 64-column slice while dU waits in registers
+      // for the next free buffer (two staging buffers suffice).
+      for (int c = 0; c < 128; c += 64) {
+        float du_keep[2][32];
+        const int bh = st.acquire();
+        const int bg = st.acquire_second();
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          float gv[32], uv[32], dh[32];
+          epi::load32(taddr + c + 32 * s, gv);
+          epi::load32(taddr + 128 + c + 32 * s, uv);
+          const int col = tn * 128 + c + 32 * s;
+          if (row_ok && col + 32 <= P.cols) {
+            const float4* src = reinterpret_cast<const float4*>(P.aux + static_cast<int64_t>(row) * P.ld_aux + col);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 w = __ldg(src + q);
+              dh[4 * q] = w.x;
+              dh[4 * q + 1] = w.y;
+              dh[4 * q + 2] = w.z;
+              dh[4 * q + 3] = w.w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              dh[j] = (row_ok && col + j < P.cols) ? P.aux[static_cast<int64_t>(row) * P.ld_aux + col + j] : 0.f;
+          }
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
-            const float s = epi::sigmoid(gv[j]);
-            const float act = gv[j] * s;
+            const float s_ = epi::sigmoid(gv[j]);
+            const float act = gv[j] * s_;
             const float h = act * uv[j];
-            const float dgv = dh[j] * uv[j] * (s * (1.0f + gv[j] * (1.0f - s)));
-            const float duv = dh[j] * act;
+            const float dgv = dh[j] * uv[j] * (s_ * (1.0f + gv[j] * (1.0f - s_)));
+            du_keep[s][j] = dh[j] * act;
             gv[j] = h;
             uv[j] = dgv;
-            dh[j] = duv;
           }
-          epi::store_bf16_row32(static_cast<__nv_bfloat16*>(P.out0) + row * P.ld0 + col, gv, valid);
-          epi::store_bf16_row32(static_cast<__nv_bfloat16*>(P.out1) + row * P.ld1 + col, uv, valid);
-          epi::store_bf16_row32(static_cast<__nv_bfloat16*>(P.out2) + row * P.ld2 + col, dh, valid);
+          st.put_bf16x32(bh, s, gv);
+          st.put_bf16x32(bg, s, uv);
         }
+        st.issue(bh, &p.maps[P.map_out0], tn * 128 + c, row0, false);
+        st.issue(bg, &p.maps[P.map_out1], tn * 128 + c, row0, false);
+        const int bu = st.acquire();
+        st.put_bf16x32(bu, 0, du_keep[0]);
+        st.put_bf16x32(bu, 1, du_keep[1]);
+        st.issue(bu, &p.maps[P.map_out2], tn * 128 + c, row0, false);
       }
       break;
     }
     case kEpiCeFwd: {
-      // 256 logits columns; group g reduces 128 of them to one partial.
-      const int v0 = tn * 256 + 128 * g;
+      // 256 logits columns -> one (max, sumexp) partial per row and tile.
+      const int v0 = tn * 256;
       const int lab = row_ok ? P.labels[row] : -1;
       float m = -INFINITY, s = 0.0f, zt = 0.0f;
-      for (int c = 0; c < 128; c += 32) {
+      for (int c = 0; c < 256; c += 32) {
         float z[32];
-        epi::load32(taddr + 128 * g + c, z);
+        epi::load32(taddr + c, z);
         const int vb = v0 + c;
         const int valid = P.cols - vb;
         float cmax = -INFINITY;
@@ -267,29 +367,32 @@ __device__ __forceinline__ void run_epilogue(const ProblemDesc& P, int tm, int t
         }
       }
       if (row_ok) {
-        P.part[static_cast<int64_t>(row) * P.nparts + tn * 2 + g] = make_float2(m, s);
-        if (lab >= v0 && lab < v0 + 128) P.ztarget[row] = zt * 0.69314718055994531f;  // back to natural units
+        P.part[static_cast<int64_t>(row) * P.nparts + tn] = make_float2(m, s);
+        if (lab >= v0 && lab < v0 + 256) P.ztarget[row] = zt * 0.69314718055994531f;  // natural units
       }
       break;
     }
     case kEpiCeBwd: {
-      const int v0 = tn * 256 + 128 * g;
+      const int v0 = tn * 256;
       const int lab = row_ok ? P.labels[row] : -1;
       const float l2 = row_ok ? P.lse[row] * epi::kLog2e : 0.0f;
       const float sc = (row_ok && lab >= 0) ? *P.scale : 0.0f;
-      for (int c = 0; c < 128; c += 32) {
-        float z[32];
-        epi::load32(taddr + 128 * g + c, z);
-        const int vb = v0 + c;
-        const int valid = P.cols - vb;
-        if (row_ok && valid > 0) {
+      const CUtensorMap* m = &p.maps[P.map_out0];
+      for (int c = 0; c < 256; c += 64) {
+        const int b = st.acquire();
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          float z[32];
+          epi::load32(taddr + c + 32 * s, z);
+          const int vb = v0 + c + 32 * s;
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
-            const float p = ptx::ex2(z[j] * epi::kLog2e - l2);
-            z[j] = (p - (vb + j == lab ? 1.0f : 0.0f)) * sc;
+            const float pr = ptx::ex2(z[j] * epi::kLog2e - l2);
+            z[j] = (pr - (vb + j == lab ? 1.0f : 0.0f)) * sc;
           }
-          epi::store_bf16_row32(static_cast<__nv_bfloat16*>(P.out0) + row * P.ld0 + vb, z, valid);
+          st.put_bf16x32(b, s, z);
         }
+        st.issue(b, m, v0 + c, row0, false);
       }
       break;
     }
@@ -305,11 +408,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + kStages * kABytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
-  uint64_t* full = bars;                     // [kStages]   (leader's are used)
-  uint64_t* empty = bars + kStages;          // [kStages]
-  uint64_t* tfull = bars + 2 * kStages;      // [2]
-  uint64_t* tempty = bars + 2 * kStages + 2; // [2]         (leader's are used)
+  uint8_t* smem_epi = smem + kStages * kStageBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_epi + kEpiBytes);
+  uint64_t* full = bars;                      // [kStages]   (leader's are used)
+  uint64_t* empty = bars + kStages;           // [kStages]
+  uint64_t* tfull = bars + 2 * kStages;       // [2]
+  uint64_t* tempty = bars + 2 * kStages + 2;  // [2]         (leader's are used)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
 
   const uint32_t rank = ptx::cluster_ctarank();
@@ -343,9 +447,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ===================== TMA producer =====================
     if (lane == 0) {
-      const uint64_t pol_first = ptx::policy_evict_first();
+      uint64_t pols[3];
+      pols[0] = ptx::policy_evict_normal();
+      pols[1] = ptx::policy_evict_last();
+      pols[2] = ptx::policy_evict_first();
       int stage = 0;
       uint32_t phase = 0;
+      MST_PROF_DECL
       for (int it = 0; it < ntiles; ++it) {
         int prob, tm, tn;
         decode_tile(p, tiles[it], prob, tm, tn);
@@ -358,8 +466,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const CUtensorMap* ma = &p.maps[d.map_a];
           const CUtensorMap* mb = &p.maps[rank ? d.map_b1 : d.map_b0];
           const int nb = tn * P.tile_n + (rank ? d.b_off1 : d.b_off0);
+          const uint64_t pa = pols[d.a_pol], pb = pols[d.b_pol];
           for (int kb = 0; kb < d.k_blocks; ++kb) {
-            ptx::mbar_wait(ptx::smem_u32(&empty[stage]), phase ^ 1);
+            MST_PROF_WAIT(0, ptx::mbar_wait(ptx::smem_u32(&empty[stage]), phase ^ 1));
             const uint32_t fbar_local = ptx::smem_u32(&full[stage]);
             if (rank == 0) ptx::mbar_arrive_expect_tx(fbar_local, stage_tx);
             const uint32_t fbar = ptx::mapa(fbar_local, 0);
@@ -367,15 +476,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t sb = ptx::smem_u32(smem_b + stage * kBBytes);
             const int k0 = kb * kBK;
             if (!d.a_mn) {
-              ptx::tma_load_2d_cg2(ma, sa, fbar, k0, arow, pol_first);
+              ptx::tma_load_2d_cg2(ma, sa, fbar, k0, arow, pa);
             } else {
-              ptx::tma_load_2d_cg2(ma, sa, fbar, arow, k0, pol_first);
-              ptx::tma_load_2d_cg2(ma, sa + 8192, fbar, arow + 64, k0, pol_first);
+              ptx::tma_load_2d_cg2(ma, sa, fbar, arow, k0, pa);
+              ptx::tma_load_2d_cg2(ma, sa + 8192, fbar, arow + 64, k0, pa);
             }
             if (!d.b_mn) {
-              ptx::tma_load_2d_cg2(mb, sb, fbar, k0, nb, pol_first);
+              ptx::tma_load_2d_cg2(mb, sb, fbar, k0, nb, pb);
             } else {
-              for (int j = 0; j < nh; j += 64) ptx::tma_load_2d_cg2(mb, sb + j * 128, fbar, nb + j, k0, pol_first);
+              for (int j = 0; j < nh; j += 64) ptx::tma_load_2d_cg2(mb, sb + j * 128, fbar, nb + j, k0, pb);
             }
             if (++stage == kStages) {
               stage = 0;
@@ -384,6 +493,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
       }
+      MST_PROF_FLUSH(0, 1);
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA) =====================
@@ -392,20 +502,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      MST_PROF_DECL
       for (int it = 0; it < ntiles; ++it) {
         int prob, tm, tn;
         decode_tile(p, tiles[it], prob, tm, tn);
         const ProblemDesc& P = p.prob[prob];
-        ptx::mbar_wait(ptx::smem_u32(&tempty[acc]), acc_phase ^ 1);
+        MST_PROF_WAIT(1, ptx::mbar_wait(ptx::smem_u32(&tempty[acc]), acc_phase ^ 1));
         ptx::tc_fence_after();
         const uint32_t d_base = tmem_base + acc * p.acc_stride;
         for (int ph = 0; ph < P.num_phases; ++ph) {
           const PhaseDesc& d = P.ph[ph];
-          const int nh = d.umma_n >> 1;
           const uint32_t idesc = ptx::idesc_bf16(256, d.umma_n, d.a_mn, d.b_mn);
           const uint32_t d_tmem = d_base + d.tmem_col;
           for (int kb = 0; kb < d.k_blocks; ++kb) {
-            ptx::mbar_wait(ptx::smem_u32(&full[stage]), phase);
+            MST_PROF_WAIT(0, ptx::mbar_wait(ptx::smem_u32(&full[stage]), phase));
             ptx::tc_fence_after();
             const uint32_t sa = ptx::smem_u32(smem_a + stage * kABytes);
             const uint32_t sb = ptx::smem_u32(smem_b + stage * kBBytes);
@@ -415,8 +525,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               // MN-major: advance 16 k-rows (2 atoms of 8 rows = 2048 B).
               const uint64_t adesc =
                   d.a_mn ? ptx::sdesc_sw128(sa + k * 2048, 8192, 1024) : ptx::sdesc_sw128(sa + k * 32, 16, 1024);
-              const uint64_t bdesc = d.b_mn ? ptx::sdesc_sw128(sb + k * 2048, (uint32_t)nh * 0 + 8192, 1024)
-                                            : ptx::sdesc_sw128(sb + k * 32, 16, 1024);
+              const uint64_t bdesc =
+                  d.b_mn ? ptx::sdesc_sw128(sb + k * 2048, 8192, 1024) : ptx::sdesc_sw128(sb + k * 32, 16, 1024);
               const uint32_t accum = (kb > 0 || k > 0 || d.acc_continue) ? 1u : 0u;
               ptx::umma_bf16_cg2(d_tmem, adesc, bdesc, idesc, accum);
             }
@@ -426,7 +536,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               phase ^= 1;
             }
           }
-          (void)nh;
         }
         ptx::umma_commit_cg2_mc(ptx::smem_u32(&tfull[acc]), 0x3);
         if (++acc == p.acc_stages) {
@@ -434,24 +543,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           acc_phase ^= 1;
         }
       }
+      MST_PROF_FLUSH(2, 2);
     }
   } else if (warp >= 4) {
     // ===================== epilogue =====================
     const int q = warp & 3;
-    const int g = (warp - 4) >> 2;
     int acc = 0;
     uint32_t acc_phase = 0;
     const uint32_t tempty_leader0 = ptx::mapa(ptx::smem_u32(&tempty[0]), 0);
     const uint32_t tempty_leader1 = ptx::mapa(ptx::smem_u32(&tempty[1]), 0);
+    epi::Stager st{smem_epi + (warp - 4) * kEpiBufs * kEpiBufBytes, lane, 0};
+    MST_PROF_DECL
     for (int it = 0; it < ntiles; ++it) {
       int prob, tm, tn;
       decode_tile(p, tiles[it], prob, tm, tn);
       const ProblemDesc& P = p.prob[prob];
-      ptx::mbar_wait(ptx::smem_u32(&tfull[acc]), acc_phase);
+      MST_PROF_WAIT(0, ptx::mbar_wait(ptx::smem_u32(&tfull[acc]), acc_phase));
       ptx::tc_fence_after();
-      const int row = tm * 256 + static_cast<int>(rank) * 128 + q * 32 + lane;
+      const int row0 = tm * 256 + static_cast<int>(rank) * 128 + q * 32;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * p.acc_stride;
-      run_epilogue(P, tm, tn, row, taddr, g);
+      MST_PROF_WAIT(1, run_epilogue(p, P, tn, row0, taddr, st));
+      // All TMEM reads of this tile are complete (tcgen05.wait::ld); release
+      // the accumulator to the MMA warp of the pair leader.
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
@@ -460,6 +573,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         acc_phase ^= 1;
       }
     }
+    if (lane == 0) ptx::bulk_wait_all();
+    __syncwarp();
+    if (lane == 0) MST_PROF_FLUSH(5, 2);
   }
 
   ptx::tc_fence_before();

@@ -108,21 +108,26 @@ struct mst_ctx {
   std::vector<cudaEvent_t> ev;  // pairs: start, end
   std::vector<double> ev_flops;
   size_t ev_used = 0;
+  unsigned long long* prof = nullptr;
+  int64_t prof_slot = 0;
 };
 
 namespace {
 
 // ------------------------------------------------------------ tensor maps
 int tmap_2d(mst_ctx* c, CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t ld_elems,
-            uint32_t box_inner, uint32_t box_outer) {
+            uint32_t box_inner, uint32_t box_outer, bool f32 = false) {
+  const uint64_t esz = f32 ? 4 : 2;
   if ((reinterpret_cast<uintptr_t>(base) & 15) != 0)
     return fail(MST_ERR_CONFIG, "tensor base %p is not 16-byte aligned", base);
-  if ((ld_elems * 2) % 16 != 0) return fail(MST_ERR_CONFIG, "row stride %llu elems not a multiple of 8", (unsigned long long)ld_elems);
+  if ((ld_elems * esz) % 16 != 0)
+    return fail(MST_ERR_CONFIG, "row stride %llu elems is not 16-byte aligned", (unsigned long long)ld_elems);
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {ld_elems * 2};
+  cuuint64_t strides[1] = {ld_elems * esz};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = c->encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+  CUresult r = c->encode(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                         const_cast<void*>(base), dims, strides, box, es,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
@@ -161,6 +166,15 @@ int add_map(mst_ctx* c, Launch& L, const Operand& o, int box_mn) {
 
 int map_index(int encoded) { return -(encoded + 100); }
 
+// Output tensor map for the epilogue's TMA stores: 32-row x 128-byte boxes
+// (64 bf16 or 32 fp32 columns), SWIZZLE_128B.  Returns the map index via *idx.
+int add_out_map(mst_ctx* c, Launch& L, void* base, int64_t cols, int64_t rows, int64_t ld, bool f32, int32_t* idx) {
+  if (L.nmaps >= mst::kMaxMaps) return fail(MST_ERR_INTERNAL, "too many tensor maps in one launch");
+  MST_TRY(tmap_2d(c, &L.p.maps[L.nmaps], base, (uint64_t)cols, (uint64_t)rows, (uint64_t)ld, f32 ? 32 : 64, 32, f32));
+  *idx = L.nmaps++;
+  return MST_OK;
+}
+
 struct PhaseSpec {
   Operand a;
   Operand b0, b1;  // B source for CTA rank 0 / 1
@@ -193,6 +207,13 @@ int add_phase(mst_ctx* c, Launch& L, ProblemDesc& P, const PhaseSpec& s) {
   d.b_off0 = s.b_off0;
   d.b_off1 = s.b_off1;
   d.acc_continue = s.acc_continue ? 1 : 0;
+  // L2 policy: an operand small enough to stay resident while every tile of
+  // the problem re-reads it (an activation chunk) is kept (evict_last); weights
+  // and large streams use the normal policy so the CTA pairs that share a
+  // B tile at the same time still hit in L2.
+  auto pol = [](const Operand& o) { return (o.mn * o.k * 2 <= (int64_t(48) << 20)) ? 1 : 0; };
+  d.a_pol = pol(s.a);
+  d.b_pol = pol(s.b0);
   L.acc_cols = std::max(L.acc_cols, s.tmem_col + s.umma_n);
   return MST_OK;
 }
@@ -206,7 +227,7 @@ double tile_cost(const ProblemDesc& P) {
     case mst::kEpiStoreBf16: bytes = 256.0 * P.ph[0].umma_n * 2; break;
     case mst::kEpiAccF32: bytes = 256.0 * P.ph[0].umma_n * 4 * (P.beta ? 2 : 1); break;
     case mst::kEpiSwiglu: bytes = 256.0 * 128 * 2; break;
-    case mst::kEpiMlpBwd: bytes = 3 * 256.0 * 128 * 2; break;
+    case mst::kEpiSwigluBwd: bytes = 3 * 256.0 * 128 * 2 + 256.0 * 128 * 4; break;
     case mst::kEpiCeFwd: bytes = 256.0 * 16; break;
     case mst::kEpiCeBwd: bytes = 256.0 * 256 * 2; break;
   }
@@ -249,6 +270,21 @@ int get_schedule(mst_ctx* c, const GemmParams& p, const int32_t** sched, const i
       per[top.second].push_back(t.code);
       heap.push({top.first + t.cost, top.second});
     }
+    // Mixing: LPT hands the long compute-bound tiles out first, which would
+    // leave every memory-heavy (dW reduce-add) tile for the end of the
+    // launch.  On every other pair that received a tile much longer than its
+    // median, run that long tile last so DRAM traffic spreads over the launch.
+    {
+      std::map<int32_t, double> cost_of;
+      for (const T& t : tiles) cost_of[t.code] = t.cost;
+      int flip = 0;
+      for (int q = 0; q < np; ++q) {
+        std::vector<int32_t>& v = per[q];
+        if (v.size() < 3) continue;
+        const double first = cost_of[v.front()], last = cost_of[v.back()];
+        if (first > 4.0 * last && (flip++ & 1)) std::rotate(v.begin(), v.begin() + 1, v.end());
+      }
+    }
     std::vector<int32_t> host(np + 1 + tiles.size());
     int32_t acc = 0;
     for (int q = 0; q < np; ++q) {
@@ -284,6 +320,8 @@ int launch(mst_ctx* c, cudaStream_t st, Launch& L) {
     p.acc_stride = 0;
   }
   MST_TRY(get_schedule(c, p, &p.sched, &p.sched_off));
+  // profile slots: 8 counters per launch, 64 slots round robin
+  p.prof = c->prof ? c->prof + 8 * (c->prof_slot++ % 64) : nullptr;
   cudaLaunchConfig_t cfg;
   std::memset(&cfg, 0, sizeof(cfg));
   cfg.gridDim = dim3(2 * c->num_pairs);
@@ -450,8 +488,7 @@ int build_k1(mst_ctx* c, Launch& L, const void* x, const void* wg, const void* w
   P.rows = (int)rows;
   P.cols = (int)I;
   P.epi = mst::kEpiSwiglu;
-  P.out0 = h;
-  P.ld0 = I;
+  MST_TRY(add_out_map(c, L, h, I, rows, I, false, &P.map_out0));
   L.flops += 2.0 * rows * (2.0 * I) * H;
   return MST_OK;
 }
@@ -475,8 +512,10 @@ int build_plain(mst_ctx* c, Launch& L, const Operand& a, const Operand& b, void*
   P.cols = (int)b.mn;
   P.epi = epi;
   P.beta = beta;
-  P.out0 = P.out1 = out;
-  P.ld0 = P.ld1 = ld_out;
+  if (epi == mst::kEpiStoreBf16 || epi == mst::kEpiAccF32 || epi == mst::kEpiCeBwd) {
+    MST_TRY(add_out_map(c, L, out, b.mn, a.mn, ld_out, epi == mst::kEpiAccF32, &P.map_out0));
+    P.map_out1 = P.map_out0;
+  }
   P.col_off0 = 0;
   P.col_off1 = 128;
   L.flops += 2.0 * a.mn * b.mn * a.k;
@@ -579,6 +618,33 @@ int mst_ctx_take_timing(mst_ctx* c, double* ms_out, double* flops_out, int64_t* 
   return MST_OK;
 }
 
+int mst_ctx_take_timing_records(mst_ctx* c, int64_t cap, double* ms, double* flops, int64_t* n_out) {
+  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  const int64_t n = (int64_t)(c->ev_used / 2);
+  int64_t w = 0;
+  for (int64_t k = 0; k < n; ++k) {
+    MST_CUDA(cudaEventSynchronize(c->ev[2 * k + 1]));
+    float t = 0;
+    MST_CUDA(cudaEventElapsedTime(&t, c->ev[2 * k], c->ev[2 * k + 1]));
+    if (w < cap) {
+      ms[w] = t;
+      flops[w] = c->ev_flops[k];
+      ++w;
+    }
+  }
+  c->ev_used = 0;
+  c->ev_flops.clear();
+  if (n_out) *n_out = w;
+  return MST_OK;
+}
+
+int mst_ctx_set_profile_buffer(mst_ctx* c, void* dev_counters) {
+  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  c->prof = static_cast<unsigned long long*>(dev_counters);
+  c->prof_slot = 0;
+  return MST_OK;
+}
+
 int mst_ctx_num_pairs(const mst_ctx* c) { return c ? c->num_pairs : 0; }
 int64_t mst_ctx_launch_count(const mst_ctx* c) { return c ? c->launches : 0; }
 
@@ -592,21 +658,25 @@ int mst_make_chunk_plan(int64_t n, int64_t m, int64_t* bounds, int64_t* num_chun
 }
 
 // ---- workspace layouts (shared by size query and execution)
-static int carve_mlp(Carve& cv, int64_t n, int64_t h, int64_t i, int64_t m, void** hbuf, void** dg, void** du) {
+static int carve_mlp(Carve& cv, int64_t n, int64_t h, int64_t i, int64_t m, void** hbuf, void** dg, void** du,
+                     float** dh = nullptr) {
   (void)h;
   const int64_t nc = max_chunk(n, m);
   const size_t hb = size_t(nc) * i * 2;
-  // forward uses two h buffers (ping-pong across chunks); backward h,dG,dU.
+  // forward uses two h buffers (ping-pong across chunks); backward h, dG,
+  // dU (bf16) and dh (fp32, exactly the accumulator values).
   *hbuf = cv.take(hb);
   *dg = cv.take(hb);
   *du = cv.take(hb);
+  float* d = static_cast<float*>(cv.take(size_t(nc) * i * 4));
+  if (dh) *dh = d;
   return MST_OK;
 }
 
 static void carve_head(Carve& cv, int64_t n, int64_t v, int64_t m, float2** part, float** zt, float** lrow,
                        void** dl, float** scales) {
   const int64_t nc = max_chunk(n, m);
-  const int64_t nparts = 2 * cdiv(v, 256);
+  const int64_t nparts = cdiv(v, 256);
   *part = static_cast<float2*>(cv.take(size_t(nc) * nparts * sizeof(float2)));
   *zt = static_cast<float*>(cv.take(size_t(nc) * 4));
   *lrow = static_cast<float*>(cv.take(size_t(nc) * 4));
@@ -710,15 +780,27 @@ int mst_mlp_backward(mst_ctx* c, void* stream, const void* dout, const mst_mlp_s
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Carve cv{static_cast<char*>(ws), ws_bytes, 0, false};
   void *hb, *dg, *du;
-  carve_mlp(cv, n, h, i, m, &hb, &dg, &du);
+  float* dhb;
+  carve_mlp(cv, n, h, i, m, &hb, &dg, &du, &dhb);
   const std::vector<int64_t> b = plan_bounds(n, m);
   const int nch = (int)b.size() - 1;
+  // K7a(j): dh = dO_j W_d^T, fp32 (B[k=h, n=i] = W_d[i, h]: K-major).
+  auto add_k7a = [&](Launch& L, int j) -> int {
+    const int64_t r0 = b[j], rows = b[j + 1] - b[j];
+    return build_plain(c, L, Operand{bptr(dout, r0 * h), rows, h, h, false}, Operand{wd, i, h, h, false}, dhb, i,
+                       mst::kEpiAccF32, 0);
+  };
+  {
+    Launch L;
+    MST_TRY(add_k7a(L, 0));
+    MST_TRY(launch(c, st, L));
+  }
   for (int j = 0; j < nch; ++j) {
     const int64_t r0 = b[j], rows = b[j + 1] - b[j];
     const int beta = (j > 0 || accumulate) ? 1 : 0;
     const void* xj = bptr(s->x, r0 * h);
     const void* doj = bptr(dout, r0 * h);
-    {  // K7: recompute G,U and dh = dO W_d^T; emit h, dG, dU.
+    {  // K7b: recompute G,U; epilogue combines with dh -> h, dG, dU (Alg. 3 lines 2-4).
       Launch L;
       ProblemDesc& P = L.p.prob[L.p.num_problems++];
       PhaseSpec p0{};
@@ -727,36 +809,27 @@ int mst_mlp_backward(mst_ctx* c, void* stream, const void* dout, const mst_mlp_s
       p0.b1 = {wu, i, h, i, true};
       p0.umma_n = 256;
       MST_TRY(add_phase(c, L, P, p0));
-      PhaseSpec p1{};
-      p1.a = {doj, rows, h, h, false};
-      p1.b0 = {wd, i, h, h, false};  // B[k=h, n=i] = W_d[i, h]: K-major
-      p1.b1 = p1.b0;
-      p1.umma_n = 128;
-      p1.tmem_col = 256;
-      p1.b_off0 = 0;
-      p1.b_off1 = 64;
-      MST_TRY(add_phase(c, L, P, p1));
       P.m_tiles = (int)cdiv(rows, 256);
       P.tile_n = 128;
       P.n_tiles = (int)cdiv(i, 128);
       P.rows = (int)rows;
       P.cols = (int)i;
-      P.epi = mst::kEpiMlpBwd;
-      P.out0 = hb;
-      P.out1 = dg;
-      P.out2 = du;
-      P.ld0 = P.ld1 = P.ld2 = i;
-      L.flops += 2.0 * rows * (2.0 * i) * h + 2.0 * rows * i * h;
+      P.epi = mst::kEpiSwigluBwd;
+      P.aux = dhb;
+      P.ld_aux = i;
+      MST_TRY(add_out_map(c, L, hb, i, rows, i, false, &P.map_out0));
+      MST_TRY(add_out_map(c, L, dg, i, rows, i, false, &P.map_out1));
+      MST_TRY(add_out_map(c, L, du, i, rows, i, false, &P.map_out2));
+      L.flops += 2.0 * rows * (2.0 * i) * h;
       MST_TRY(launch(c, st, L));
     }
-    {  // K8 + K9 + K10 in one grouped launch (mutually independent).
+    {  // K9 + K8 + K10 (mutually independent) + K7a of the next chunk, one launch.
       Launch L;
-      // K9 first: its 64 long-K tiles get scheduled first by LPT anyway.
-      {
+      {  // K9: dX_j = dG W_g^T + dU W_u^T (B K-major), one accumulator over both phases.
         ProblemDesc& P = L.p.prob[L.p.num_problems++];
         PhaseSpec q0{};
         q0.a = {dg, rows, i, i, false};
-        q0.b0 = {wg, h, i, i, false};  // B[k=i, n=h] = W_g[h, i]: K-major
+        q0.b0 = {wg, h, i, i, false};
         q0.b1 = q0.b0;
         q0.umma_n = 256;
         q0.b_off1 = 128;
@@ -773,8 +846,8 @@ int mst_mlp_backward(mst_ctx* c, void* stream, const void* dout, const mst_mlp_s
         P.rows = (int)rows;
         P.cols = (int)h;
         P.epi = mst::kEpiStoreBf16;
-        P.out0 = P.out1 = const_cast<char*>(bptr(dx, r0 * h));
-        P.ld0 = P.ld1 = h;
+        MST_TRY(add_out_map(c, L, const_cast<char*>(bptr(dx, r0 * h)), h, rows, h, false, &P.map_out0));
+        P.map_out1 = P.map_out0;
         P.col_off0 = 0;
         P.col_off1 = 128;
         L.flops += 2.0 * 2.0 * rows * h * i;
@@ -782,8 +855,7 @@ int mst_mlp_backward(mst_ctx* c, void* stream, const void* dout, const mst_mlp_s
       // K8: dW_d[I,H] += h^T dO_j
       MST_TRY(build_plain(c, L, Operand{hb, i, rows, i, true}, Operand{doj, h, rows, h, true}, dwd, h,
                           mst::kEpiAccF32, beta));
-      // K10: [dW_g | dW_u][H, I] += X_j^T [dG | dU]
-      {
+      {  // K10: [dW_g | dW_u][H, I] += X_j^T [dG | dU]
         ProblemDesc& P = L.p.prob[L.p.num_problems++];
         PhaseSpec q{};
         q.a = {xj, h, rows, h, true};
@@ -798,12 +870,12 @@ int mst_mlp_backward(mst_ctx* c, void* stream, const void* dout, const mst_mlp_s
         P.cols = (int)i;
         P.epi = mst::kEpiAccF32;
         P.beta = beta;
-        P.out0 = dwg;
-        P.out1 = dwu;
-        P.ld0 = P.ld1 = i;
+        MST_TRY(add_out_map(c, L, dwg, i, h, i, true, &P.map_out0));
+        MST_TRY(add_out_map(c, L, dwu, i, h, i, true, &P.map_out1));
         P.col_off0 = P.col_off1 = 0;
         L.flops += 2.0 * h * (2.0 * i) * rows;
       }
+      if (j + 1 < nch) MST_TRY(add_k7a(L, j + 1));
       MST_TRY(launch(c, st, L));
     }
   }
@@ -830,7 +902,7 @@ int mst_lmhead_forward(mst_ctx* c, void* stream, const void* x, const int32_t* l
   carve_head(cv, n, v, m, &part, &zt, &lrow, &dl, &scales);
   const std::vector<int64_t> b = plan_bounds(n, m);
   const int nch = (int)b.size() - 1;
-  const int nparts = (int)(2 * cdiv(v, 256));
+  const int nparts = (int)cdiv(v, 256);
   MST_CUDA(cudaMemsetAsync(stats, 0, sizeof(float) * MST_STATS_LEN(nch), st));
   for (int j = 0; j < nch; ++j) {
     const int64_t r0 = b[j], rows = b[j + 1] - b[j];

@@ -25,7 +25,11 @@ from typing import Optional
 
 import torch
 
-_LIB_PATH = Path(__file__).resolve().parent / "lib" / "libmst.so"
+import os
+
+# MST_LIB overrides the library path (tuning variants built by tools/); the
+# default is the in-tree product build.
+_LIB_PATH = Path(os.environ.get("MST_LIB", Path(__file__).resolve().parent / "lib" / "libmst.so"))
 
 # ----------------------------------------------------------------- errors
 class Error(RuntimeError):
@@ -95,6 +99,9 @@ _SIGS = {
     "mst_ctx_set_timing": ([_VP, _I32], ctypes.c_int),
     "mst_ctx_take_timing": ([_VP, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                              ctypes.POINTER(_I64)], ctypes.c_int),
+    "mst_ctx_set_profile_buffer": ([_VP, _VP], ctypes.c_int),
+    "mst_ctx_take_timing_records": ([_VP, _I64, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                                     ctypes.POINTER(_I64)], ctypes.c_int),
     "mst_make_chunk_plan": ([_I64, _I64, ctypes.POINTER(_I64), ctypes.POINTER(_I64)], ctypes.c_int),
     "mst_mlp_workspace": ([_I64, _I64, _I64, _I64, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
     "mst_lmhead_workspace": ([_I64, _I64, _I64, _I64, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
@@ -187,6 +194,12 @@ class Context:
         ms_, fl, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
         _check(self.lib.mst_ctx_take_timing(self.handle, ctypes.byref(ms_), ctypes.byref(fl), ctypes.byref(n)))
         return ms_.value, fl.value, n.value
+
+    def take_timing_records(self, cap: int = 4096) -> list[tuple[float, float]]:
+        """Per-launch (device ms, algorithmic FLOPs) since the last take."""
+        ms_, fl, n = (ctypes.c_double * cap)(), (ctypes.c_double * cap)(), ctypes.c_int64()
+        _check(self.lib.mst_ctx_take_timing_records(self.handle, cap, ms_, fl, ctypes.byref(n)))
+        return [(ms_[k], fl[k]) for k in range(n.value)]
 
 
 def _stream(t: torch.Tensor) -> int:
