@@ -1,0 +1,53 @@
+// Host-only smoke test of the C++ binding (include/mst/miniseq.hpp) over
+// libmst.so: chunk plans and the error mapping.  Built and run by
+// tests/test_cpp_binding.py, once standalone and once against the
+// reference's own minitrain/error.hpp when /root/reference is present.
+#include <cstdio>
+#include <typeinfo>
+
+#include "mst/miniseq.hpp"
+
+int main() {
+  int fails = 0;
+  auto expect = [&](bool ok, const char* what) {
+    if (!ok) {
+      std::printf("FAIL %s\n", what);
+      ++fails;
+    }
+  };
+  const mst::ChunkPlan p = mst::make_chunk_plan(8, 2);
+  expect(p.ranges.size() == 2 && p.ranges[0] == std::make_pair<int64_t, int64_t>(0, 4) &&
+             p.ranges[1] == std::make_pair<int64_t, int64_t>(4, 8),
+         "plan (8,2)");
+  const mst::ChunkPlan q = mst::make_chunk_plan(7, 2);
+  expect(q.ranges.size() == 2 && q.ranges[1].first == 4 && q.ranges[1].second == 7, "plan (7,2)");
+  bool threw = false;
+  try {
+    mst::make_chunk_plan(0, 4);
+  } catch (const mst::DataError&) {
+    threw = true;
+  }
+  expect(threw, "N=0 -> DataError");
+  threw = false;
+  try {
+    mst::make_chunk_plan(8, 0);
+  } catch (const mst::ConfigError&) {
+    threw = true;
+  }
+  expect(threw, "M=0 -> ConfigError");
+  threw = false;
+  try {
+    int32_t L[4] = {0, 1, 2, 3};
+    mst::mask_labels_for_chunk(L, 4, {2, 9});
+  } catch (const mst::BoundsError&) {
+    threw = true;
+  }
+  expect(threw, "bad range -> BoundsError");
+#ifdef MST_HAVE_MINITRAIN_ERRORS
+  std::printf("errors: reference minitrain::Error hierarchy\n");
+#else
+  std::printf("errors: standalone hierarchy\n");
+#endif
+  std::printf(fails ? "abi_smoke FAILED\n" : "abi_smoke OK\n");
+  return fails ? 1 : 0;
+}
