@@ -120,6 +120,14 @@ MST_API int mst_ctx_take_timing_records(mst_ctx* ctx, int64_t cap, double* ms, d
  * disables.  No effect in product builds. */
 MST_API int mst_ctx_set_profile_buffer(mst_ctx* ctx, void* dev_counters);
 
+/* Tuning knobs (benchmark / A-B use; defaults are the tuned values):
+ *   "sched":   0 plain LPT (default), 1 LPT + long tile last on alternate
+ *              pairs, 2 long tile placed mid-list (static lists only);
+ *   "dynamic": 1 (default) CTA pairs pull tiles from the global LPT order
+ *              through an atomic counter; 0 static per-pair lists.
+ * Unknown keys are MST_ERR_CONFIG.  Changing a knob clears the schedule cache. */
+MST_API int mst_ctx_set_tuning(mst_ctx* ctx, const char* key, int value);
+
 /* make_chunk_plan(N, M) — SPEC.md:286-294.  Writes min(M,N)+1 row bounds
  * into `bounds` (capacity >= min(M,N)+1): chunk c is [bounds[c], bounds[c+1]).
  * Balanced rule: the first N mod M chunks hold ceil(N/M) rows. */

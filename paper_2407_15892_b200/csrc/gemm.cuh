@@ -42,6 +42,9 @@ namespace mst {
 #ifndef MST_EPI_BUFS
 #define MST_EPI_BUFS 2
 #endif
+#ifndef MST_DW_EVICT_FIRST
+#define MST_DW_EVICT_FIRST 1  // fp32 dW stores / reduce-adds stream through L2 with evict_first
+#endif
 constexpr int kStages = MST_STAGES;
 constexpr int kBK = 64;                      // K elements per stage (128 B rows)
 constexpr int kABytes = 128 * kBK * 2;       // per-CTA A tile (16 KB)
@@ -55,7 +58,7 @@ constexpr int kEpiBytes = kNumEpiWarps * kEpiBufs * kEpiBufBytes;
 constexpr int kMaxProblems = 4;
 constexpr int kMaxMaps = 16;
 constexpr int kTmemCols = 512;
-constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 512 /*barriers, tile ring*/;
 
 enum EpiKind : int32_t {
   kEpiStoreBf16 = 0,  // out{g}[row, col] = bf16(acc)                     (TMA store)
@@ -107,6 +110,62 @@ struct GemmParams {
   const int32_t* sched;      // encoded tiles (problem << 24 | tile), grouped per pair
   const int32_t* sched_off;  // [num_pairs + 1]
   unsigned long long* prof;  // MST_PROFILE builds: per-role wait-cycle counters (else unused)
+  // Dynamic scheduling (dynamic != 0): CTA pairs pull tiles from `order`
+  // (all tiles, longest first) through the atomic `tile_counter` (zeroed
+  // before the launch) instead of walking their static `sched` lists.
+  int32_t dynamic;
+  int32_t total_tiles;
+  const int32_t* order;
+  int32_t* tile_counter;
+};
+
+constexpr int kTileSlots = 4;          // tile-code ring between the pair leader's producer and all roles
+constexpr int kTileConsumers = 10;     // leader MMA + 4 leader epi warps + peer producer + 4 peer epi warps
+
+// Per-role iterator over this pair's tiles.  Static mode walks the host LPT
+// list; dynamic mode: the leader's producer claims the next tile of the
+// global LPT order with an atomic and publishes its code into a 4-slot ring
+// in both CTAs (st.shared::cluster + release.cluster arrive); every other
+// role reads the ring and releases the slot back to the leader.
+struct TileFeed {
+  const int32_t* list;
+  int n, it;
+  int32_t* codes;      // smem ring [kTileSlots]
+  uint64_t* full;      // [kTileSlots] per CTA, count 1
+  uint64_t* empty;     // [kTileSlots] leader's, count kTileConsumers
+  int slot;
+  uint32_t phase;
+
+  // Leader producer (dynamic) / any role (static).
+  __device__ __forceinline__ int32_t produce(const GemmParams& p) {
+    if (!p.dynamic) return it < n ? list[it++] : -1;
+    ptx::mbar_wait(ptx::smem_u32(&empty[slot]), phase ^ 1);
+    const int32_t t = atomicAdd(p.tile_counter, 1);
+    const int32_t code = t < p.total_tiles ? __ldg(p.order + t) : -1;
+    codes[slot] = code;
+    ptx::st_shared_cluster_u32(ptx::mapa(ptx::smem_u32(&codes[slot]), 1), static_cast<uint32_t>(code));
+    ptx::mbar_arrive_local(ptx::smem_u32(&full[slot]));
+    ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&full[slot]), 1));
+    advance();
+    return code;
+  }
+  // Every other role.  `lane0_arrives`: warp-wide consumer (all lanes call,
+  // lane 0 releases the slot); single-thread roles pass true.
+  __device__ __forceinline__ int32_t consume(const GemmParams& p, int lane) {
+    if (!p.dynamic) return it < n ? list[it++] : -1;
+    ptx::mbar_wait_cluster(ptx::smem_u32(&full[slot]), phase);
+    const int32_t code = *reinterpret_cast<volatile int32_t*>(&codes[slot]);
+    __syncwarp(__activemask());
+    if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&empty[slot]), 0));
+    advance();
+    return code;
+  }
+  __device__ __forceinline__ void advance() {
+    if (++slot == kTileSlots) {
+      slot = 0;
+      phase ^= 1;
+    }
+  }
 };
 
 // Instrumentation (tuning builds only, -DMST_PROFILE): clock64 spent in
@@ -220,6 +279,28 @@ struct Stager {
       ptx::bulk_commit();
     }
   }
+  // fp32 weight-gradient tiles: touched once per chunk, so they should not
+  // displace operands that other tiles re-read.
+  __device__ __forceinline__ void issue_dw(int b, const CUtensorMap* m, int col, int row, bool reduce) const {
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      const uint32_t src = ptx::smem_u32(buf(b));
+#if MST_DW_EVICT_FIRST
+      const uint64_t pol = ptx::policy_evict_first();
+      if (reduce)
+        ptx::tma_reduce_add_2d_hint(m, src, col, row, pol);
+      else
+        ptx::tma_store_2d_hint(m, src, col, row, pol);
+#else
+      if (reduce)
+        ptx::tma_reduce_add_2d(m, src, col, row);
+      else
+        ptx::tma_store_2d(m, src, col, row);
+#endif
+      ptx::bulk_commit();
+    }
+  }
 };
 
 }  // namespace epi
@@ -261,7 +342,7 @@ __device__ __forceinline__ void run_epilogue(const GemmParams& p, const ProblemD
           float v[32];
           epi::load32(taddr + g * half + c, v);
           st.put_f32x32(b, v);
-          st.issue(b, m, col0 + c, row0, P.beta != 0);
+          st.issue_dw(b, m, col0 + c, row0, P.beta != 0);
         }
       }
       break;
@@ -414,7 +495,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* empty = bars + kStages;           // [kStages]
   uint64_t* tfull = bars + 2 * kStages;       // [2]
   uint64_t* tempty = bars + 2 * kStages + 2;  // [2]         (leader's are used)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+  uint64_t* tile_full = bars + 2 * kStages + 4;                // [kTileSlots]
+  uint64_t* tile_empty = tile_full + kTileSlots;               // [kTileSlots] (leader's are used)
+  int32_t* tile_codes = reinterpret_cast<int32_t*>(tile_empty + kTileSlots);  // [kTileSlots]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_codes + kTileSlots);
 
   const uint32_t rank = ptx::cluster_ctarank();
   const int warp = threadIdx.x >> 5;
@@ -433,6 +517,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       ptx::mbar_init(ptx::smem_u32(&tfull[a]), 1);
       ptx::mbar_init(ptx::smem_u32(&tempty[a]), 2 * kNumEpiWarps);
     }
+    for (int k = 0; k < kTileSlots; ++k) {
+      ptx::mbar_init(ptx::smem_u32(&tile_full[k]), 1);
+      ptx::mbar_init(ptx::smem_u32(&tile_empty[k]), kTileConsumers);
+    }
     ptx::fence_mbarrier_init();
   }
   if (warp == 2) ptx::tmem_alloc_cg2(ptx::smem_u32(tmem_slot), kTmemCols);
@@ -441,8 +529,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int32_t* tiles = p.sched + p.sched_off[pair];
-  const int ntiles = p.sched_off[pair + 1] - p.sched_off[pair];
+  TileFeed feed{p.sched + p.sched_off[pair], p.sched_off[pair + 1] - p.sched_off[pair], 0, tile_codes,
+                tile_full, tile_empty, 0, 0};
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -454,9 +542,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       MST_PROF_DECL
-      for (int it = 0; it < ntiles; ++it) {
+      for (;;) {
+        const int32_t code = rank == 0 ? feed.produce(p) : feed.consume(p, 0);
+        if (code < 0) break;
         int prob, tm, tn;
-        decode_tile(p, tiles[it], prob, tm, tn);
+        decode_tile(p, code, prob, tm, tn);
         const ProblemDesc& P = p.prob[prob];
         const int arow = tm * 256 + static_cast<int>(rank) * 128;
         for (int ph = 0; ph < P.num_phases; ++ph) {
@@ -503,9 +593,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       MST_PROF_DECL
-      for (int it = 0; it < ntiles; ++it) {
+      for (;;) {
+        const int32_t code = feed.consume(p, 0);
+        if (code < 0) break;
         int prob, tm, tn;
-        decode_tile(p, tiles[it], prob, tm, tn);
+        decode_tile(p, code, prob, tm, tn);
         const ProblemDesc& P = p.prob[prob];
         MST_PROF_WAIT(1, ptx::mbar_wait(ptx::smem_u32(&tempty[acc]), acc_phase ^ 1));
         ptx::tc_fence_after();
@@ -554,9 +646,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t tempty_leader1 = ptx::mapa(ptx::smem_u32(&tempty[1]), 0);
     epi::Stager st{smem_epi + (warp - 4) * kEpiBufs * kEpiBufBytes, lane, 0};
     MST_PROF_DECL
-    for (int it = 0; it < ntiles; ++it) {
+    for (;;) {
+      const int32_t code = feed.consume(p, lane);
+      if (code < 0) break;
       int prob, tm, tn;
-      decode_tile(p, tiles[it], prob, tm, tn);
+      decode_tile(p, code, prob, tm, tn);
       const ProblemDesc& P = p.prob[prob];
       MST_PROF_WAIT(0, ptx::mbar_wait(ptx::smem_u32(&tfull[acc]), acc_phase));
       ptx::tc_fence_after();

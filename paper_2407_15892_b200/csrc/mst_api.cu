@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -91,8 +92,9 @@ struct Carve {
 }  // namespace
 
 struct SchedEntry {
-  int32_t* dev = nullptr;  // [off (pairs+1) | tiles]
+  int32_t* dev = nullptr;  // [off (pairs+1) | per-pair tiles | global LPT order]
   int32_t num_pairs = 0;
+  int32_t total = 0;
 };
 
 struct mst_ctx {
@@ -110,6 +112,8 @@ struct mst_ctx {
   size_t ev_used = 0;
   unsigned long long* prof = nullptr;
   int64_t prof_slot = 0;
+  int sched_mode = 0;  // MST_SCHED: 0 plain LPT, 1 LPT + long tile last on alternate pairs, 2 long tile mid-list
+  int dynamic = 1;     // MST_DYNAMIC: pairs pull tiles from the global LPT order (atomic counter)
 };
 
 namespace {
@@ -235,7 +239,8 @@ double tile_cost(const ProblemDesc& P) {
   return std::max(mma, epi) + 800.0;
 }
 
-int get_schedule(mst_ctx* c, const GemmParams& p, const int32_t** sched, const int32_t** off) {
+int get_schedule(mst_ctx* c, const GemmParams& p, const int32_t** sched, const int32_t** off, const int32_t** order,
+                 int32_t* total) {
   std::string key;
   for (int i = 0; i < p.num_problems; ++i) {
     const ProblemDesc& P = p.prob[i];
@@ -278,14 +283,21 @@ int get_schedule(mst_ctx* c, const GemmParams& p, const int32_t** sched, const i
       std::map<int32_t, double> cost_of;
       for (const T& t : tiles) cost_of[t.code] = t.cost;
       int flip = 0;
-      for (int q = 0; q < np; ++q) {
+      for (int q = 0; q < np && c->sched_mode != 0; ++q) {
         std::vector<int32_t>& v = per[q];
         if (v.size() < 3) continue;
         const double first = cost_of[v.front()], last = cost_of[v.back()];
-        if (first > 4.0 * last && (flip++ & 1)) std::rotate(v.begin(), v.begin() + 1, v.end());
+        if (first <= 4.0 * last) continue;
+        if (c->sched_mode == 1) {
+          if (flip++ & 1) std::rotate(v.begin(), v.begin() + 1, v.end());
+        } else {
+          // place the long tile after ~(pair rank / pairs) of the short work
+          const size_t pos = 1 + (size_t)((v.size() - 1) * (double)(flip++ % 8) / 8.0);
+          std::rotate(v.begin(), v.begin() + 1, v.begin() + pos);
+        }
       }
     }
-    std::vector<int32_t> host(np + 1 + tiles.size());
+    std::vector<int32_t> host(np + 1 + 2 * tiles.size());
     int32_t acc = 0;
     for (int q = 0; q < np; ++q) {
       host[q] = acc;
@@ -295,14 +307,18 @@ int get_schedule(mst_ctx* c, const GemmParams& p, const int32_t** sched, const i
     size_t w = np + 1;
     for (int q = 0; q < np; ++q)
       for (int32_t code : per[q]) host[w++] = code;
+    for (const T& t : tiles) host[w++] = t.code;  // global LPT order (dynamic mode)
     SchedEntry e;
     e.num_pairs = np;
+    e.total = (int32_t)tiles.size();
     MST_CUDA(cudaMalloc(&e.dev, host.size() * sizeof(int32_t)));
     MST_CUDA(cudaMemcpy(e.dev, host.data(), host.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     it = c->sched_cache.emplace(key, e).first;
   }
   *off = it->second.dev;
   *sched = it->second.dev + c->num_pairs + 1;
+  *order = *sched + it->second.total;
+  *total = it->second.total;
   return MST_OK;
 }
 
@@ -319,7 +335,10 @@ int launch(mst_ctx* c, cudaStream_t st, Launch& L) {
     p.acc_stages = 1;
     p.acc_stride = 0;
   }
-  MST_TRY(get_schedule(c, p, &p.sched, &p.sched_off));
+  MST_TRY(get_schedule(c, p, &p.sched, &p.sched_off, &p.order, &p.total_tiles));
+  p.dynamic = c->dynamic;
+  p.tile_counter = reinterpret_cast<int32_t*>(c->scratch_dev);
+  if (p.dynamic) MST_CUDA(cudaMemsetAsync(p.tile_counter, 0, sizeof(int32_t), st));
   // profile slots: 8 counters per launch, 64 slots round robin
   p.prof = c->prof ? c->prof + 8 * (c->prof_slot++ % 64) : nullptr;
   cudaLaunchConfig_t cfg;
@@ -553,6 +572,8 @@ int mst_ctx_create(int device, mst_ctx** out) {
     return fail(MST_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   }
   c->encode = reinterpret_cast<EncodeTiledFn>(fn);
+  if (const char* sm = getenv("MST_SCHED")) c->sched_mode = atoi(sm);
+  if (const char* dy = getenv("MST_DYNAMIC")) c->dynamic = atoi(dy) != 0;
   e = cudaFuncSetAttribute(mst::mst_grouped_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            mst::kSmemBytes);
   if (e != cudaSuccess) {
@@ -642,6 +663,21 @@ int mst_ctx_set_profile_buffer(mst_ctx* c, void* dev_counters) {
   if (!c) return fail(MST_ERR_STATE, "NULL context");
   c->prof = static_cast<unsigned long long*>(dev_counters);
   c->prof_slot = 0;
+  return MST_OK;
+}
+
+int mst_ctx_set_tuning(mst_ctx* c, const char* key, int value) {
+  if (!c || !key) return fail(MST_ERR_STATE, "NULL context or key");
+  if (std::strcmp(key, "sched") == 0) {
+    if (value < 0 || value > 2) return fail(MST_ERR_CONFIG, "sched must be 0..2");
+    c->sched_mode = value;
+  } else if (std::strcmp(key, "dynamic") == 0) {
+    c->dynamic = value != 0;
+  } else {
+    return fail(MST_ERR_CONFIG, "unknown tuning key '%s'", key);
+  }
+  for (auto& kv : c->sched_cache) cudaFree(kv.second.dev);
+  c->sched_cache.clear();
   return MST_OK;
 }
 

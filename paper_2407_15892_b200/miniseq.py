@@ -100,6 +100,7 @@ _SIGS = {
     "mst_ctx_take_timing": ([_VP, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                              ctypes.POINTER(_I64)], ctypes.c_int),
     "mst_ctx_set_profile_buffer": ([_VP, _VP], ctypes.c_int),
+    "mst_ctx_set_tuning": ([_VP, ctypes.c_char_p, _I32], ctypes.c_int),
     "mst_ctx_take_timing_records": ([_VP, _I64, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                                      ctypes.POINTER(_I64)], ctypes.c_int),
     "mst_make_chunk_plan": ([_I64, _I64, ctypes.POINTER(_I64), ctypes.POINTER(_I64)], ctypes.c_int),
