@@ -78,6 +78,7 @@ struct PhaseDesc {
   int32_t b_off0, b_off1;         // per-rank B column offset (added to tn*tile_n)
   int32_t acc_continue;           // 1: keep accumulating onto the previous phase
   int32_t a_pol, b_pol;           // L2 policy of the operand loads: 0 normal, 1 evict_last, 2 evict_first
+  int32_t a_3d, b_3d;             // MN-major operand described by a 3-D map: one TMA per slab
 };
 
 struct ProblemDesc {
@@ -567,12 +568,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const int k0 = kb * kBK;
             if (!d.a_mn) {
               ptx::tma_load_2d_cg2(ma, sa, fbar, k0, arow, pa);
+            } else if (d.a_3d) {
+              ptx::tma_load_3d_cg2(ma, sa, fbar, 0, k0, arow >> 6, pa);
             } else {
               ptx::tma_load_2d_cg2(ma, sa, fbar, arow, k0, pa);
               ptx::tma_load_2d_cg2(ma, sa + 8192, fbar, arow + 64, k0, pa);
             }
             if (!d.b_mn) {
               ptx::tma_load_2d_cg2(mb, sb, fbar, k0, nb, pb);
+            } else if (d.b_3d) {
+              ptx::tma_load_3d_cg2(mb, sb, fbar, 0, k0, nb >> 6, pb);
             } else {
               for (int j = 0; j < nh; j += 64) ptx::tma_load_2d_cg2(mb, sb + j * 128, fbar, nb + j, k0, pb);
             }

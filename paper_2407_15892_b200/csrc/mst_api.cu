@@ -118,6 +118,9 @@ struct mst_ctx {
 
 namespace {
 
+// MN-major operands as 3-D tensor maps (one TMA per slab); tuning knob "tma3d".
+bool c3d_enabled = true;
+
 // ------------------------------------------------------------ tensor maps
 int tmap_2d(mst_ctx* c, CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t ld_elems,
             uint32_t box_inner, uint32_t box_outer, bool f32 = false) {
@@ -137,6 +140,24 @@ int tmap_2d(mst_ctx* c, CUtensorMap* m, const void* base, uint64_t inner, uint64
   if (r != CUDA_SUCCESS)
     return fail(MST_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) dims=%llu x %llu box=%u x %u", (int)r,
                 (unsigned long long)inner, (unsigned long long)outer, box_inner, box_outer);
+  return MST_OK;
+}
+
+// MN-major operand as a 3-D map {64, K, MN/64} with strides {ld, 64 elements}:
+// one box {64, 64, nblk} fetches a 64*nblk-wide slab in the [block][k][64]
+// order the UMMA MN-major SW128 descriptor expects (LBO = 8 KB).
+int tmap_3d_mn(mst_ctx* c, CUtensorMap* m, const void* base, uint64_t mn, uint64_t k, uint64_t ld_elems,
+               uint32_t nblk) {
+  cuuint64_t dims[3] = {64, k, mn / 64};
+  cuuint64_t strides[2] = {ld_elems * 2, 128};
+  cuuint32_t box[3] = {64, 64, nblk};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = c->encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(MST_ERR_CUDA, "cuTensorMapEncodeTiled(3d) failed (%d) mn=%llu k=%llu", (int)r,
+                (unsigned long long)mn, (unsigned long long)k);
   return MST_OK;
 }
 
@@ -160,10 +181,16 @@ struct Launch {
   Launch() { std::memset(&p, 0, sizeof(p)); }
 };
 
+bool use_3d(const Operand& o, int box_mn) {
+  return o.mn_major && c3d_enabled && o.mn % 64 == 0 && box_mn % 64 == 0 && (reinterpret_cast<uintptr_t>(o.base) & 127) == 0;
+}
+
 int add_map(mst_ctx* c, Launch& L, const Operand& o, int box_mn) {
   if (L.nmaps >= mst::kMaxMaps) return fail(MST_ERR_INTERNAL, "too many tensor maps in one launch");
   CUtensorMap* m = &L.p.maps[L.nmaps];
-  int s = o.mn_major ? tmap_2d(c, m, o.base, o.mn, o.k, o.ld, 64, 64) : tmap_2d(c, m, o.base, o.k, o.mn, o.ld, 64, box_mn);
+  int s = !o.mn_major      ? tmap_2d(c, m, o.base, o.k, o.mn, o.ld, 64, box_mn)
+          : use_3d(o, box_mn) ? tmap_3d_mn(c, m, o.base, o.mn, o.k, o.ld, box_mn / 64)
+                              : tmap_2d(c, m, o.base, o.mn, o.k, o.ld, 64, 64);
   if (s != MST_OK) return s;
   return -(L.nmaps++) - 100;  // encoded index (negative to distinguish from status)
 }
@@ -205,6 +232,8 @@ int add_phase(mst_ctx* c, Launch& L, ProblemDesc& P, const PhaseSpec& s) {
   d.map_b1 = map_index(eb1);
   d.a_mn = s.a.mn_major ? 1 : 0;
   d.b_mn = s.b0.mn_major ? 1 : 0;
+  d.a_3d = use_3d(s.a, 128) ? 1 : 0;
+  d.b_3d = (use_3d(s.b0, nh) && use_3d(s.b1, nh)) ? 1 : 0;
   d.umma_n = s.umma_n;
   d.tmem_col = s.tmem_col;
   d.k_blocks = static_cast<int32_t>(cdiv(s.a.k, mst::kBK));
@@ -463,6 +492,58 @@ __global__ void grad_scale_kernel(const float* global_stats, const float* local_
   scales[c] = sc;
 }
 
+// dst[c, r] = src[r, c] for a rows x cols bf16 block (row strides ld_src /
+// ld_dst elements).  Feeds the dW GEMMs a K-major A operand (X^T, O^T, h^T):
+// MN-major A costs ~25% tensor throughput on sm_100a, a transpose of the
+// chunk costs ~0.1% of the step.  64x64 tiles, 16-byte global accesses.
+__global__ void __launch_bounds__(256) transpose_bf16_kernel(const uint16_t* __restrict__ src, int64_t ld_src,
+                                                              uint16_t* __restrict__ dst, int64_t ld_dst, int rows,
+                                                              int cols) {
+  __shared__ uint16_t tile[64][72];
+  const int r0 = blockIdx.y * 64, c0 = blockIdx.x * 64;
+  for (int i = threadIdx.x; i < 64 * 8; i += 256) {
+    const int r = i >> 3, cc = (i & 7) * 8;
+    const int gr = r0 + r, gc = c0 + cc;
+    if (gr < rows) {
+      const uint16_t* p = src + static_cast<int64_t>(gr) * ld_src + gc;
+      if (gc + 8 <= cols) {
+        const uint4 v = *reinterpret_cast<const uint4*>(p);
+        const uint16_t* e = reinterpret_cast<const uint16_t*>(&v);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) tile[r][cc + k] = e[k];
+      } else {
+        for (int k = 0; k < 8; ++k) tile[r][cc + k] = gc + k < cols ? p[k] : 0;
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 64 * 8; i += 256) {
+    const int c = i >> 3, rr = (i & 7) * 8;
+    const int gc = c0 + c, gr = r0 + rr;
+    if (gc >= cols || gr >= rows) continue;
+    uint16_t* p = dst + static_cast<int64_t>(gc) * ld_dst + gr;
+    if (gr + 8 <= rows) {
+      uint4 v;
+      uint16_t* e = reinterpret_cast<uint16_t*>(&v);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) e[k] = tile[rr + k][c];
+      *reinterpret_cast<uint4*>(p) = v;
+    } else {
+      for (int k = 0; k < 8 && gr + k < rows; ++k) p[k] = tile[rr + k][c];
+    }
+  }
+}
+
+int transpose_bf16(mst_ctx* c, cudaStream_t st, const void* src, int64_t ld_src, void* dst, int64_t ld_dst,
+                   int64_t rows, int64_t cols) {
+  dim3 grid((unsigned)cdiv(cols, 64), (unsigned)cdiv(rows, 64));
+  transpose_bf16_kernel<<<grid, 256, 0, st>>>(static_cast<const uint16_t*>(src), ld_src, static_cast<uint16_t*>(dst),
+                                               ld_dst, (int)rows, (int)cols);
+  c->launches++;
+  MST_CUDA(cudaGetLastError());
+  return MST_OK;
+}
+
 // ------------------------------------------------------------ validation
 int check_dims(int64_t n, int64_t h, int64_t x, int64_t m, const char* xname) {
   if (n <= 0) return fail(MST_ERR_DATA, "N must be >= 1 (SPEC.md:290), got %lld", (long long)n);
@@ -673,6 +754,8 @@ int mst_ctx_set_tuning(mst_ctx* c, const char* key, int value) {
     c->sched_mode = value;
   } else if (std::strcmp(key, "dynamic") == 0) {
     c->dynamic = value != 0;
+  } else if (std::strcmp(key, "tma3d") == 0) {
+    c3d_enabled = value != 0;
   } else {
     return fail(MST_ERR_CONFIG, "unknown tuning key '%s'", key);
   }
@@ -694,9 +777,12 @@ int mst_make_chunk_plan(int64_t n, int64_t m, int64_t* bounds, int64_t* num_chun
 }
 
 // ---- workspace layouts (shared by size query and execution)
+// Row stride (elements) of the transposed chunk buffers [feature, token]:
+// the chunk's token count rounded up to 16-byte rows.
+static int64_t ld_t(int64_t n, int64_t m) { return (max_chunk(n, m) + 7) / 8 * 8; }
+
 static int carve_mlp(Carve& cv, int64_t n, int64_t h, int64_t i, int64_t m, void** hbuf, void** dg, void** du,
-                     float** dh = nullptr) {
-  (void)h;
+                     float** dh = nullptr, void** xt = nullptr, void** ht = nullptr) {
   const int64_t nc = max_chunk(n, m);
   const size_t hb = size_t(nc) * i * 2;
   // forward uses two h buffers (ping-pong across chunks); backward h, dG,
@@ -706,11 +792,16 @@ static int carve_mlp(Carve& cv, int64_t n, int64_t h, int64_t i, int64_t m, void
   *du = cv.take(hb);
   float* d = static_cast<float*>(cv.take(size_t(nc) * i * 4));
   if (dh) *dh = d;
+  // X_j^T and h^T (K-major A operands of the dW GEMMs K10 / K8)
+  void* x = cv.take(size_t(h) * ld_t(n, m) * 2);
+  void* t = cv.take(size_t(i) * ld_t(n, m) * 2);
+  if (xt) *xt = x;
+  if (ht) *ht = t;
   return MST_OK;
 }
 
-static void carve_head(Carve& cv, int64_t n, int64_t v, int64_t m, float2** part, float** zt, float** lrow,
-                       void** dl, float** scales) {
+static void carve_head(Carve& cv, int64_t n, int64_t h, int64_t v, int64_t m, float2** part, float** zt,
+                       float** lrow, void** dl, float** scales, void** ot = nullptr) {
   const int64_t nc = max_chunk(n, m);
   const int64_t nparts = cdiv(v, 256);
   *part = static_cast<float2*>(cv.take(size_t(nc) * nparts * sizeof(float2)));
@@ -718,6 +809,8 @@ static void carve_head(Carve& cv, int64_t n, int64_t v, int64_t m, float2** part
   *lrow = static_cast<float*>(cv.take(size_t(nc) * 4));
   *dl = cv.take(size_t(nc) * v * 2);
   *scales = static_cast<float*>(cv.take(size_t(std::min(n, m)) * 4 + 64));
+  void* o = cv.take(size_t(h) * ld_t(n, m) * 2);  // X_j^T: K-major A operand of K6
+  if (ot) *ot = o;
 }
 
 int mst_mlp_workspace(int64_t n, int64_t h, int64_t i, int64_t m, size_t* bytes) {
@@ -735,7 +828,7 @@ int mst_lmhead_workspace(int64_t n, int64_t h, int64_t v, int64_t m, size_t* byt
   float2* part;
   float *zt, *lr, *sc;
   void* dl;
-  carve_head(cv, n, v, m, &part, &zt, &lr, &dl, &sc);
+  carve_head(cv, n, h, v, m, &part, &zt, &lr, &dl, &sc);
   *bytes = align_up(cv.used, 256);
   return MST_OK;
 }
@@ -815,9 +908,10 @@ int mst_mlp_backward(mst_ctx* c, void* stream, const void* dout, const mst_mlp_s
   if (!ws || ws_bytes < need) return fail(MST_ERR_CONFIG, "workspace too small (%zu < %zu)", ws_bytes, need);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Carve cv{static_cast<char*>(ws), ws_bytes, 0, false};
-  void *hb, *dg, *du;
+  void *hb, *dg, *du, *xt, *ht;
   float* dhb;
-  carve_mlp(cv, n, h, i, m, &hb, &dg, &du, &dhb);
+  carve_mlp(cv, n, h, i, m, &hb, &dg, &du, &dhb, &xt, &ht);
+  const int64_t ldt = ld_t(n, m);
   const std::vector<int64_t> b = plan_bounds(n, m);
   const int nch = (int)b.size() - 1;
   // K7a(j): dh = dO_j W_d^T, fp32 (B[k=h, n=i] = W_d[i, h]: K-major).
@@ -859,6 +953,9 @@ int mst_mlp_backward(mst_ctx* c, void* stream, const void* dout, const mst_mlp_s
       L.flops += 2.0 * rows * (2.0 * i) * h;
       MST_TRY(launch(c, st, L));
     }
+    // K-major A operands for the dW GEMMs: h^T (K8) and X_j^T (K10).
+    MST_TRY(transpose_bf16(c, st, hb, i, ht, ldt, rows, i));
+    MST_TRY(transpose_bf16(c, st, xj, h, xt, ldt, rows, h));
     {  // K9 + K8 + K10 (mutually independent) + K7a of the next chunk, one launch.
       Launch L;
       {  // K9: dX_j = dG W_g^T + dU W_u^T (B K-major), one accumulator over both phases.
@@ -889,12 +986,12 @@ int mst_mlp_backward(mst_ctx* c, void* stream, const void* dout, const mst_mlp_s
         L.flops += 2.0 * 2.0 * rows * h * i;
       }
       // K8: dW_d[I,H] += h^T dO_j
-      MST_TRY(build_plain(c, L, Operand{hb, i, rows, i, true}, Operand{doj, h, rows, h, true}, dwd, h,
+      MST_TRY(build_plain(c, L, Operand{ht, i, rows, ldt, false}, Operand{doj, h, rows, h, true}, dwd, h,
                           mst::kEpiAccF32, beta));
       {  // K10: [dW_g | dW_u][H, I] += X_j^T [dG | dU]
         ProblemDesc& P = L.p.prob[L.p.num_problems++];
         PhaseSpec q{};
-        q.a = {xj, h, rows, h, true};
+        q.a = {xt, h, rows, ldt, false};
         q.b0 = {dg, i, rows, i, true};
         q.b1 = {du, i, rows, i, true};
         q.umma_n = 256;
@@ -935,7 +1032,7 @@ int mst_lmhead_forward(mst_ctx* c, void* stream, const void* x, const int32_t* l
   float2* part;
   float *zt, *lrow, *scales;
   void* dl;
-  carve_head(cv, n, v, m, &part, &zt, &lrow, &dl, &scales);
+  carve_head(cv, n, h, v, m, &part, &zt, &lrow, &dl, &scales);
   const std::vector<int64_t> b = plan_bounds(n, m);
   const int nch = (int)b.size() - 1;
   const int nparts = (int)cdiv(v, 256);
@@ -993,8 +1090,9 @@ int mst_lmhead_backward(mst_ctx* c, void* stream, const mst_lmhead_saved* s, con
   Carve cv{static_cast<char*>(ws), ws_bytes, 0, false};
   float2* part;
   float *zt, *lrow, *scales;
-  void* dl;
-  carve_head(cv, n, v, m, &part, &zt, &lrow, &dl, &scales);
+  void *dl, *ot;
+  carve_head(cv, n, h, v, m, &part, &zt, &lrow, &dl, &scales, &ot);
+  const int64_t ldt = ld_t(n, m);
   const std::vector<int64_t> b = plan_bounds(n, m);
   const int nch = (int)b.size() - 1;
   grad_scale_kernel<<<(nch + 255) / 256, 256, 0, st>>>(global_stats ? global_stats : s->stats, s->stats, nch,
@@ -1004,6 +1102,7 @@ int mst_lmhead_backward(mst_ctx* c, void* stream, const mst_lmhead_saved* s, con
     const int64_t r0 = b[j], rows = b[j + 1] - b[j];
     const int beta = (j > 0 || accumulate) ? 1 : 0;
     const void* xj = bptr(s->x, r0 * h);
+    MST_TRY(transpose_bf16(c, st, xj, h, ot, ldt, rows, h));  // (head input)_j^T: K-major A of K6
     {  // K4: recompute logits, dlogits = (softmax - onehot) * scale -> bf16
       Launch L;
       MST_TRY(build_plain(c, L, Operand{xj, rows, h, h, false}, Operand{wout, v, h, v, true}, dl, v,
@@ -1018,7 +1117,7 @@ int mst_lmhead_backward(mst_ctx* c, void* stream, const mst_lmhead_saved* s, con
       Launch L;
       MST_TRY(build_plain(c, L, Operand{dl, rows, v, v, false}, Operand{wout, h, v, v, false},
                           const_cast<char*>(bptr(dx, r0 * h)), h, mst::kEpiStoreBf16, 0));
-      MST_TRY(build_plain(c, L, Operand{xj, h, rows, h, true}, Operand{dl, v, rows, v, true}, dwout, v,
+      MST_TRY(build_plain(c, L, Operand{ot, h, rows, ldt, false}, Operand{dl, v, rows, v, true}, dwout, v,
                           mst::kEpiAccF32, beta));
       MST_TRY(launch(c, st, L));
     }

@@ -134,6 +134,17 @@ __device__ __forceinline__ void tma_load_2d_cg2(const CUtensorMap* m, uint32_t d
       : "memory");
 }
 
+// 3-D variant: {64 MN elements, K rows, MN/64 blocks} lands as [block][k][64],
+// i.e. the MN-major SW128 canonical layout with LBO = one block.
+__device__ __forceinline__ void tma_load_3d_cg2(const CUtensorMap* m, uint32_t dst, uint32_t bar, int c0, int c1,
+                                                int c2, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
+      : "memory");
+}
+
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
