@@ -35,9 +35,10 @@ H, I, V = 4096, 14336, 128256
 
 
 def flops_per_token(h=H, i=I, v=V) -> float:
-    """Canonical executed FLOPs per token of MsT with per-chunk recompute
-    (SURVEY.md 8d): MLP 6HI fwd + 4HI recompute + 12HI bwd; head 2HV fwd +
-    2HV recompute + 4HV bwd."""
+    """Canonical FLOPs per token of MsT with per-chunk recompute (SURVEY.md
+    8d): MLP 6HI fwd + 4HI recompute + 12HI bwd; head 2HV fwd + 2HV
+    recompute + 4HV bwd.  (block_step's single-pass head executes 6HV for
+    the head; `executed_flops_per_token` in the JSON is the engine's count.)"""
     return 22.0 * h * i + 8.0 * h * v
 
 
@@ -353,7 +354,8 @@ def main() -> None:
     peaks = load_peaks()
     achieved = gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
     traffic = ncu_traffic_per_launch()
-    tflops_step = tokens_step / world * flops_per_token() / (ms_step / 1e3) / 1e12
+    executed_fpt = gemm_flops / args.steps / S if gemm_flops else flops_per_token()
+    tflops_step = tokens_step / world * executed_fpt / (ms_step / 1e3) / 1e12
     ws_m1 = ms.block_workspace_bytes(S, H, I, V, 1, 1)
     nc = lambda n, m: math.ceil(n / min(n, m))  # noqa: E731
     inter = lambda mm, mh: max(3 * nc(S, mm) * I * 2, nc(S, mh) * V * 2)  # noqa: E731
@@ -367,6 +369,9 @@ def main() -> None:
                    "parallelism": f"sp{world}" if world > 1 else "single",
                    "l2": "no flush: every step streams 1.4 GB of bf16 weights and 2.8 GB of fp32 dW (>> 126 MB L2)"},
         "tflops_per_gpu": tflops_step,
+        "executed_flops_per_token": executed_fpt,
+        "canonical_flops_per_token": flops_per_token(),
+        "canonical_tflops_per_gpu": tokens_step / world * flops_per_token() / (ms_step / 1e3) / 1e12,
         "mfu_model_flops": tokens_step / world * model_flops_per_token() / (ms_step / 1e3) / 1e12 / peaks["tflops"],
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peaks["tflops_sustained"], "unit": "TFLOP/s",
                      "frac": achieved / peaks["tflops_sustained"] if achieved else None, "traffic": traffic,

@@ -124,7 +124,13 @@ MST_API int mst_ctx_set_profile_buffer(mst_ctx* ctx, void* dev_counters);
  *   "sched":   0 plain LPT (default), 1 LPT + long tile last on alternate
  *              pairs, 2 long tile placed mid-list (static lists only);
  *   "dynamic": 1 (default) CTA pairs pull tiles from the global LPT order
- *              through an atomic counter; 0 static per-pair lists.
+ *              through an atomic counter; 0 static per-pair lists;
+ *   "ksplit5": split-K of the LM-Head dX GEMM (1, 2, 4; deterministic
+ *              fixed-order fp32 combine);
+ *   "ksplit9": 2 = MLP dX as two fp32 partial GEMMs + combine, 1 = fused;
+ *   "tma3d":   MN-major operands as 3-D tensor maps (process-wide);
+ *   "fused_head": 1 (default) block_step runs mst_lmhead_fused, 0 runs the
+ *              separate forward + backward (logits recomputed).
  * Unknown keys are MST_ERR_CONFIG.  Changing a knob clears the schedule cache. */
 MST_API int mst_ctx_set_tuning(mst_ctx* ctx, const char* key, int value);
 
@@ -166,6 +172,20 @@ MST_API int mst_lmhead_forward(mst_ctx* ctx, void* stream, const void* x, const 
 MST_API int mst_lmhead_backward(mst_ctx* ctx, void* stream, const mst_lmhead_saved* saved, const void* w_out,
                         const float* global_stats, float grad_loss, void* grad_x, float* grad_w_out,
                         int accumulate, void* workspace, size_t workspace_bytes);
+
+/* Single-pass LM-Head forward + backward (forward and backward of SPEC.md
+ * 313-330 in one chunk loop, for callers that run them back to back): one
+ * logits GEMM per chunk whose epilogue keeps the online-softmax partials and
+ * writes the unnormalised softmax numerators in-tile; an in-place pass turns
+ * them into dlogits once the row LSE is known.  Logits are never stored and
+ * the only [n/M, V] buffer is the dlogits chunk.  `global_valid` (device
+ * float, nullable) overrides the local valid-token count for token-weighted
+ * scaling under sequence sharding.  Writes stats (loss in [2]), lse, dX and
+ * dW_out (accumulate as in mst_lmhead_backward). */
+MST_API int mst_lmhead_fused(mst_ctx* ctx, void* stream, const void* x, const int32_t* labels, const void* w_out,
+                             int64_t n, int64_t h, int64_t v, int64_t m, int loss_mode, float grad_loss,
+                             const float* global_valid, float* stats, float* lse, void* grad_x, float* grad_w_out,
+                             int accumulate, void* workspace, size_t workspace_bytes);
 
 /* One fused MLP -> LM-Head block, forward + backward (the bench unit):
  * O = mlp(X); loss = CE(O W_out, L); then dW_out, dO, dX, dW_{gate,up,down}.

@@ -25,8 +25,8 @@
 // fp32) or TMA reduce-add (fp32 weight-gradient accumulation in L2), so no
 // epilogue thread ever waits on a global store.
 //
-// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer (leader CTA
-// only), w2 TMEM allocator, w3 idle, w4..w7 epilogue (warp w owns TMEM lanes
+// Warp roles (256 threads): w0 TMA producer for A, w3 TMA producer for B,
+// w1 MMA issuer (leader CTA only), w2 TMEM allocator, w4..w7 epilogue (warp w owns TMEM lanes
 // 32*(w%4) .. +31, i.e. 32 output rows, and all accumulator columns).
 #pragma once
 
@@ -42,6 +42,12 @@ namespace mst {
 #ifndef MST_EPI_BUFS
 #define MST_EPI_BUFS 2
 #endif
+#ifndef MST_SPLIT_PRODUCER
+#define MST_SPLIT_PRODUCER 1  // warp 0 issues A loads, warp 3 issues B loads (0: one producer)
+#endif
+#ifndef MST_DW_RED_GLOBAL
+#define MST_DW_RED_GLOBAL 0  // 1: fp32 dW accumulation with red.global.add.v4.f32 from registers
+#endif
 #ifndef MST_DW_EVICT_FIRST
 #define MST_DW_EVICT_FIRST 1  // fp32 dW stores / reduce-adds stream through L2 with evict_first
 #endif
@@ -55,8 +61,8 @@ constexpr int kThreads = 128 + 32 * kNumEpiWarps;
 constexpr int kEpiBufBytes = 4096;           // one 32-row x 128-byte TMA box
 constexpr int kEpiBufs = MST_EPI_BUFS;       // per epilogue warp (>= 2)
 constexpr int kEpiBytes = kNumEpiWarps * kEpiBufs * kEpiBufBytes;
-constexpr int kMaxProblems = 4;
-constexpr int kMaxMaps = 16;
+constexpr int kMaxProblems = 8;
+constexpr int kMaxMaps = 24;
 constexpr int kTmemCols = 512;
 constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 512 /*barriers, tile ring*/;
 
@@ -67,6 +73,7 @@ enum EpiKind : int32_t {
   kEpiAccF32 = 3,     // out{g}[row, col] (+)= acc  fp32                   (TMA store / reduce-add)
   kEpiCeFwd = 4,      // per-row (max, sumexp) partial + target logit
   kEpiCeBwd = 5,      // dlogits = (softmax - onehot) * scale              (TMA store)
+  kEpiCeFwdNum = 6,   // kEpiCeFwd + softmax numerator 2^(z log2e - m_tile) (TMA store, bf16)
 };
 
 struct PhaseDesc {
@@ -79,6 +86,8 @@ struct PhaseDesc {
   int32_t acc_continue;           // 1: keep accumulating onto the previous phase
   int32_t a_pol, b_pol;           // L2 policy of the operand loads: 0 normal, 1 evict_last, 2 evict_first
   int32_t a_3d, b_3d;             // MN-major operand described by a 3-D map: one TMA per slab
+  int32_t k_start;                // first K block (split-K problems)
+  int32_t _pad;
 };
 
 struct ProblemDesc {
@@ -93,6 +102,9 @@ struct ProblemDesc {
   int32_t map_out0, map_out1, map_out2;  // output tensor maps (TMA store boxes)
   int32_t _pad;
   int64_t ld_aux;
+  void* out0;          // kEpiAccF32 with red.global: output base pointers (halves g = 0, 1)
+  void* out1;
+  int64_t ld0, ld1;
   const float* aux;    // kEpiSwigluBwd: dh [rows, ld_aux] fp32
   const int32_t* labels;
   const float* lse;    // kEpiCeBwd: log-sum-exp per row (natural log)
@@ -121,7 +133,8 @@ struct GemmParams {
 };
 
 constexpr int kTileSlots = 4;          // tile-code ring between the pair leader's producer and all roles
-constexpr int kTileConsumers = 10;     // leader MMA + 4 leader epi warps + peer producer + 4 peer epi warps
+// leader MMA + 4 leader epi warps + peer producer + 4 peer epi warps (+ both B producers)
+constexpr int kTileConsumers = 10 + 2 * MST_SPLIT_PRODUCER;
 
 // Per-role iterator over this pair's tiles.  Static mode walks the host LPT
 // list; dynamic mode: the leader's producer claims the next tile of the
@@ -335,6 +348,37 @@ __device__ __forceinline__ void run_epilogue(const GemmParams& p, const ProblemD
     }
     case kEpiAccF32: {
       const int half = P.ph[0].umma_n >> 1;
+#if MST_DW_RED_GLOBAL
+      if (P.beta) {
+        // Accumulate straight from registers: 16-byte vector reductions in
+        // L2, no shared-memory staging (which competes with TMA / UMMA).
+        for (int g = 0; g < 2; ++g) {
+          float* out = static_cast<float*>(g ? P.out1 : P.out0);
+          const int64_t ld = g ? P.ld1 : P.ld0;
+          const int col0 = tn * P.tile_n + (g ? P.col_off1 : P.col_off0);
+          for (int c = 0; c < half; c += 32) {
+            float v[32];
+            epi::load32(taddr + g * half + c, v);
+            const int col = col0 + c;
+            if (row_ok) {
+              float* dst = out + static_cast<int64_t>(row) * ld + col;
+              if (col + 32 <= P.cols) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * q), "f"(v[4 * q]),
+                               "f"(v[4 * q + 1]), "f"(v[4 * q + 2]), "f"(v[4 * q + 3])
+                               : "memory");
+              } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                  if (col + j < P.cols) atomicAdd(dst + j, v[j]);
+              }
+            }
+          }
+        }
+        break;
+      }
+#endif
       for (int g = 0; g < 2; ++g) {
         const CUtensorMap* m = &p.maps[g ? P.map_out1 : P.map_out0];
         const int col0 = tn * P.tile_n + (g ? P.col_off1 : P.col_off0);
@@ -454,6 +498,56 @@ __device__ __forceinline__ void run_epilogue(const GemmParams& p, const ProblemD
       }
       break;
     }
+    case kEpiCeFwdNum: {
+      // Single-pass LM-Head forward+backward: per (row, 256-column tile)
+      // pass 1 finds m = max z*log2e over the tile, pass 2 writes the
+      // unnormalised softmax numerator e = 2^(z*log2e - m) (bf16, in (0,1])
+      // into the dlogits buffer and accumulates s = sum e (fp32).  Logits
+      // themselves are never stored; after the row LSE is known,
+      // normalize_dlogits turns e into (e 2^(m - lse2) - onehot) * scale.
+      const int v0 = tn * 256;
+      const int lab = row_ok ? P.labels[row] : -1;
+      float m = -INFINITY, zt = 0.0f;
+      for (int c = 0; c < 256; c += 32) {
+        float z[32];
+        epi::load32(taddr + c, z);
+        const int vb = v0 + c;
+        const int valid = P.cols - vb;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < valid) m = fmaxf(m, z[j] * epi::kLog2e);
+        if (lab >= vb && lab < vb + 32) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (lab == vb + j) zt = z[j];
+        }
+      }
+      float s = 0.0f;
+      const CUtensorMap* mo = &p.maps[P.map_out0];
+      for (int c = 0; c < 256; c += 64) {
+        const int b = st.acquire();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float z[32];
+          epi::load32(taddr + c + 32 * h, z);
+          const int vb = v0 + c + 32 * h;
+          const int valid = P.cols - vb;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float e = j < valid ? ptx::ex2(z[j] * epi::kLog2e - m) : 0.0f;
+            s += e;
+            z[j] = e;
+          }
+          st.put_bf16x32(b, h, z);
+        }
+        st.issue(b, mo, v0 + c, row0, false);
+      }
+      if (row_ok) {
+        P.part[static_cast<int64_t>(row) * P.nparts + tn] = make_float2(m, s);
+        if (lab >= v0 && lab < v0 + 256) P.ztarget[row] = zt;
+      }
+      break;
+    }
     case kEpiCeBwd: {
       const int v0 = tn * 256;
       const int lab = row_ok ? P.labels[row] : -1;
@@ -533,8 +627,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   TileFeed feed{p.sched + p.sched_off[pair], p.sched_off[pair + 1] - p.sched_off[pair], 0, tile_codes,
                 tile_full, tile_empty, 0, 0};
 
-  if (warp == 0) {
-    // ===================== TMA producer =====================
+  if (warp == 0 || (MST_SPLIT_PRODUCER && warp == 3)) {
+    // ===================== TMA producer(s) =====================
+    // With MST_SPLIT_PRODUCER warp 0 issues the A loads (and the expect_tx),
+    // warp 3 the B loads; both follow the same stage ring.
+    const bool do_a = warp == 0;
+    const bool do_b = !MST_SPLIT_PRODUCER || warp == 3;
     if (lane == 0) {
       uint64_t pols[3];
       pols[0] = ptx::policy_evict_normal();
@@ -544,7 +642,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       MST_PROF_DECL
       for (;;) {
-        const int32_t code = rank == 0 ? feed.produce(p) : feed.consume(p, 0);
+        const int32_t code = (rank == 0 && warp == 0) ? feed.produce(p) : feed.consume(p, 0);
         if (code < 0) break;
         int prob, tm, tn;
         decode_tile(p, code, prob, tm, tn);
@@ -561,12 +659,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int kb = 0; kb < d.k_blocks; ++kb) {
             MST_PROF_WAIT(0, ptx::mbar_wait(ptx::smem_u32(&empty[stage]), phase ^ 1));
             const uint32_t fbar_local = ptx::smem_u32(&full[stage]);
-            if (rank == 0) ptx::mbar_arrive_expect_tx(fbar_local, stage_tx);
+            if (rank == 0 && do_a) ptx::mbar_arrive_expect_tx(fbar_local, stage_tx);
             const uint32_t fbar = ptx::mapa(fbar_local, 0);
             const uint32_t sa = ptx::smem_u32(smem_a + stage * kABytes);
             const uint32_t sb = ptx::smem_u32(smem_b + stage * kBBytes);
-            const int k0 = kb * kBK;
-            if (!d.a_mn) {
+            const int k0 = (d.k_start + kb) * kBK;
+            if (!do_a) {
+            } else if (!d.a_mn) {
               ptx::tma_load_2d_cg2(ma, sa, fbar, k0, arow, pa);
             } else if (d.a_3d) {
               ptx::tma_load_3d_cg2(ma, sa, fbar, 0, k0, arow >> 6, pa);
@@ -574,7 +673,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               ptx::tma_load_2d_cg2(ma, sa, fbar, arow, k0, pa);
               ptx::tma_load_2d_cg2(ma, sa + 8192, fbar, arow + 64, k0, pa);
             }
-            if (!d.b_mn) {
+            if (!do_b) {
+            } else if (!d.b_mn) {
               ptx::tma_load_2d_cg2(mb, sb, fbar, k0, nb, pb);
             } else if (d.b_3d) {
               ptx::tma_load_3d_cg2(mb, sb, fbar, 0, k0, nb >> 6, pb);

@@ -114,6 +114,9 @@ struct mst_ctx {
   int64_t prof_slot = 0;
   int sched_mode = 0;  // MST_SCHED: 0 plain LPT, 1 LPT + long tile last on alternate pairs, 2 long tile mid-list
   int dynamic = 1;     // MST_DYNAMIC: pairs pull tiles from the global LPT order (atomic counter)
+  int ksplit5 = 1;     // split-K of the LM-Head dX GEMM (K5): 1, 2 or 4
+  int ksplit9 = 1;     // MLP dX GEMM (K9): 1 = two-phase accumulate, 2 = one problem per phase + combine
+  int fused_head = 1;  // block_step: single-pass LM-Head forward+backward (mst_lmhead_fused)
 };
 
 namespace {
@@ -213,6 +216,8 @@ struct PhaseSpec {
   int tmem_col;
   int b_off0, b_off1;
   bool acc_continue;
+  int k_start = 0;   // first K block (split-K slice)
+  int k_blocks = 0;  // 0: the whole K extent
 };
 
 int add_phase(mst_ctx* c, Launch& L, ProblemDesc& P, const PhaseSpec& s) {
@@ -236,7 +241,8 @@ int add_phase(mst_ctx* c, Launch& L, ProblemDesc& P, const PhaseSpec& s) {
   d.b_3d = (use_3d(s.b0, nh) && use_3d(s.b1, nh)) ? 1 : 0;
   d.umma_n = s.umma_n;
   d.tmem_col = s.tmem_col;
-  d.k_blocks = static_cast<int32_t>(cdiv(s.a.k, mst::kBK));
+  d.k_start = s.k_start;
+  d.k_blocks = s.k_blocks ? s.k_blocks : static_cast<int32_t>(cdiv(s.a.k, mst::kBK) - s.k_start);
   d.b_off0 = s.b_off0;
   d.b_off1 = s.b_off1;
   d.acc_continue = s.acc_continue ? 1 : 0;
@@ -544,6 +550,64 @@ int transpose_bf16(mst_ctx* c, cudaStream_t st, const void* src, int64_t ld_src,
   return MST_OK;
 }
 
+// Per-chunk valid-label counts straight from the labels (balanced chunk
+// plan recomputed in-kernel), so the single-pass head knows every dlogits
+// scale before its first chunk: stats[4+M+c] and stats[1] (total).
+__global__ void chunk_valid_kernel(const int32_t* __restrict__ labels, int64_t n, int m, int vocab, float* stats) {
+  __shared__ float sv[32];
+  const int c = blockIdx.x;
+  const int64_t q = n / m, r = n % m;
+  const int64_t s0 = c * q + (c < r ? c : r), s1 = s0 + q + (c < r ? 1 : 0);
+  float v = 0.f;
+  for (int64_t i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
+    const int lab = labels[i];
+    v += (lab >= 0 && lab < vocab) ? 1.f : 0.f;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
+  if ((threadIdx.x & 31) == 0) sv[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sv[w];
+    stats[4 + m + c] = t;
+  }
+}
+
+__global__ void sum_valid_kernel(float* stats, int m) {
+  if (threadIdx.x != 0) return;
+  double t = 0;
+  for (int c = 0; c < m; ++c) t += stats[4 + m + c];
+  stats[1] = (float)t;
+}
+
+// In place: e (bf16 softmax numerator, tile max m_tile in part[].x) ->
+// dlogits = (e * 2^(m_tile - lse*log2e) - [v == label]) * scale, bf16.
+__global__ void normalize_dlogits_kernel(uint16_t* __restrict__ dl, int64_t ld, int rows, int cols,
+                                         const float2* __restrict__ part, int nparts, const float* __restrict__ lse,
+                                         const int32_t* __restrict__ labels, const float* __restrict__ scale) {
+  const int64_t per_row = cols / 8;
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t r = idx / per_row;
+  if (r >= rows) return;
+  const int c = static_cast<int>(idx - r * per_row) * 8;
+  const int lab = labels[r];
+  const float sc = (lab >= 0 && lab < cols) ? *scale : 0.f;
+  const float f = exp2f(part[r * nparts + (c >> 8)].x - lse[r] * 1.4426950408889634f);
+  uint4* p = reinterpret_cast<uint4*>(dl + r * ld + c);
+  uint4 w = *p;
+  uint32_t* u = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float e0 = __uint_as_float(u[k] << 16), e1 = __uint_as_float(u[k] & 0xffff0000u);
+    const float d0 = (e0 * f - (c + 2 * k == lab ? 1.f : 0.f)) * sc;
+    const float d1 = (e1 * f - (c + 2 * k + 1 == lab ? 1.f : 0.f)) * sc;
+    u[k] = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(d0)) |
+           ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(d1)) << 16);
+  }
+  *p = w;
+}
+
 // ------------------------------------------------------------ validation
 int check_dims(int64_t n, int64_t h, int64_t x, int64_t m, const char* xname) {
   if (n <= 0) return fail(MST_ERR_DATA, "N must be >= 1 (SPEC.md:290), got %lld", (long long)n);
@@ -612,13 +676,83 @@ int build_plain(mst_ctx* c, Launch& L, const Operand& a, const Operand& b, void*
   P.cols = (int)b.mn;
   P.epi = epi;
   P.beta = beta;
-  if (epi == mst::kEpiStoreBf16 || epi == mst::kEpiAccF32 || epi == mst::kEpiCeBwd) {
+  if (epi == mst::kEpiStoreBf16 || epi == mst::kEpiAccF32 || epi == mst::kEpiCeBwd || epi == mst::kEpiCeFwdNum) {
     MST_TRY(add_out_map(c, L, out, b.mn, a.mn, ld_out, epi == mst::kEpiAccF32, &P.map_out0));
     P.map_out1 = P.map_out0;
   }
+  P.out0 = P.out1 = out;
+  P.ld0 = P.ld1 = ld_out;
   P.col_off0 = 0;
   P.col_off1 = 128;
   L.flops += 2.0 * a.mn * b.mn * a.k;
+  return MST_OK;
+}
+
+// Split-K: `splits` problems, slice s covers K blocks [s*kps, (s+1)*kps) and
+// stores fp32 partials into part + s*rows*ldp; splitk_combine sums them in
+// slice order (deterministic) into the bf16 output.  Used for the long-K,
+// few-tile dX GEMMs (K5: K = V, K9: K = 2I) so they interleave with the
+// short-K dW tiles of the same launch instead of dominating its tail.
+int build_plain_splitk(mst_ctx* c, Launch& L, const Operand& a, const Operand& b, float* part, int64_t ldp,
+                       int splits) {
+  const int kb = (int)cdiv(a.k, mst::kBK);
+  const int kps = (int)cdiv(kb, splits);
+  for (int s = 0; s < splits; ++s) {
+    const int k0 = s * kps;
+    if (k0 >= kb) break;
+    ProblemDesc& P = L.p.prob[L.p.num_problems++];
+    PhaseSpec ps{};
+    ps.a = a;
+    ps.b0 = b;
+    ps.b1 = b;
+    ps.umma_n = 256;
+    ps.b_off1 = 128;
+    ps.k_start = k0;
+    ps.k_blocks = std::min(kps, kb - k0);
+    MST_TRY(add_phase(c, L, P, ps));
+    P.m_tiles = (int)cdiv(a.mn, 256);
+    P.tile_n = 256;
+    P.n_tiles = (int)cdiv(b.mn, 256);
+    P.rows = (int)a.mn;
+    P.cols = (int)b.mn;
+    P.epi = mst::kEpiAccF32;
+    P.beta = 0;
+    MST_TRY(add_out_map(c, L, part + (int64_t)s * a.mn * ldp, b.mn, a.mn, ldp, true, &P.map_out0));
+    P.map_out1 = P.map_out0;
+    P.col_off0 = 0;
+    P.col_off1 = 128;
+    L.flops += 2.0 * a.mn * b.mn * std::min<int64_t>(a.k - (int64_t)k0 * mst::kBK, (int64_t)kps * mst::kBK);
+  }
+  return MST_OK;
+}
+
+__global__ void splitk_combine_kernel(const float* __restrict__ part, int splits, int64_t split_stride, int rows,
+                                      int cols, int64_t ldp, uint16_t* __restrict__ out, int64_t ld_out) {
+  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+  const int64_t r = i / cols, col = i % cols;
+  if (r >= rows) return;
+  const float* p = part + r * ldp + col;
+  float4 acc = *reinterpret_cast<const float4*>(p);
+  for (int s = 1; s < splits; ++s) {
+    const float4 v = *reinterpret_cast<const float4*>(p + s * split_stride);
+    acc.x += v.x;
+    acc.y += v.y;
+    acc.z += v.z;
+    acc.w += v.w;
+  }
+  uint2 w;
+  w.x = ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(acc.y)) << 16) | __bfloat16_as_ushort(__float2bfloat16_rn(acc.x));
+  w.y = ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(acc.w)) << 16) | __bfloat16_as_ushort(__float2bfloat16_rn(acc.z));
+  *reinterpret_cast<uint2*>(out + r * ld_out + col) = w;
+}
+
+int splitk_combine(mst_ctx* c, cudaStream_t st, const float* part, int splits, int64_t rows, int64_t cols, void* out,
+                   int64_t ld_out) {
+  const int64_t n4 = rows * cols / 4;  // cols % 8 == 0
+  splitk_combine_kernel<<<(unsigned)cdiv(n4, 256), 256, 0, st>>>(part, splits, rows * cols, (int)rows, (int)cols,
+                                                                  cols, static_cast<uint16_t*>(out), ld_out);
+  c->launches++;
+  MST_CUDA(cudaGetLastError());
   return MST_OK;
 }
 
@@ -754,6 +888,14 @@ int mst_ctx_set_tuning(mst_ctx* c, const char* key, int value) {
     c->sched_mode = value;
   } else if (std::strcmp(key, "dynamic") == 0) {
     c->dynamic = value != 0;
+  } else if (std::strcmp(key, "ksplit5") == 0) {
+    if (value != 1 && value != 2 && value != 4) return fail(MST_ERR_CONFIG, "ksplit5 must be 1, 2 or 4");
+    c->ksplit5 = value;
+  } else if (std::strcmp(key, "ksplit9") == 0) {
+    if (value != 1 && value != 2) return fail(MST_ERR_CONFIG, "ksplit9 must be 1 or 2");
+    c->ksplit9 = value;
+  } else if (std::strcmp(key, "fused_head") == 0) {
+    c->fused_head = value != 0;
   } else if (std::strcmp(key, "tma3d") == 0) {
     c3d_enabled = value != 0;
   } else {
@@ -782,7 +924,7 @@ int mst_make_chunk_plan(int64_t n, int64_t m, int64_t* bounds, int64_t* num_chun
 static int64_t ld_t(int64_t n, int64_t m) { return (max_chunk(n, m) + 7) / 8 * 8; }
 
 static int carve_mlp(Carve& cv, int64_t n, int64_t h, int64_t i, int64_t m, void** hbuf, void** dg, void** du,
-                     float** dh = nullptr, void** xt = nullptr, void** ht = nullptr) {
+                     float** dh = nullptr, void** xt = nullptr, void** ht = nullptr, float** part9 = nullptr) {
   const int64_t nc = max_chunk(n, m);
   const size_t hb = size_t(nc) * i * 2;
   // forward uses two h buffers (ping-pong across chunks); backward h, dG,
@@ -797,11 +939,13 @@ static int carve_mlp(Carve& cv, int64_t n, int64_t h, int64_t i, int64_t m, void
   void* t = cv.take(size_t(i) * ld_t(n, m) * 2);
   if (xt) *xt = x;
   if (ht) *ht = t;
+  float* p9 = static_cast<float*>(cv.take(size_t(2) * nc * h * 4));  // K9 split partials
+  if (part9) *part9 = p9;
   return MST_OK;
 }
 
 static void carve_head(Carve& cv, int64_t n, int64_t h, int64_t v, int64_t m, float2** part, float** zt,
-                       float** lrow, void** dl, float** scales, void** ot = nullptr) {
+                       float** lrow, void** dl, float** scales, void** ot = nullptr, float** part5 = nullptr) {
   const int64_t nc = max_chunk(n, m);
   const int64_t nparts = cdiv(v, 256);
   *part = static_cast<float2*>(cv.take(size_t(nc) * nparts * sizeof(float2)));
@@ -811,6 +955,8 @@ static void carve_head(Carve& cv, int64_t n, int64_t h, int64_t v, int64_t m, fl
   *scales = static_cast<float*>(cv.take(size_t(std::min(n, m)) * 4 + 64));
   void* o = cv.take(size_t(h) * ld_t(n, m) * 2);  // X_j^T: K-major A operand of K6
   if (ot) *ot = o;
+  float* p5 = static_cast<float*>(cv.take(size_t(4) * nc * h * 4));  // K5 split-K partials
+  if (part5) *part5 = p5;
 }
 
 int mst_mlp_workspace(int64_t n, int64_t h, int64_t i, int64_t m, size_t* bytes) {
@@ -910,7 +1056,8 @@ int mst_mlp_backward(mst_ctx* c, void* stream, const void* dout, const mst_mlp_s
   Carve cv{static_cast<char*>(ws), ws_bytes, 0, false};
   void *hb, *dg, *du, *xt, *ht;
   float* dhb;
-  carve_mlp(cv, n, h, i, m, &hb, &dg, &du, &dhb, &xt, &ht);
+  float* part9;
+  carve_mlp(cv, n, h, i, m, &hb, &dg, &du, &dhb, &xt, &ht, &part9);
   const int64_t ldt = ld_t(n, m);
   const std::vector<int64_t> b = plan_bounds(n, m);
   const int nch = (int)b.size() - 1;
@@ -958,7 +1105,11 @@ int mst_mlp_backward(mst_ctx* c, void* stream, const void* dout, const mst_mlp_s
     MST_TRY(transpose_bf16(c, st, xj, h, xt, ldt, rows, h));
     {  // K9 + K8 + K10 (mutually independent) + K7a of the next chunk, one launch.
       Launch L;
-      {  // K9: dX_j = dG W_g^T + dU W_u^T (B K-major), one accumulator over both phases.
+      if (c->ksplit9 > 1) {  // K9 as two fp32 partial GEMMs (dG W_g^T, dU W_u^T) + combine
+        MST_TRY(build_plain_splitk(c, L, Operand{dg, rows, i, i, false}, Operand{wg, h, i, i, false}, part9, h, 1));
+        MST_TRY(build_plain_splitk(c, L, Operand{du, rows, i, i, false}, Operand{wu, h, i, i, false},
+                                   part9 + rows * h, h, 1));
+      } else {  // K9: dX_j = dG W_g^T + dU W_u^T (B K-major), one accumulator over both phases.
         ProblemDesc& P = L.p.prob[L.p.num_problems++];
         PhaseSpec q0{};
         q0.a = {dg, rows, i, i, false};
@@ -1005,11 +1156,15 @@ int mst_mlp_backward(mst_ctx* c, void* stream, const void* dout, const mst_mlp_s
         P.beta = beta;
         MST_TRY(add_out_map(c, L, dwg, i, h, i, true, &P.map_out0));
         MST_TRY(add_out_map(c, L, dwu, i, h, i, true, &P.map_out1));
+        P.out0 = dwg;
+        P.out1 = dwu;
+        P.ld0 = P.ld1 = i;
         P.col_off0 = P.col_off1 = 0;
         L.flops += 2.0 * h * (2.0 * i) * rows;
       }
       if (j + 1 < nch) MST_TRY(add_k7a(L, j + 1));
       MST_TRY(launch(c, st, L));
+      if (c->ksplit9 > 1) MST_TRY(splitk_combine(c, st, part9, 2, rows, h, const_cast<char*>(bptr(dx, r0 * h)), h));
     }
   }
   MST_CUDA(cudaGetLastError());
@@ -1091,7 +1246,8 @@ int mst_lmhead_backward(mst_ctx* c, void* stream, const mst_lmhead_saved* s, con
   float2* part;
   float *zt, *lrow, *scales;
   void *dl, *ot;
-  carve_head(cv, n, h, v, m, &part, &zt, &lrow, &dl, &scales, &ot);
+  float* part5;
+  carve_head(cv, n, h, v, m, &part, &zt, &lrow, &dl, &scales, &ot, &part5);
   const int64_t ldt = ld_t(n, m);
   const std::vector<int64_t> b = plan_bounds(n, m);
   const int nch = (int)b.size() - 1;
@@ -1113,6 +1269,83 @@ int mst_lmhead_backward(mst_ctx* c, void* stream, const mst_lmhead_saved* s, con
       P.scale = scales + j;
       MST_TRY(launch(c, st, L));
     }
+    {  // K5 (dX = dl W_out^T, optionally split-K) + K6 (dW_out += X^T dl), grouped.
+      Launch L;
+      const Operand a5{dl, rows, v, v, false}, b5{wout, h, v, v, false};
+      if (c->ksplit5 > 1)
+        MST_TRY(build_plain_splitk(c, L, a5, b5, part5, h, c->ksplit5));
+      else
+        MST_TRY(build_plain(c, L, a5, b5, const_cast<char*>(bptr(dx, r0 * h)), h, mst::kEpiStoreBf16, 0));
+      MST_TRY(build_plain(c, L, Operand{ot, h, rows, ldt, false}, Operand{dl, v, rows, v, true}, dwout, v,
+                          mst::kEpiAccF32, beta));
+      MST_TRY(launch(c, st, L));
+      if (c->ksplit5 > 1)
+        MST_TRY(splitk_combine(c, st, part5, c->ksplit5, rows, h, const_cast<char*>(bptr(dx, r0 * h)), h));
+    }
+  }
+  MST_CUDA(cudaGetLastError());
+  return MST_OK;
+}
+
+int mst_lmhead_fused(mst_ctx* c, void* stream, const void* x, const int32_t* labels, const void* wout, int64_t n,
+                     int64_t h, int64_t v, int64_t m, int loss_mode, float grad_loss, const float* global_valid,
+                     float* stats, float* lse, void* dx, float* dwout, int accumulate, void* ws, size_t ws_bytes) {
+  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  MST_TRY(check_dims(n, h, v, m, "V"));
+  if (loss_mode != MST_LOSS_TOKEN_WEIGHTED && loss_mode != MST_LOSS_PAPER_MEAN)
+    return fail(MST_ERR_CONFIG, "unknown loss mode %d", loss_mode);
+  if (!x || !labels || !wout || !stats || !lse || !dx || !dwout) return fail(MST_ERR_CONFIG, "NULL tensor pointer");
+  size_t need = 0;
+  MST_TRY(mst_lmhead_workspace(n, h, v, m, &need));
+  if (!ws || ws_bytes < need) return fail(MST_ERR_CONFIG, "workspace too small (%zu < %zu)", ws_bytes, need);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Carve cv{static_cast<char*>(ws), ws_bytes, 0, false};
+  float2* part;
+  float *zt, *lrow, *scales;
+  void *dl, *ot;
+  float* part5;
+  carve_head(cv, n, h, v, m, &part, &zt, &lrow, &dl, &scales, &ot, &part5);
+  const int64_t ldt = ld_t(n, m);
+  const std::vector<int64_t> b = plan_bounds(n, m);
+  const int nch = (int)b.size() - 1;
+  const int nparts = (int)cdiv(v, 256);
+  // Scales first (they only depend on the labels): per-chunk valid counts,
+  // total (or the caller's global count), dlogits scale per chunk.
+  MST_CUDA(cudaMemsetAsync(stats, 0, sizeof(float) * MST_STATS_LEN(nch), st));
+  chunk_valid_kernel<<<nch, 256, 0, st>>>(labels, n, nch, (int)v, stats);
+  sum_valid_kernel<<<1, 32, 0, st>>>(stats, nch);
+  float* gstats = c->scratch_dev + 64;  // [2]: (unused, global valid)
+  if (global_valid) {
+    MST_CUDA(cudaMemcpyAsync(gstats + 1, global_valid, sizeof(float), cudaMemcpyDeviceToDevice, st));
+  } else {
+    MST_CUDA(cudaMemcpyAsync(gstats + 1, stats + 1, sizeof(float), cudaMemcpyDeviceToDevice, st));
+  }
+  grad_scale_kernel<<<(nch + 255) / 256, 256, 0, st>>>(gstats, stats, nch, loss_mode, grad_loss, scales);
+  c->launches += 3;
+  for (int j = 0; j < nch; ++j) {
+    const int64_t r0 = b[j], rows = b[j + 1] - b[j];
+    const int beta = (j > 0 || accumulate) ? 1 : 0;
+    const void* xj = bptr(x, r0 * h);
+    MST_TRY(transpose_bf16(c, st, xj, h, ot, ldt, rows, h));  // (head input)_j^T: K-major A of K6
+    {  // K3': logits GEMM; epilogue = online-softmax partials + softmax numerators (bf16)
+      Launch L;
+      MST_TRY(build_plain(c, L, Operand{xj, rows, h, h, false}, Operand{wout, v, h, v, true}, dl, v,
+                          mst::kEpiCeFwdNum, 0));
+      ProblemDesc& P = L.p.prob[0];
+      P.labels = labels + r0;
+      P.part = part;
+      P.ztarget = zt;
+      P.nparts = nparts;
+      MST_TRY(launch(c, st, L));
+    }
+    const int threads = 256;
+    ce_combine_kernel<<<(unsigned)cdiv(rows * 32, threads), threads, 0, st>>>(part, nparts, zt, labels + r0, (int)rows,
+                                                                               (int)v, lse + r0, lrow, stats + 3);
+    chunk_reduce_kernel<<<1, 1024, 0, st>>>(lrow, labels + r0, (int)rows, (int)v, stats + 4 + j,
+                                            stats + 4 + nch + j);
+    normalize_dlogits_kernel<<<(unsigned)cdiv(rows * (v / 8), 256), 256, 0, st>>>(
+        static_cast<uint16_t*>(dl), v, (int)rows, (int)v, part, nparts, lse + r0, labels + r0, scales + j);
+    c->launches += 3;
     {  // K5 (dX = dl W_out^T) + K6 (dW_out += X^T dl), grouped.
       Launch L;
       MST_TRY(build_plain(c, L, Operand{dl, rows, v, v, false}, Operand{wout, h, v, v, false},
@@ -1122,6 +1355,8 @@ int mst_lmhead_backward(mst_ctx* c, void* stream, const mst_lmhead_saved* s, con
       MST_TRY(launch(c, st, L));
     }
   }
+  finalize_loss_kernel<<<1, 32, 0, st>>>(stats, nch, loss_mode);
+  c->launches += 1;
   MST_CUDA(cudaGetLastError());
   return MST_OK;
 }
@@ -1144,8 +1379,14 @@ int mst_block_step(mst_ctx* c, void* stream, const void* x, const int32_t* label
   mst_mlp_saved ms;
   mst_lmhead_saved hs;
   MST_TRY(mst_mlp_forward(c, stream, x, wg, wu, wd, o, n, h, i, m_mlp, rest, rest_bytes, &ms));
-  MST_TRY(mst_lmhead_forward(c, stream, o, labels, wout, n, h, v, m_head, loss_mode, stats, lse, rest, rest_bytes, &hs));
-  MST_TRY(mst_lmhead_backward(c, stream, &hs, wout, stats, grad_loss, dO, dwout, accumulate, rest, rest_bytes));
+  if (c->fused_head) {
+    MST_TRY(mst_lmhead_fused(c, stream, o, labels, wout, n, h, v, m_head, loss_mode, grad_loss, nullptr, stats, lse,
+                             dO, dwout, accumulate, rest, rest_bytes));
+  } else {
+    MST_TRY(mst_lmhead_forward(c, stream, o, labels, wout, n, h, v, m_head, loss_mode, stats, lse, rest, rest_bytes,
+                               &hs));
+    MST_TRY(mst_lmhead_backward(c, stream, &hs, wout, stats, grad_loss, dO, dwout, accumulate, rest, rest_bytes));
+  }
   MST_TRY(mst_mlp_backward(c, stream, dO, &ms, wg, wu, wd, dx, dwg, dwu, dwd, accumulate, rest, rest_bytes));
   return MST_OK;
 }

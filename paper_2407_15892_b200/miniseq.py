@@ -115,6 +115,8 @@ _SIGS = {
                             ctypes.POINTER(_HeadSaved)], ctypes.c_int),
     "mst_lmhead_backward": ([_VP, _VP, ctypes.POINTER(_HeadSaved), _VP, _VP, _F32, _VP, _VP, _I32, _VP,
                              ctypes.c_size_t], ctypes.c_int),
+    "mst_lmhead_fused": ([_VP, _VP, _VP, _VP, _VP, _I64, _I64, _I64, _I64, _I32, _F32, _VP, _VP, _VP, _VP, _VP, _I32,
+                          _VP, ctypes.c_size_t], ctypes.c_int),
     "mst_block_step": ([_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _F32,
                         _VP, _VP, _VP, _VP, _VP, _VP, _I32, _VP, ctypes.c_size_t], ctypes.c_int),
     "mst_debug_gemm": ([_VP, _VP, _VP, _VP, _VP, _I64, _I64, _I64, _I32, _I32, _I32, _I32], ctypes.c_int),
@@ -424,6 +426,37 @@ def miniseq_lmhead_backward(saved: LmHeadSaved, w: LmHeadWeights, plan: ChunkPla
                                        gs.data_ptr(), float(grad_loss), dX.data_ptr(), dW_out.data_ptr(),
                                        int(accumulate), ws.data_ptr(), ws.numel()))
     return dX, dW_out
+
+
+def miniseq_lmhead_fused(X: torch.Tensor, L: torch.Tensor, w: LmHeadWeights, plan: ChunkPlan,
+                         mode: int = TOKEN_WEIGHTED, grad_loss: float = 1.0,
+                         global_valid: Optional[torch.Tensor] = None, dW_out: Optional[torch.Tensor] = None,
+                         accumulate: bool = False):
+    """LM-Head forward + backward in one pass over the chunks (SPEC.md:313-330
+    back to back): returns (loss, stats, lse, dX, dW_out).  `global_valid`
+    (0-d/1-elem device float) overrides the local valid count (sequence sharding)."""
+    ctx = Context.get(X.device.index)
+    N, H = X.shape
+    V = w.W_out.shape[1]
+    _plan_check(plan, N)
+    _req(X, "X", torch.bfloat16, (N, H))
+    _req(L, "L", torch.int32, (N,))
+    _req(w.W_out, "W_out", torch.bfloat16, (H, V))
+    if dW_out is None:
+        dW_out = torch.empty(H, V, dtype=torch.float32, device=X.device)
+        accumulate = False
+    _req(dW_out, "dW_out", torch.float32, (H, V))
+    stats = torch.empty(stats_len(len(plan)), dtype=torch.float32, device=X.device)
+    lse = torch.empty(N, dtype=torch.float32, device=X.device)
+    dX = torch.empty_like(X)
+    nb = ctypes.c_size_t()
+    _check(ctx.lib.mst_lmhead_workspace(N, H, V, plan.M, ctypes.byref(nb)))
+    ws = ctx.workspace(nb.value)
+    _check(ctx.lib.mst_lmhead_fused(ctx.handle, _stream(X), X.data_ptr(), L.data_ptr(), w.W_out.data_ptr(), N, H, V,
+                                    plan.M, int(mode), float(grad_loss), _ptr(global_valid), stats.data_ptr(),
+                                    lse.data_ptr(), dX.data_ptr(), dW_out.data_ptr(), int(accumulate), ws.data_ptr(),
+                                    ws.numel()))
+    return stats[2], stats, lse, dX, dW_out
 
 
 # ----------------------------------------------------------------- block

@@ -225,3 +225,44 @@ def test_llama3_8b_shapes_against_torch_fp32():
     assert R.relerr(gr.W_out, ref["dWout"]) <= 1e-2
     assert R.relerr(gr.W_gate, ref["dWg"]) <= 1e-2
     assert R.relerr(gr.W_down, ref["dWd"]) <= 1e-2
+
+
+@pytest.mark.parametrize("shape", [(1024, 256, 4096, 4), (257, 64, 520, 3), (600, 128, 1000, 16)])
+def test_lmhead_fused_matches_oracle(orc, shape):
+    """Single-pass head (mst_lmhead_fused) == separate forward + backward
+    within bf16 tolerance; loss to 1e-4 relative."""
+    N, H, V, M = shape
+    c = orc.make_inputs(41, N, H, 64, V, p_ignore=0.1)
+    g = to_gpu(c)
+    head = ms.LmHeadWeights(g["Wout"])
+    plan = ms.make_chunk_plan(N, M)
+    for mode in (ms.TOKEN_WEIGHTED, ms.PAPER_MEAN):
+        loss, stats, lse, dX, dW = ms.miniseq_lmhead_fused(g["X"], g["L"], head, plan, mode, grad_loss=0.7)
+        ref_loss, ref_lse, _, _ = orc.miniseq_lmhead_forward(c["X"], c["L"], c["Wout"], M, mode)
+        rdX, rdW = orc.miniseq_lmhead_backward(c["X"], c["L"], c["Wout"], M, mode, 0.7, True)
+        assert abs(float(loss) - ref_loss) <= 1e-4 * abs(ref_loss)
+        assert np.abs(lse.cpu().numpy() - ref_lse).max() <= 2e-3 * max(1.0, np.abs(ref_lse).max())
+        assert rel(dX, rdX) <= 6e-3, rel(dX, rdX)
+        assert rel(dW, rdW) <= 4e-3, rel(dW, rdW)
+
+
+def test_block_step_fused_vs_two_pass_head():
+    """block_step with the single-pass head agrees with the two-pass head."""
+    import ctypes
+
+    torch.manual_seed(3)
+    N, H, I, V, M = 1024, 256, 512, 2048, 4
+    X = torch.randn(N, H, device="cuda").bfloat16()
+    W = [(0.05 * torch.randn(*s, device="cuda")).bfloat16() for s in ((H, I), (H, I), (I, H), (H, V))]
+    L = torch.randint(0, V, (N,), device="cuda", dtype=torch.int32)
+    mlp, head = ms.MlpWeights(*W[:3]), ms.LmHeadWeights(W[3])
+    ctx = ms.Context.get(0)
+    out = {}
+    for fused in (1, 0):
+        ms._check(ctx.lib.mst_ctx_set_tuning(ctx.handle, b"fused_head", fused))
+        st, gr = ms.block_step(X, L, mlp, head, M, M)
+        out[fused] = (float(st[2]), gr.dX.clone(), gr.W_out.clone(), gr.W_gate.clone())
+    ms._check(ctx.lib.mst_ctx_set_tuning(ctx.handle, b"fused_head", 1))
+    assert abs(out[1][0] - out[0][0]) <= 1e-5 * abs(out[0][0])
+    for a, b in zip(out[1][1:], out[0][1:]):
+        assert rel(a, b.double().cpu().numpy()) <= 6e-3
