@@ -187,6 +187,11 @@ MST_API int mst_lmhead_fused(mst_ctx* ctx, void* stream, const void* x, const in
                              const float* global_valid, float* stats, float* lse, void* grad_x, float* grad_w_out,
                              int accumulate, void* workspace, size_t workspace_bytes);
 
+/* Number of labels in [0, V) among the n labels, written to *out (device
+ * float) — the local count a sequence shard all-reduces before
+ * mst_lmhead_fused. */
+MST_API int mst_count_valid(mst_ctx* ctx, void* stream, const int32_t* labels, int64_t n, int64_t v, float* out);
+
 /* One fused MLP -> LM-Head block, forward + backward (the bench unit):
  * O = mlp(X); loss = CE(O W_out, L); then dW_out, dO, dX, dW_{gate,up,down}.
  * `stats` as in mst_lmhead_forward (device, MST_STATS_LEN(m_head) floats). */

@@ -1361,6 +1361,20 @@ int mst_lmhead_fused(mst_ctx* c, void* stream, const void* x, const int32_t* lab
   return MST_OK;
 }
 
+int mst_count_valid(mst_ctx* c, void* stream, const int32_t* labels, int64_t n, int64_t v, float* out) {
+  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  if (!labels || !out) return fail(MST_ERR_CONFIG, "NULL pointer");
+  if (n <= 0) return fail(MST_ERR_DATA, "N must be >= 1");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float* tmp = c->scratch_dev + 128;  // MST_STATS_LEN(1) scratch floats
+  chunk_valid_kernel<<<1, 1024, 0, st>>>(labels, n, 1, (int)v, tmp);
+  sum_valid_kernel<<<1, 32, 0, st>>>(tmp, 1);
+  MST_CUDA(cudaMemcpyAsync(out, tmp + 1, sizeof(float), cudaMemcpyDeviceToDevice, st));
+  c->launches += 2;
+  MST_CUDA(cudaGetLastError());
+  return MST_OK;
+}
+
 int mst_block_step(mst_ctx* c, void* stream, const void* x, const int32_t* labels, const void* wg, const void* wu,
                    const void* wd, const void* wout, int64_t n, int64_t h, int64_t i, int64_t v, int64_t m_mlp,
                    int64_t m_head, int loss_mode, float grad_loss, float* stats, void* dx, float* dwg, float* dwu,

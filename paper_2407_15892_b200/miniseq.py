@@ -117,6 +117,7 @@ _SIGS = {
                              ctypes.c_size_t], ctypes.c_int),
     "mst_lmhead_fused": ([_VP, _VP, _VP, _VP, _VP, _I64, _I64, _I64, _I64, _I32, _F32, _VP, _VP, _VP, _VP, _VP, _I32,
                           _VP, ctypes.c_size_t], ctypes.c_int),
+    "mst_count_valid": ([_VP, _VP, _VP, _I64, _I64, _VP], ctypes.c_int),
     "mst_block_step": ([_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _F32,
                         _VP, _VP, _VP, _VP, _VP, _VP, _I32, _VP, ctypes.c_size_t], ctypes.c_int),
     "mst_debug_gemm": ([_VP, _VP, _VP, _VP, _VP, _I64, _I64, _I64, _I32, _I32, _I32, _I32], ctypes.c_int),
@@ -426,6 +427,14 @@ def miniseq_lmhead_backward(saved: LmHeadSaved, w: LmHeadWeights, plan: ChunkPla
                                        gs.data_ptr(), float(grad_loss), dX.data_ptr(), dW_out.data_ptr(),
                                        int(accumulate), ws.data_ptr(), ws.numel()))
     return dX, dW_out
+
+
+def count_valid(L: torch.Tensor, V: int) -> torch.Tensor:
+    """Device count of labels in [0, V) (1-element float tensor, no sync)."""
+    ctx = Context.get(L.device.index)
+    out = torch.empty(1, dtype=torch.float32, device=L.device)
+    _check(ctx.lib.mst_count_valid(ctx.handle, _stream(L), L.data_ptr(), L.shape[0], V, out.data_ptr()))
+    return out
 
 
 def miniseq_lmhead_fused(X: torch.Tensor, L: torch.Tensor, w: LmHeadWeights, plan: ChunkPlan,

@@ -4,13 +4,12 @@ Tokens are independent through the MLP and LM-Head blocks, so each rank owns
 a contiguous sequence shard (WorkerState) and runs the full
 mini-sequence pipeline on it.  The only cross-rank traffic is:
 
-  1. the LM-Head statistics (loss sum, valid-token count): all-reduce SUM of
-     two floats between the head forward and backward, so every rank scales
-     its dlogits by the GLOBAL valid count (token-weighted loss,
-     SPEC.md:647-648) — the per-rank gradients then already sum to the
-     P=1 gradient;
+  1. the valid-token count: all-reduce SUM of one float before the LM-Head,
+     so every rank scales its dlogits by the GLOBAL count (token-weighted
+     loss) — the per-rank gradients then already sum to the
+     P=1 gradient; then the (loss sum, valid) pair for the reported loss;
   2. the weight gradients: all-reduce SUM.  dW_out is final after the head
-     backward and is reduced on a side stream while the MLP backward runs;
+     and is reduced asynchronously while the MLP backward runs;
      dW_{gate,up,down} are reduced at the end.
 
 The collective backend is whatever torch.distributed was initialised with:
@@ -60,6 +59,15 @@ class GpuOps:
         _, saved = self.ms.miniseq_lmhead_forward(O, L, self.ms.LmHeadWeights(Wout), plan)
         return saved.stats, saved
 
+    def count_valid(self, L, V):
+        return self.ms.count_valid(L, V)
+
+    def lmhead_fused(self, O, L, Wout, M, global_valid, dW_out):
+        plan = self.ms.make_chunk_plan(O.shape[0], M)
+        _, stats, _, dO, _ = self.ms.miniseq_lmhead_fused(O, L, self.ms.LmHeadWeights(Wout), plan,
+                                                          global_valid=global_valid, dW_out=dW_out)
+        return stats, dO
+
     def lmhead_backward(self, saved, Wout, global_stats, dW_out):
         return self.ms.miniseq_lmhead_backward(saved, self.ms.LmHeadWeights(Wout), saved.plan,
                                                global_stats=global_stats, dW_out=dW_out)[0]
@@ -70,21 +78,33 @@ class GpuOps:
 
 
 def sp_block_step(ops, X: torch.Tensor, L: torch.Tensor, w: tuple, Wout: torch.Tensor, M_mlp: int, M_head: int,
-                  grads: tuple, group=None, overlap: bool = True) -> StepResult:
+                  grads: tuple, group=None, overlap: bool = True, fused: bool = True) -> StepResult:
     """One sequence-parallel MLP -> LM-Head forward+backward on this rank's shard.
 
     w = (W_gate, W_up, W_down); grads = (dW_gate, dW_up, dW_down, dW_out) buffers
     (overwritten).  Returns global loss and SUM-reduced gradients."""
     world = dist.get_world_size(group) if dist.is_initialized() else 1
-    O, msaved = ops.mlp_forward(X, w, M_mlp)
-    stats, hsaved = ops.lmhead_forward(O, L, Wout, M_head)
-    gstats = stats.clone()
-    if world > 1:
-        head = gstats[:2].contiguous()
-        dist.all_reduce(head, op=dist.ReduceOp.SUM, group=group)
-        gstats[:2] = head
     dWg, dWu, dWd, dWo = grads
-    dO = ops.lmhead_backward(hsaved, Wout, gstats, dWo)
+    O, msaved = ops.mlp_forward(X, w, M_mlp)
+    if fused and hasattr(ops, "lmhead_fused"):
+        # single-pass head: the global valid count must be known up front
+        valid = ops.count_valid(L, Wout.shape[1])
+        if world > 1:
+            dist.all_reduce(valid, op=dist.ReduceOp.SUM, group=group)
+        stats, dO = ops.lmhead_fused(O, L, Wout, M_head, valid, dWo)
+        gstats = stats.clone()
+        if world > 1:
+            head = gstats[:2].contiguous()
+            dist.all_reduce(head, op=dist.ReduceOp.SUM, group=group)
+            gstats[:2] = head
+    else:
+        stats, hsaved = ops.lmhead_forward(O, L, Wout, M_head)
+        gstats = stats.clone()
+        if world > 1:
+            head = gstats[:2].contiguous()
+            dist.all_reduce(head, op=dist.ReduceOp.SUM, group=group)
+            gstats[:2] = head
+        dO = ops.lmhead_backward(hsaved, Wout, gstats, dWo)
     work = None
     if world > 1:
         # The process group runs the collective on its own stream, ordered

@@ -40,6 +40,14 @@ class OracleOps:
         dW_out.copy_(torch.from_numpy(dW))
         return torch.from_numpy(dX)
 
+    def count_valid(self, L, V):
+        return torch.tensor([float(((L >= 0) & (L < V)).sum())], dtype=torch.float64)
+
+    def lmhead_fused(self, O, L, Wout, M, global_valid, dW_out):
+        stats, saved = self.lmhead_forward(O, L, Wout, M)
+        dO = self.lmhead_backward(saved, Wout, torch.stack([stats[0], global_valid[0]]), dW_out)
+        return stats, dO
+
     def mlp_backward(self, dO, saved, w, grads):
         X, M = saved
         dX, dWg, dWu, dWd = self.orc.miniseq_mlp_backward(dO.numpy(), X.numpy(), *[t.numpy() for t in w], M)
@@ -54,7 +62,7 @@ def _inputs(orc):
     return c
 
 
-def _worker(rank, world, port, ret):
+def _worker(rank, world, port, ret, fused):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -67,7 +75,7 @@ def _worker(rank, world, port, ret):
         X, L = f(c["X"][s:e]), torch.from_numpy(c["L"][s:e].copy())
         w = (f(c["Wg"]), f(c["Wu"]), f(c["Wd"]))
         grads = tuple(torch.zeros_like(t) for t in (*w, f(c["Wout"])))
-        r = sp_block_step(OracleOps(orc), X, L, w, f(c["Wout"]), M_MLP, M_HEAD, grads)
+        r = sp_block_step(OracleOps(orc), X, L, w, f(c["Wout"]), M_MLP, M_HEAD, grads, fused=fused)
         ref = orc.block(c["X"], c["L"], c["Wg"], c["Wu"], c["Wd"], c["Wout"], M_MLP, M_HEAD, round_bf16=False)
         errs = dict(loss=abs(float(r.loss) - ref["loss"]),
                     dX=float(np.abs(r.dX.numpy() - ref["dX"][s:e]).max()),
@@ -86,11 +94,11 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world", [1, 2, 4])
-def test_sequence_parallel_matches_single_process(world, orc):
+@pytest.mark.parametrize("world,fused", [(1, True), (2, True), (4, True), (2, False)])
+def test_sequence_parallel_matches_single_process(world, fused, orc):
     mgr = mp.Manager()
     ret = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), ret), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), ret, fused), nprocs=world, join=True)
     assert len(ret) == world
     for rank, errs in ret.items():
         assert errs["loss"] <= 1e-12, (rank, errs)

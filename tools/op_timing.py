@@ -35,8 +35,7 @@ with ClockSampler(0, 0.005) as clk:
     for it in range(2):
         recs = []
         O, sv = ms.miniseq_mlp_forward(X, mlp, plan); recs.append(('mlp_fwd', ctx.take_timing_records()))
-        loss, hs = ms.miniseq_lmhead_forward(O, L, head, plan); recs.append(('head_fwd', ctx.take_timing_records()))
-        dO, _ = ms.miniseq_lmhead_backward(hs, head, plan, dW_out=dWo); recs.append(('head_bwd', ctx.take_timing_records()))
+        loss, _, _, dO, _ = ms.miniseq_lmhead_fused(O, L, head, plan, dW_out=dWo); recs.append(('head_fused', ctx.take_timing_records()))
         dX, _ = ms.miniseq_mlp_backward(dO, sv, mlp, plan, grads=grads); recs.append(('mlp_bwd', ctx.take_timing_records()))
         recs_all.append(recs)
 cs = clk.summary()
