@@ -232,21 +232,43 @@ __device__ __forceinline__ void load32(uint32_t taddr, float (&v)[32]) {
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
 }
 
-// Per-warp staging buffers: 32 rows x 128 B, SWIZZLE_128B layout (16-byte
-// chunk j of row r lives at chunk j ^ (r & 7)), matching the output tensor
-// maps so one thread per row writes conflict-free and TMA stores a box.
+// Staging buffers for the TMA-store epilogues: rows of 128 B in SWIZZLE_128B
+// layout (16-byte chunk j of row r lives at chunk j ^ (r & 7)), matching the
+// output tensor maps, so one thread per row writes conflict-free.  Buffer b
+// is a 128-row box; epilogue warp q owns rows [32q, 32q+32) of it.
+//  * per-warp mode (bf16 outputs): each warp issues its own 32-row box;
+//  * team mode (fp32 weight-gradient tiles, measured +1.8%): named barrier 1
+//    hands the box between the 4 epilogue warps and warp 0 issues one
+//    128-row TMA store / reduce-add (4x fewer, 4x larger bulk operations).
+// Modes switch only between tiles, after draining all outstanding reads.
 struct Stager {
-  uint8_t* base;  // kEpiBufs buffers of kEpiBufBytes, 1024-aligned
+  uint8_t* base;  // shared staging area (kEpiBufs x 16 KB)
   int lane;
   int next;       // round-robin buffer index
+  int q;          // epilogue warp index 0..3
+  bool team;
 
-  __device__ __forceinline__ uint8_t* buf(int b) const { return base + b * kEpiBufBytes; }
+  __device__ __forceinline__ uint8_t* buf(int b) const { return base + b * (4 * kEpiBufBytes) + q * kEpiBufBytes; }
+  __device__ __forceinline__ bool issuer() const { return team ? (q == 0 && lane == 0) : lane == 0; }
+  __device__ __forceinline__ void sync() const {
+    if (team)
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+    else
+      __syncwarp();
+  }
+  __device__ __forceinline__ void set_mode(bool want_team) {
+    if (want_team == team) return;
+    if (lane == 0) ptx::bulk_wait_read<0>();
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    team = want_team;
+    next = 0;
+  }
 
   // Claim the next buffer: the group that last read it was issued kEpiBufs
   // groups ago, so at most kEpiBufs-1 may still be pending.
   __device__ __forceinline__ int acquire() {
-    if (lane == 0) ptx::bulk_wait_read<kEpiBufs - 1>();
-    __syncwarp();
+    if (issuer()) ptx::bulk_wait_read<kEpiBufs - 1>();
+    sync();
     const int b = next;
     next = next + 1 == kEpiBufs ? 0 : next + 1;
     return b;
@@ -254,8 +276,8 @@ struct Stager {
   // Claim the next buffer while one claimed buffer is not yet issued: one
   // group fewer may be pending.
   __device__ __forceinline__ int acquire_second() {
-    if (lane == 0) ptx::bulk_wait_read<kEpiBufs - 2>();
-    __syncwarp();
+    if (issuer()) ptx::bulk_wait_read<kEpiBufs - 2>();
+    sync();
     const int b = next;
     next = next + 1 == kEpiBufs ? 0 : next + 1;
     return b;
@@ -280,40 +302,43 @@ struct Stager {
                            ptx::pack_bf16(v[8 * j + 4], v[8 * j + 5]), ptx::pack_bf16(v[8 * j + 6], v[8 * j + 7])));
   }
   // Publish buffer b to the async proxy and store (or reduce-add) it at
-  // tensor coordinates (col, row).  One bulk group per issue.
-  __device__ __forceinline__ void issue(int b, const CUtensorMap* m, int col, int row, bool reduce) const {
+  // tensor coordinates (col, this warp's first row).  One bulk group per
+  // issue.  `dw`: fp32 weight-gradient tile (evict_first hint).
+  __device__ __forceinline__ void issue(int b, const CUtensorMap* m, int col, int row, bool reduce,
+                                        bool dw = false) const {
     ptx::fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0) {
-      const uint32_t src = ptx::smem_u32(buf(b));
-      if (reduce)
-        ptx::tma_reduce_add_2d(m, src, col, row);
-      else
-        ptx::tma_store_2d(m, src, col, row);
+    sync();
+    if (issuer()) {
+      uint32_t src = ptx::smem_u32(buf(b));
+      if (team) {
+        src = ptx::smem_u32(base + b * (4 * kEpiBufBytes));
+        row -= q * 32;
+      }
+#if MST_DW_EVICT_FIRST
+      if (dw) {
+        const uint64_t pol = ptx::policy_evict_first();
+        if (reduce)
+          ptx::tma_reduce_add_2d_hint(m, src, col, row, pol);
+        else
+          ptx::tma_store_2d_hint(m, src, col, row, pol);
+      } else
+#endif
+      {
+        if (reduce)
+          ptx::tma_reduce_add_2d(m, src, col, row);
+        else
+          ptx::tma_store_2d(m, src, col, row);
+      }
       ptx::bulk_commit();
     }
   }
-  // fp32 weight-gradient tiles: touched once per chunk, so they should not
-  // displace operands that other tiles re-read.
   __device__ __forceinline__ void issue_dw(int b, const CUtensorMap* m, int col, int row, bool reduce) const {
-    ptx::fence_proxy_async_smem();
+    issue(b, m, col, row, reduce, true);
+  }
+  // All bulk groups issued by this thread have completed.
+  __device__ __forceinline__ void drain() const {
+    if (lane == 0) ptx::bulk_wait_all();
     __syncwarp();
-    if (lane == 0) {
-      const uint32_t src = ptx::smem_u32(buf(b));
-#if MST_DW_EVICT_FIRST
-      const uint64_t pol = ptx::policy_evict_first();
-      if (reduce)
-        ptx::tma_reduce_add_2d_hint(m, src, col, row, pol);
-      else
-        ptx::tma_store_2d_hint(m, src, col, row, pol);
-#else
-      if (reduce)
-        ptx::tma_reduce_add_2d(m, src, col, row);
-      else
-        ptx::tma_store_2d(m, src, col, row);
-#endif
-      ptx::bulk_commit();
-    }
   }
 };
 
@@ -327,6 +352,7 @@ __device__ __forceinline__ void run_epilogue(const GemmParams& p, const ProblemD
   const int lane = st.lane;
   const int row = row0 + lane;
   const bool row_ok = row < P.rows;
+  st.set_mode(P.epi == kEpiAccF32);  // fp32 dW tiles: one 128-row box per slice
   switch (P.epi) {
     case kEpiStoreBf16: {
       const int half = P.ph[0].umma_n >> 1;
@@ -749,7 +775,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     const uint32_t tempty_leader0 = ptx::mapa(ptx::smem_u32(&tempty[0]), 0);
     const uint32_t tempty_leader1 = ptx::mapa(ptx::smem_u32(&tempty[1]), 0);
-    epi::Stager st{smem_epi + (warp - 4) * kEpiBufs * kEpiBufBytes, lane, 0};
+    epi::Stager st{smem_epi, lane, 0, q, false};
     MST_PROF_DECL
     for (;;) {
       const int32_t code = feed.consume(p, lane);
@@ -772,8 +798,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         acc_phase ^= 1;
       }
     }
-    if (lane == 0) ptx::bulk_wait_all();
-    __syncwarp();
+    st.drain();
     if (lane == 0) MST_PROF_FLUSH(5, 2);
   }
 

@@ -204,7 +204,11 @@ int map_index(int encoded) { return -(encoded + 100); }
 // (64 bf16 or 32 fp32 columns), SWIZZLE_128B.  Returns the map index via *idx.
 int add_out_map(mst_ctx* c, Launch& L, void* base, int64_t cols, int64_t rows, int64_t ld, bool f32, int32_t* idx) {
   if (L.nmaps >= mst::kMaxMaps) return fail(MST_ERR_INTERNAL, "too many tensor maps in one launch");
-  MST_TRY(tmap_2d(c, &L.p.maps[L.nmaps], base, (uint64_t)cols, (uint64_t)rows, (uint64_t)ld, f32 ? 32 : 64, 32, f32));
+  // fp32 (weight-gradient) tiles are staged by the 4 epilogue warps together:
+  // one box per 128-row CTA slice; bf16 outputs: one 32-row box per warp.
+  const uint32_t box_rows = f32 ? 128 : 32;
+  MST_TRY(tmap_2d(c, &L.p.maps[L.nmaps], base, (uint64_t)cols, (uint64_t)rows, (uint64_t)ld, f32 ? 32 : 64, box_rows,
+                  f32));
   *idx = L.nmaps++;
   return MST_OK;
 }
