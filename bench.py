@@ -357,8 +357,9 @@ def main() -> None:
     executed_fpt = gemm_flops / args.steps / S if gemm_flops else flops_per_token()
     tflops_step = tokens_step / world * executed_fpt / (ms_step / 1e3) / 1e12
     ws_m1 = ms.block_workspace_bytes(S, H, I, V, 1, 1)
-    nc = lambda n, m: math.ceil(n / min(n, m))  # noqa: E731
-    inter = lambda mm, mh: max(3 * nc(S, mm) * I * 2, nc(S, mh) * V * 2)  # noqa: E731
+    # block workspace = O, dO, lse ([S]-sized activations) + the chunk buffers
+    act_fixed = 2 * S * H * 2 + S * 4
+    inter = lambda mm, mh: ms.block_workspace_bytes(S, H, I, V, mm, mh) - act_fixed  # noqa: E731
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",

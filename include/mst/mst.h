@@ -130,7 +130,10 @@ MST_API int mst_ctx_set_profile_buffer(mst_ctx* ctx, void* dev_counters);
  *   "ksplit9": 2 = MLP dX as two fp32 partial GEMMs + combine, 1 = fused;
  *   "tma3d":   MN-major operands as 3-D tensor maps (process-wide);
  *   "fused_head": 1 (default) block_step runs mst_lmhead_fused, 0 runs the
- *              separate forward + backward (logits recomputed).
+ *              separate forward + backward (logits recomputed);
+ *   "chunked_block": 1 (default) block_step with M_mlp == M_head runs the
+ *              chunk-wise MLP -> head -> MLP-backward schedule (no G,U
+ *              recompute; bitwise-equal results), 0 the op-by-op schedule.
  * Unknown keys are MST_ERR_CONFIG.  Changing a knob clears the schedule cache. */
 MST_API int mst_ctx_set_tuning(mst_ctx* ctx, const char* key, int value);
 

@@ -74,6 +74,7 @@ enum EpiKind : int32_t {
   kEpiCeFwd = 4,      // per-row (max, sumexp) partial + target logit
   kEpiCeBwd = 5,      // dlogits = (softmax - onehot) * scale              (TMA store)
   kEpiCeFwdNum = 6,   // kEpiCeFwd + softmax numerator 2^(z log2e - m_tile) (TMA store, bf16)
+  kEpiSwigluSave = 7, // kEpiSwiglu + G, U saved in fp32 (chunk-wise block: no backward recompute)
 };
 
 struct PhaseDesc {
@@ -433,6 +434,33 @@ __device__ __forceinline__ void run_epilogue(const GemmParams& p, const ProblemD
           st.put_bf16x32(b, s, gv);
         }
         st.issue(b, m, tn * 128 + c, row0, false);
+      }
+      break;
+    }
+    case kEpiSwigluSave: {
+      // D = [G (128) | U (128)] -> h (bf16) and the accumulators G, U (fp32,
+      // exactly what the backward recompute would produce).
+      for (int c = 0; c < 128; c += 64) {
+        float hk[2][32];
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          float gv[32], uv[32];
+          epi::load32(taddr + c + 32 * s, gv);
+          epi::load32(taddr + 128 + c + 32 * s, uv);
+          const int col = tn * 128 + c + 32 * s;
+          int b = st.acquire();
+          st.put_f32x32(b, gv);
+          st.issue(b, &p.maps[P.map_out1], col, row0, false);
+          b = st.acquire();
+          st.put_f32x32(b, uv);
+          st.issue(b, &p.maps[P.map_out2], col, row0, false);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) hk[s][j] = (gv[j] * epi::sigmoid(gv[j])) * uv[j];
+        }
+        const int b = st.acquire();
+        st.put_bf16x32(b, 0, hk[0]);
+        st.put_bf16x32(b, 1, hk[1]);
+        st.issue(b, &p.maps[P.map_out0], tn * 128 + c, row0, false);
       }
       break;
     }

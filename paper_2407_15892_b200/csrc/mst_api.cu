@@ -117,6 +117,7 @@ struct mst_ctx {
   int ksplit5 = 1;     // split-K of the LM-Head dX GEMM (K5): 1, 2 or 4
   int ksplit9 = 1;     // MLP dX GEMM (K9): 1 = two-phase accumulate, 2 = one problem per phase + combine
   int fused_head = 1;  // block_step: single-pass LM-Head forward+backward (mst_lmhead_fused)
+  int chunked_block = 1;  // block_step with M_mlp == M_head: chunk-wise MLP -> head -> MLP-backward schedule
 };
 
 namespace {
@@ -202,11 +203,12 @@ int map_index(int encoded) { return -(encoded + 100); }
 
 // Output tensor map for the epilogue's TMA stores: 32-row x 128-byte boxes
 // (64 bf16 or 32 fp32 columns), SWIZZLE_128B.  Returns the map index via *idx.
-int add_out_map(mst_ctx* c, Launch& L, void* base, int64_t cols, int64_t rows, int64_t ld, bool f32, int32_t* idx) {
+int add_out_map(mst_ctx* c, Launch& L, void* base, int64_t cols, int64_t rows, int64_t ld, bool f32, int32_t* idx,
+                bool team = true) {
   if (L.nmaps >= mst::kMaxMaps) return fail(MST_ERR_INTERNAL, "too many tensor maps in one launch");
-  // fp32 (weight-gradient) tiles are staged by the 4 epilogue warps together:
-  // one box per 128-row CTA slice; bf16 outputs: one 32-row box per warp.
-  const uint32_t box_rows = f32 ? 128 : 32;
+  // fp32 weight-gradient tiles are staged by the 4 epilogue warps together:
+  // one box per 128-row CTA slice; everything else: one 32-row box per warp.
+  const uint32_t box_rows = (f32 && team) ? 128 : 32;
   MST_TRY(tmap_2d(c, &L.p.maps[L.nmaps], base, (uint64_t)cols, (uint64_t)rows, (uint64_t)ld, f32 ? 32 : 64, box_rows,
                   f32));
   *idx = L.nmaps++;
@@ -612,6 +614,33 @@ __global__ void normalize_dlogits_kernel(uint16_t* __restrict__ dl, int64_t ld, 
   *p = w;
 }
 
+// SwiGLU backward from the saved fp32 accumulators (chunk-wise block):
+// same arithmetic as the kEpiSwigluBwd epilogue, so results are bitwise
+// those of the recompute path.  dG, dU bf16.
+__device__ __forceinline__ float sig_rn(float x) { return __frcp_rn(1.0f + __expf(-x)); }
+__global__ void swiglu_bwd_kernel(const float* __restrict__ G, const float* __restrict__ U,
+                                  const float* __restrict__ dh, uint16_t* __restrict__ dG, uint16_t* __restrict__ dU,
+                                  int64_t n4) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n4) return;
+  const float4 g = reinterpret_cast<const float4*>(G)[i];
+  const float4 u = reinterpret_cast<const float4*>(U)[i];
+  const float4 d = reinterpret_cast<const float4*>(dh)[i];
+  const float gv[4] = {g.x, g.y, g.z, g.w}, uv[4] = {u.x, u.y, u.z, u.w}, dv[4] = {d.x, d.y, d.z, d.w};
+  uint16_t og[4], ou[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float s_ = sig_rn(gv[k]);
+    const float act = gv[k] * s_;
+    const float dgv = dv[k] * uv[k] * (s_ * (1.0f + gv[k] * (1.0f - s_)));
+    const float duv = dv[k] * act;
+    og[k] = __bfloat16_as_ushort(__float2bfloat16_rn(dgv));
+    ou[k] = __bfloat16_as_ushort(__float2bfloat16_rn(duv));
+  }
+  reinterpret_cast<uint2*>(dG)[i] = make_uint2(og[0] | ((uint32_t)og[1] << 16), og[2] | ((uint32_t)og[3] << 16));
+  reinterpret_cast<uint2*>(dU)[i] = make_uint2(ou[0] | ((uint32_t)ou[1] << 16), ou[2] | ((uint32_t)ou[3] << 16));
+}
+
 // ------------------------------------------------------------ validation
 int check_dims(int64_t n, int64_t h, int64_t x, int64_t m, const char* xname) {
   if (n <= 0) return fail(MST_ERR_DATA, "N must be >= 1 (SPEC.md:290), got %lld", (long long)n);
@@ -760,6 +789,72 @@ int splitk_combine(mst_ctx* c, cudaStream_t st, const float* part, int splits, i
   return MST_OK;
 }
 
+// K9 (dX_j = dG W_g^T + dU W_u^T), K8 (dW_d += h^T dO_j) and K10
+// ([dW_g | dW_u] += X_j^T [dG | dU]) of one chunk: mutually independent,
+// added to one grouped launch (Alg. 3 lines 5-7).
+int add_mlp_grads(mst_ctx* c, Launch& L, const void* dg, const void* du, const void* ht, const void* xt,
+                  const void* doj, const void* wg, const void* wu, void* dxj, float* dwg, float* dwu, float* dwd,
+                  int64_t rows, int64_t h, int64_t i, int64_t ldt, int beta, float* part9) {
+  if (c->ksplit9 > 1) {  // K9 as two fp32 partial GEMMs (dG W_g^T, dU W_u^T) + combine
+    MST_TRY(build_plain_splitk(c, L, Operand{dg, rows, i, i, false}, Operand{wg, h, i, i, false}, part9, h, 1));
+    MST_TRY(build_plain_splitk(c, L, Operand{du, rows, i, i, false}, Operand{wu, h, i, i, false}, part9 + rows * h,
+                               h, 1));
+  } else {  // K9: one accumulator over both phases (B K-major)
+    ProblemDesc& P = L.p.prob[L.p.num_problems++];
+    PhaseSpec q0{};
+    q0.a = {dg, rows, i, i, false};
+    q0.b0 = {wg, h, i, i, false};
+    q0.b1 = q0.b0;
+    q0.umma_n = 256;
+    q0.b_off1 = 128;
+    MST_TRY(add_phase(c, L, P, q0));
+    PhaseSpec q1 = q0;
+    q1.a = {du, rows, i, i, false};
+    q1.b0 = {wu, h, i, i, false};
+    q1.b1 = q1.b0;
+    q1.acc_continue = true;
+    MST_TRY(add_phase(c, L, P, q1));
+    P.m_tiles = (int)cdiv(rows, 256);
+    P.tile_n = 256;
+    P.n_tiles = (int)cdiv(h, 256);
+    P.rows = (int)rows;
+    P.cols = (int)h;
+    P.epi = mst::kEpiStoreBf16;
+    MST_TRY(add_out_map(c, L, dxj, h, rows, h, false, &P.map_out0));
+    P.map_out1 = P.map_out0;
+    P.col_off0 = 0;
+    P.col_off1 = 128;
+    L.flops += 2.0 * 2.0 * rows * h * i;
+  }
+  // K8: dW_d[I,H] += h^T dO_j (A = h^T, K-major)
+  MST_TRY(build_plain(c, L, Operand{ht, i, rows, ldt, false}, Operand{doj, h, rows, h, true}, dwd, h, mst::kEpiAccF32,
+                      beta));
+  {  // K10: [dW_g | dW_u][H, I] += X_j^T [dG | dU]  (A = X_j^T, K-major)
+    ProblemDesc& P = L.p.prob[L.p.num_problems++];
+    PhaseSpec q{};
+    q.a = {xt, h, rows, ldt, false};
+    q.b0 = {dg, i, rows, i, true};
+    q.b1 = {du, i, rows, i, true};
+    q.umma_n = 256;
+    MST_TRY(add_phase(c, L, P, q));
+    P.m_tiles = (int)cdiv(h, 256);
+    P.tile_n = 128;
+    P.n_tiles = (int)cdiv(i, 128);
+    P.rows = (int)h;
+    P.cols = (int)i;
+    P.epi = mst::kEpiAccF32;
+    P.beta = beta;
+    MST_TRY(add_out_map(c, L, dwg, i, h, i, true, &P.map_out0));
+    MST_TRY(add_out_map(c, L, dwu, i, h, i, true, &P.map_out1));
+    P.out0 = dwg;
+    P.out1 = dwu;
+    P.ld0 = P.ld1 = i;
+    P.col_off0 = P.col_off1 = 0;
+    L.flops += 2.0 * h * (2.0 * i) * rows;
+  }
+  return MST_OK;
+}
+
 }  // namespace
 
 // =================================================================== C ABI
@@ -900,6 +995,8 @@ int mst_ctx_set_tuning(mst_ctx* c, const char* key, int value) {
     c->ksplit9 = value;
   } else if (std::strcmp(key, "fused_head") == 0) {
     c->fused_head = value != 0;
+  } else if (std::strcmp(key, "chunked_block") == 0) {
+    c->chunked_block = value != 0;
   } else if (std::strcmp(key, "tma3d") == 0) {
     c3d_enabled = value != 0;
   } else {
@@ -985,11 +1082,19 @@ int mst_lmhead_workspace(int64_t n, int64_t h, int64_t v, int64_t m, size_t* byt
 
 static size_t block_fixed_bytes(int64_t n, int64_t h) { return align_up(size_t(n) * h * 2, 256) * 2 + align_up(size_t(n) * 4, 256); }
 
+// Chunk-wise block (M_mlp == M_head): MLP and head chunk buffers coexist,
+// plus the forward's fp32 G, U accumulators of one chunk.
+static size_t chunked_extra_bytes(int64_t n, int64_t i, int64_t m) {
+  return 2 * align_up(size_t(max_chunk(n, m)) * i * 4, 256) + 512;
+}
+
 int mst_block_workspace(int64_t n, int64_t h, int64_t i, int64_t v, int64_t m_mlp, int64_t m_head, size_t* bytes) {
   size_t a = 0, b = 0;
   MST_TRY(mst_mlp_workspace(n, h, i, m_mlp, &a));
   MST_TRY(mst_lmhead_workspace(n, h, v, m_head, &b));
-  *bytes = block_fixed_bytes(n, h) + 256 + std::max(a, b);
+  const size_t two_pass = block_fixed_bytes(n, h) + 256 + std::max(a, b);
+  const size_t chunked = m_mlp == m_head ? block_fixed_bytes(n, h) + 256 + a + b + chunked_extra_bytes(n, i, m_mlp) : 0;
+  *bytes = std::max(two_pass, chunked);
   return MST_OK;
 }
 
@@ -1109,63 +1214,8 @@ int mst_mlp_backward(mst_ctx* c, void* stream, const void* dout, const mst_mlp_s
     MST_TRY(transpose_bf16(c, st, xj, h, xt, ldt, rows, h));
     {  // K9 + K8 + K10 (mutually independent) + K7a of the next chunk, one launch.
       Launch L;
-      if (c->ksplit9 > 1) {  // K9 as two fp32 partial GEMMs (dG W_g^T, dU W_u^T) + combine
-        MST_TRY(build_plain_splitk(c, L, Operand{dg, rows, i, i, false}, Operand{wg, h, i, i, false}, part9, h, 1));
-        MST_TRY(build_plain_splitk(c, L, Operand{du, rows, i, i, false}, Operand{wu, h, i, i, false},
-                                   part9 + rows * h, h, 1));
-      } else {  // K9: dX_j = dG W_g^T + dU W_u^T (B K-major), one accumulator over both phases.
-        ProblemDesc& P = L.p.prob[L.p.num_problems++];
-        PhaseSpec q0{};
-        q0.a = {dg, rows, i, i, false};
-        q0.b0 = {wg, h, i, i, false};
-        q0.b1 = q0.b0;
-        q0.umma_n = 256;
-        q0.b_off1 = 128;
-        MST_TRY(add_phase(c, L, P, q0));
-        PhaseSpec q1 = q0;
-        q1.a = {du, rows, i, i, false};
-        q1.b0 = {wu, h, i, i, false};
-        q1.b1 = q1.b0;
-        q1.acc_continue = true;
-        MST_TRY(add_phase(c, L, P, q1));
-        P.m_tiles = (int)cdiv(rows, 256);
-        P.tile_n = 256;
-        P.n_tiles = (int)cdiv(h, 256);
-        P.rows = (int)rows;
-        P.cols = (int)h;
-        P.epi = mst::kEpiStoreBf16;
-        MST_TRY(add_out_map(c, L, const_cast<char*>(bptr(dx, r0 * h)), h, rows, h, false, &P.map_out0));
-        P.map_out1 = P.map_out0;
-        P.col_off0 = 0;
-        P.col_off1 = 128;
-        L.flops += 2.0 * 2.0 * rows * h * i;
-      }
-      // K8: dW_d[I,H] += h^T dO_j
-      MST_TRY(build_plain(c, L, Operand{ht, i, rows, ldt, false}, Operand{doj, h, rows, h, true}, dwd, h,
-                          mst::kEpiAccF32, beta));
-      {  // K10: [dW_g | dW_u][H, I] += X_j^T [dG | dU]
-        ProblemDesc& P = L.p.prob[L.p.num_problems++];
-        PhaseSpec q{};
-        q.a = {xt, h, rows, ldt, false};
-        q.b0 = {dg, i, rows, i, true};
-        q.b1 = {du, i, rows, i, true};
-        q.umma_n = 256;
-        MST_TRY(add_phase(c, L, P, q));
-        P.m_tiles = (int)cdiv(h, 256);
-        P.tile_n = 128;
-        P.n_tiles = (int)cdiv(i, 128);
-        P.rows = (int)h;
-        P.cols = (int)i;
-        P.epi = mst::kEpiAccF32;
-        P.beta = beta;
-        MST_TRY(add_out_map(c, L, dwg, i, h, i, true, &P.map_out0));
-        MST_TRY(add_out_map(c, L, dwu, i, h, i, true, &P.map_out1));
-        P.out0 = dwg;
-        P.out1 = dwu;
-        P.ld0 = P.ld1 = i;
-        P.col_off0 = P.col_off1 = 0;
-        L.flops += 2.0 * h * (2.0 * i) * rows;
-      }
+      MST_TRY(add_mlp_grads(c, L, dg, du, ht, xt, doj, wg, wu, const_cast<char*>(bptr(dx, r0 * h)), dwg, dwu, dwd,
+                            rows, h, i, ldt, beta, part9));
       if (j + 1 < nch) MST_TRY(add_k7a(L, j + 1));
       MST_TRY(launch(c, st, L));
       if (c->ksplit9 > 1) MST_TRY(splitk_combine(c, st, part9, 2, rows, h, const_cast<char*>(bptr(dx, r0 * h)), h));
@@ -1379,13 +1429,162 @@ int mst_count_valid(mst_ctx* c, void* stream, const int32_t* labels, int64_t n, 
   return MST_OK;
 }
 
+// Chunk-wise block schedule (block_step when M_mlp == M_head).  With the
+// single-pass head, chunk j of the LM-Head needs only O_j, so each chunk
+// runs MLP forward -> head forward+backward -> MLP backward.  The forward's
+// fp32 G, U accumulators are kept for the chunk's backward, so the
+// backward's G,U recompute GEMM becomes an elementwise pass (bitwise the
+// same values: same tiles, same K order).  K8/K9/K10 of chunk j-1 share a
+// launch with K2 of chunk j.  Chunk buffers of both blocks coexist (peak
+// intermediate = one MLP chunk + one head chunk).
+static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const int32_t* labels, const void* wg,
+                              const void* wu, const void* wd, const void* wout, int64_t n, int64_t h, int64_t i,
+                              int64_t v, int64_t m, int loss_mode, float grad_loss, float* stats, void* dx, float* dwg,
+                              float* dwu, float* dwd, float* dwout, int accumulate, void* ws, size_t ws_bytes) {
+  char* base = static_cast<char*>(ws);
+  const size_t ob = align_up(size_t(n) * h * 2, 256);
+  void* o = base;
+  void* dO = base + ob;
+  float* lse = reinterpret_cast<float*>(base + 2 * ob);
+  Carve cv{base + block_fixed_bytes(n, h) + 256, ws_bytes, 0, false};
+  void *hb, *dg, *du, *xt, *ht, *dl, *ot;
+  float *dhb, *part9, *zt, *lrow, *scales, *part5;
+  float2* part;
+  carve_mlp(cv, n, h, i, m, &hb, &dg, &du, &dhb, &xt, &ht, &part9);
+  carve_head(cv, n, h, v, m, &part, &zt, &lrow, &dl, &scales, &ot, &part5);
+  float* g32 = static_cast<float*>(cv.take(size_t(max_chunk(n, m)) * i * 4));
+  float* u32 = static_cast<float*>(cv.take(size_t(max_chunk(n, m)) * i * 4));
+  const int64_t ldt = ld_t(n, m);
+  const std::vector<int64_t> b = plan_bounds(n, m);
+  const int nch = (int)b.size() - 1;
+  const int nparts = (int)cdiv(v, 256);
+  // dlogits scales depend only on the labels: compute them up front.
+  MST_CUDA(cudaMemsetAsync(stats, 0, sizeof(float) * MST_STATS_LEN(nch), st));
+  chunk_valid_kernel<<<nch, 256, 0, st>>>(labels, n, nch, (int)v, stats);
+  sum_valid_kernel<<<1, 32, 0, st>>>(stats, nch);
+  grad_scale_kernel<<<(nch + 255) / 256, 256, 0, st>>>(stats, stats, nch, loss_mode, grad_loss, scales);
+  c->launches += 3;
+  auto rows_of = [&](int j) { return b[j + 1] - b[j]; };
+  auto add_k1s = [&](Launch& L, int j) -> int {  // K1 saving G, U (fp32) and h (bf16)
+    const int64_t rows = rows_of(j);
+    ProblemDesc& P = L.p.prob[L.p.num_problems++];
+    PhaseSpec s{};
+    s.a = {bptr(x, b[j] * h), rows, h, h, false};
+    s.b0 = {wg, i, h, i, true};
+    s.b1 = {wu, i, h, i, true};
+    s.umma_n = 256;
+    MST_TRY(add_phase(c, L, P, s));
+    P.m_tiles = (int)cdiv(rows, 256);
+    P.tile_n = 128;
+    P.n_tiles = (int)cdiv(i, 128);
+    P.rows = (int)rows;
+    P.cols = (int)i;
+    P.epi = mst::kEpiSwigluSave;
+    MST_TRY(add_out_map(c, L, hb, i, rows, i, false, &P.map_out0));
+    MST_TRY(add_out_map(c, L, g32, i, rows, i, true, &P.map_out1, false));
+    MST_TRY(add_out_map(c, L, u32, i, rows, i, true, &P.map_out2, false));
+    L.flops += 2.0 * rows * (2.0 * i) * h;
+    return MST_OK;
+  };
+  auto add_grads = [&](Launch& L, int j) -> int {
+    const int64_t rows = rows_of(j);
+    const int beta = (j > 0 || accumulate) ? 1 : 0;
+    return add_mlp_grads(c, L, dg, du, ht, xt, bptr(dO, b[j] * h), wg, wu, const_cast<char*>(bptr(dx, b[j] * h)),
+                         dwg, dwu, dwd, rows, h, i, ldt, beta, part9);
+  };
+  {
+    Launch L;
+    MST_TRY(add_k1s(L, 0));
+    MST_TRY(launch(c, st, L));
+  }
+  for (int j = 0; j < nch; ++j) {
+    const int64_t r0 = b[j], rows = rows_of(j);
+    const int beta = (j > 0 || accumulate) ? 1 : 0;
+    void* oj = const_cast<char*>(bptr(o, r0 * h));
+    void* doj = const_cast<char*>(bptr(dO, r0 * h));
+    {  // K2(j) + the weight/input gradients of chunk j-1
+      Launch L;
+      MST_TRY(build_plain(c, L, Operand{hb, rows, i, i, false}, Operand{wd, h, i, h, true}, oj, h, mst::kEpiStoreBf16,
+                          0));
+      if (j > 0) MST_TRY(add_grads(L, j - 1));
+      MST_TRY(launch(c, st, L));
+      if (j > 0 && c->ksplit9 > 1)
+        MST_TRY(splitk_combine(c, st, part9, 2, rows_of(j - 1), h, const_cast<char*>(bptr(dx, b[j - 1] * h)), h));
+    }
+    MST_TRY(transpose_bf16(c, st, oj, h, ot, ldt, rows, h));
+    {  // K3': logits GEMM, partials + softmax numerators
+      Launch L;
+      MST_TRY(build_plain(c, L, Operand{oj, rows, h, h, false}, Operand{wout, v, h, v, true}, dl, v,
+                          mst::kEpiCeFwdNum, 0));
+      ProblemDesc& P = L.p.prob[0];
+      P.labels = labels + r0;
+      P.part = part;
+      P.ztarget = zt;
+      P.nparts = nparts;
+      MST_TRY(launch(c, st, L));
+    }
+    ce_combine_kernel<<<(unsigned)cdiv(rows * 32, 256), 256, 0, st>>>(part, nparts, zt, labels + r0, (int)rows, (int)v,
+                                                                     lse + r0, lrow, stats + 3);
+    chunk_reduce_kernel<<<1, 1024, 0, st>>>(lrow, labels + r0, (int)rows, (int)v, stats + 4 + j, stats + 4 + nch + j);
+    normalize_dlogits_kernel<<<(unsigned)cdiv(rows * (v / 8), 256), 256, 0, st>>>(
+        static_cast<uint16_t*>(dl), v, (int)rows, (int)v, part, nparts, lse + r0, labels + r0, scales + j);
+    c->launches += 3;
+    {  // K5 + K6
+      Launch L;
+      MST_TRY(build_plain(c, L, Operand{dl, rows, v, v, false}, Operand{wout, h, v, v, false}, doj, h,
+                          mst::kEpiStoreBf16, 0));
+      MST_TRY(build_plain(c, L, Operand{ot, h, rows, ldt, false}, Operand{dl, v, rows, v, true}, dwout, v,
+                          mst::kEpiAccF32, beta));
+      MST_TRY(launch(c, st, L));
+    }
+    {  // K7a: dh = dO_j W_d^T (fp32)
+      Launch L;
+      MST_TRY(build_plain(c, L, Operand{doj, rows, h, h, false}, Operand{wd, i, h, h, false}, dhb, i,
+                          mst::kEpiAccF32, 0));
+      MST_TRY(launch(c, st, L));
+    }
+    {  // SwiGLU backward from the saved accumulators
+      const int64_t n4 = rows * i / 4;
+      swiglu_bwd_kernel<<<(unsigned)cdiv(n4, 256), 256, 0, st>>>(g32, u32, dhb, static_cast<uint16_t*>(dg),
+                                                                 static_cast<uint16_t*>(du), n4);
+      c->launches += 1;
+    }
+    MST_TRY(transpose_bf16(c, st, hb, i, ht, ldt, rows, i));
+    MST_TRY(transpose_bf16(c, st, bptr(x, r0 * h), h, xt, ldt, rows, h));
+    if (j + 1 < nch) {
+      Launch L;
+      MST_TRY(add_k1s(L, j + 1));
+      MST_TRY(launch(c, st, L));
+    }
+  }
+  {
+    Launch L;
+    MST_TRY(add_grads(L, nch - 1));
+    MST_TRY(launch(c, st, L));
+    if (c->ksplit9 > 1)
+      MST_TRY(splitk_combine(c, st, part9, 2, rows_of(nch - 1), h, const_cast<char*>(bptr(dx, b[nch - 1] * h)), h));
+  }
+  finalize_loss_kernel<<<1, 32, 0, st>>>(stats, nch, loss_mode);
+  c->launches += 1;
+  MST_CUDA(cudaGetLastError());
+  return MST_OK;
+}
+
 int mst_block_step(mst_ctx* c, void* stream, const void* x, const int32_t* labels, const void* wg, const void* wu,
                    const void* wd, const void* wout, int64_t n, int64_t h, int64_t i, int64_t v, int64_t m_mlp,
                    int64_t m_head, int loss_mode, float grad_loss, float* stats, void* dx, float* dwg, float* dwu,
                    float* dwd, float* dwout, int accumulate, void* ws, size_t ws_bytes) {
+  if (!c) return fail(MST_ERR_STATE, "NULL context");
   size_t need = 0;
   MST_TRY(mst_block_workspace(n, h, i, v, m_mlp, m_head, &need));
   if (!ws || ws_bytes < need) return fail(MST_ERR_CONFIG, "workspace too small (%zu < %zu)", ws_bytes, need);
+  if (loss_mode != MST_LOSS_TOKEN_WEIGHTED && loss_mode != MST_LOSS_PAPER_MEAN)
+    return fail(MST_ERR_CONFIG, "unknown loss mode %d", loss_mode);
+  if (!x || !labels || !wg || !wu || !wd || !wout || !stats || !dx || !dwg || !dwu || !dwd || !dwout)
+    return fail(MST_ERR_CONFIG, "NULL tensor pointer");
+  if (c->chunked_block && c->fused_head && m_mlp == m_head)
+    return block_step_chunked(c, static_cast<cudaStream_t>(stream), x, labels, wg, wu, wd, wout, n, h, i, v, m_mlp,
+                              loss_mode, grad_loss, stats, dx, dwg, dwu, dwd, dwout, accumulate, ws, ws_bytes);
   char* base = static_cast<char*>(ws);
   const size_t ob = align_up(size_t(n) * h * 2, 256);
   void* o = base;

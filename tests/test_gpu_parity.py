@@ -266,3 +266,29 @@ def test_block_step_fused_vs_two_pass_head():
     assert abs(out[1][0] - out[0][0]) <= 1e-5 * abs(out[0][0])
     for a, b in zip(out[1][1:], out[0][1:]):
         assert rel(a, b.double().cpu().numpy()) <= 6e-3
+
+
+@pytest.mark.parametrize("shape", [(1024, 256, 688, 4096, 4), (777, 64, 136, 520, 3)])
+def test_block_step_chunked_matches_op_by_op(shape):
+    """Chunk-wise block schedule (saved G,U, no recompute) == op-by-op
+    schedule: same kernels and accumulation orders, so agreement is at
+    fp32-rounding level (FMA contraction may differ in the SwiGLU backward)."""
+    N, H, I, V, M = shape
+    torch.manual_seed(7)
+    X = torch.randn(N, H, device="cuda").bfloat16()
+    W = [(0.05 * torch.randn(*s, device="cuda")).bfloat16() for s in ((H, I), (H, I), (I, H), (H, V))]
+    L = torch.randint(0, V, (N,), device="cuda", dtype=torch.int32)
+    L[::9] = -100
+    mlp, head = ms.MlpWeights(*W[:3]), ms.LmHeadWeights(W[3])
+    ctx = ms.Context.get(0)
+    out = {}
+    for chunked in (1, 0):
+        ms._check(ctx.lib.mst_ctx_set_tuning(ctx.handle, b"chunked_block", chunked))
+        st, gr = ms.block_step(X, L, mlp, head, M, M)
+        torch.cuda.synchronize()
+        out[chunked] = (float(st[2]), gr.dX.clone(), gr.W_gate.clone(), gr.W_up.clone(), gr.W_down.clone(),
+                        gr.W_out.clone())
+    ms._check(ctx.lib.mst_ctx_set_tuning(ctx.handle, b"chunked_block", 1))
+    assert out[1][0] == out[0][0]
+    for a, b in zip(out[1][1:], out[0][1:]):
+        assert rel(a, b.double().cpu().numpy()) <= 1e-5
