@@ -48,6 +48,15 @@ namespace mst {
 #ifndef MST_DW_RED_GLOBAL
 #define MST_DW_RED_GLOBAL 0  // 1: fp32 dW accumulation with red.global.add.v4.f32 from registers
 #endif
+// Diagnostic builds only (tools/pipe_limits.py): MST_DIAG_NO_MMA skips the
+// tcgen05.mma issue (commits still arrive), MST_DIAG_NO_TMA replaces the
+// operand loads with plain barrier arrivals.  Results are garbage.
+#ifndef MST_DIAG_NO_MMA
+#define MST_DIAG_NO_MMA 0
+#endif
+#ifndef MST_DIAG_NO_TMA
+#define MST_DIAG_NO_TMA 0
+#endif
 #ifndef MST_DW_EVICT_FIRST
 #define MST_DW_EVICT_FIRST 1  // fp32 dW stores / reduce-adds stream through L2 with evict_first
 #endif
@@ -713,6 +722,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int kb = 0; kb < d.k_blocks; ++kb) {
             MST_PROF_WAIT(0, ptx::mbar_wait(ptx::smem_u32(&empty[stage]), phase ^ 1));
             const uint32_t fbar_local = ptx::smem_u32(&full[stage]);
+#if MST_DIAG_NO_TMA
+            if (rank == 0 && do_a) ptx::mbar_arrive_local(fbar_local);
+            (void)stage_tx;
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+#endif
             if (rank == 0 && do_a) ptx::mbar_arrive_expect_tx(fbar_local, stage_tx);
             const uint32_t fbar = ptx::mapa(fbar_local, 0);
             const uint32_t sa = ptx::smem_u32(smem_a + stage * kABytes);
@@ -779,7 +797,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               const uint64_t bdesc =
                   d.b_mn ? ptx::sdesc_sw128(sb + k * 2048, 8192, 1024) : ptx::sdesc_sw128(sb + k * 32, 16, 1024);
               const uint32_t accum = (kb > 0 || k > 0 || d.acc_continue) ? 1u : 0u;
-              ptx::umma_bf16_cg2(d_tmem, adesc, bdesc, idesc, accum);
+              if (!MST_DIAG_NO_MMA) ptx::umma_bf16_cg2(d_tmem, adesc, bdesc, idesc, accum);
             }
             ptx::umma_commit_cg2_mc(ptx::smem_u32(&empty[stage]), 0x3);
             if (++stage == kStages) {

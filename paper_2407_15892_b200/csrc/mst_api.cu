@@ -101,6 +101,7 @@ struct mst_ctx {
   int device = 0;
   int num_sms = 0;
   int num_pairs = 0;
+  int max_pairs = 0;
   EncodeTiledFn encode = nullptr;
   std::map<std::string, SchedEntry> sched_cache;
   int64_t launches = 0;
@@ -911,6 +912,7 @@ int mst_ctx_create(int device, mst_ctx** out) {
   e = cudaOccupancyMaxActiveClusters(&clusters, mst::mst_grouped_gemm_kernel, &cfg);
   if (e != cudaSuccess || clusters <= 0) clusters = c->num_sms / 2;
   c->num_pairs = std::min(clusters, c->num_sms / 2);
+  c->max_pairs = c->num_pairs;
   e = cudaMalloc(&c->scratch_dev, 4096);
   if (e != cudaSuccess) {
     delete c;
@@ -997,6 +999,9 @@ int mst_ctx_set_tuning(mst_ctx* c, const char* key, int value) {
     c->fused_head = value != 0;
   } else if (std::strcmp(key, "chunked_block") == 0) {
     c->chunked_block = value != 0;
+  } else if (std::strcmp(key, "pairs") == 0) {  // diagnostics: run GEMMs on fewer CTA pairs
+    if (value < 1 || value > c->max_pairs) return fail(MST_ERR_CONFIG, "pairs must be 1..%d", c->max_pairs);
+    c->num_pairs = value;
   } else if (std::strcmp(key, "tma3d") == 0) {
     c3d_enabled = value != 0;
   } else {

@@ -44,14 +44,15 @@ def main():
         hdr, units = rows[0], rows[1]
         keys = ['gpu__time_duration.sum', 'sm__cycles_elapsed.avg.per_second', 'dram__bytes_read.sum', 'dram__bytes_write.sum',
                 'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed', 'lts__throughput.avg.pct_of_peak_sustained_elapsed',
-                'TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed',
+                'sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed',
+                'l1tex__m_xbar2l1tex_read_bytes.sum', 'lts__t_sector_hit_rate.pct',
                 'launch__registers_per_thread', 'smsp__warps_active.avg.pct_of_peak_sustained_active']
         for r in rows[2:]:
             full.append({'source': p.split('/')[-1], **{k: f"{r[hdr.index(k)]} {units[hdr.index(k)]}" for k in keys if k in hdr}})
     if full:
         lines += ["", "# ncu --set full captures (per launch)", ""]
         for f in full:
-            lines.append("* " + ", ".join(f"{k.split('.')[0] if not k.startswith('TPC') else 'tensor_pipe_active_pct'}: {v}" for k, v in f.items()))
+            lines.append("* " + ", ".join(f"{'tensor_pipe_active_pct' if 'pipe_tensor' in k else k.split('.')[0]}: {v}" for k, v in f.items()))
     open(out + '.md', 'w').write("\n".join(lines) + "\n")
     json.dump({"dominant_kernel": {"name": "mst_grouped_gemm_kernel", "launches_per_step": len(gem),
                                     "dram_bytes_per_launch": (g_rd + g_wr) / max(1, len(gem)),
