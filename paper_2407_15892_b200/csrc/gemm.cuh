@@ -36,8 +36,8 @@
 
 namespace mst {
 
-#ifndef MST_STAGES
-#define MST_STAGES 6
+#ifndef MST_SLOTS
+#define MST_SLOTS 12
 #endif
 #ifndef MST_EPI_BUFS
 #define MST_EPI_BUFS 2
@@ -60,11 +60,19 @@ namespace mst {
 #ifndef MST_DW_EVICT_FIRST
 #define MST_DW_EVICT_FIRST 1  // fp32 dW stores / reduce-adds stream through L2 with evict_first
 #endif
-constexpr int kStages = MST_STAGES;
-constexpr int kBK = 64;                      // K elements per stage (128 B rows)
-constexpr int kABytes = 128 * kBK * 2;       // per-CTA A tile (16 KB)
-constexpr int kBBytes = 128 * kBK * 2;       // per-CTA B tile, max (16 KB)
-constexpr int kStageBytes = kABytes + kBBytes;
+// Operand staging: 12 slots of 16 KB grouped into pipeline stages of
+// 1 + nblk slots (per launch): one A slot (128 rows x 64 K per CTA) and one
+// B slot per N block b (up to 128 columns x 64 K per CTA).  A slots of all
+// stages come first, then the B slots (stage-major).  Launches of normal tiles run 6 stages of 2 slots; launches with wide
+// tiles (two N blocks sharing the A slot, 256 x 512 per pair: 25% fewer
+// operand bytes per FLOP) run 4 stages of 3 slots.  One full and one empty
+// barrier per stage (a tcgen05.commit per extra slot measurably slows the
+// pipeline).
+constexpr int kSlots = MST_SLOTS;
+constexpr int kBK = 64;                      // K elements per K block (128 B rows)
+constexpr int kSlotBytes = 128 * kBK * 2;    // 16 KB
+constexpr int kABytes = kSlotBytes;          // per-CTA A tile
+constexpr int kMaxNBlk = 2;                  // N blocks per tile (wide tiles)
 constexpr int kNumEpiWarps = 4;
 constexpr int kThreads = 128 + 32 * kNumEpiWarps;
 constexpr int kEpiBufBytes = 4096;           // one 32-row x 128-byte TMA box
@@ -73,7 +81,7 @@ constexpr int kEpiBytes = kNumEpiWarps * kEpiBufs * kEpiBufBytes;
 constexpr int kMaxProblems = 8;
 constexpr int kMaxMaps = 24;
 constexpr int kTmemCols = 512;
-constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 512 /*barriers, tile ring*/;
+constexpr int kSmemBytes = kSlots * kSlotBytes + kEpiBytes + 1024 /*align*/ + 512 /*barriers, tile ring*/;
 
 enum EpiKind : int32_t {
   kEpiStoreBf16 = 0,  // out{g}[row, col] = bf16(acc)                     (TMA store)
@@ -103,7 +111,9 @@ struct PhaseDesc {
 struct ProblemDesc {
   int32_t num_phases;
   PhaseDesc ph[2];
-  int32_t m_tiles, n_tiles, tile_n;
+  int32_t m_tiles, n_tiles, tile_n;  // n_tiles counts logical N tiles of tile_n columns
+  int32_t nblk;        // logical N tiles per scheduled tile (1, or 2 = wide tile sharing the A slot)
+  int32_t n_wide;      // scheduled tiles along N = ceil(n_tiles / nblk)
   int32_t rows, cols;  // valid output rows / columns
   int32_t epi;
   int32_t beta;        // kEpiAccF32: 1 = reduce-add onto the existing value
@@ -129,7 +139,8 @@ struct GemmParams {
   int32_t num_problems;
   int32_t acc_stages;  // 1 or 2 TMEM accumulator buffers
   int32_t acc_stride;  // TMEM column distance between accumulator buffers
-  int32_t _pad;
+  int32_t stage_slots; // 1 + max nblk over the launch's problems
+  int32_t num_stages;  // kSlots / stage_slots
   const int32_t* sched;      // encoded tiles (problem << 24 | tile), grouped per pair
   const int32_t* sched_off;  // [num_pairs + 1]
   unsigned long long* prof;  // MST_PROFILE builds: per-role wait-cycle counters (else unused)
@@ -219,13 +230,34 @@ struct TileFeed {
 #define MST_PROF_FLUSH(base, n)
 #endif
 
-__device__ __forceinline__ void decode_tile(const GemmParams& p, int32_t code, int& prob, int& tm, int& tn) {
+// Scheduled tile -> (problem, m tile, first logical n tile, number of logical n tiles).
+__device__ __forceinline__ void decode_tile(const GemmParams& p, int32_t code, int& prob, int& tm, int& tn0,
+                                            int& nb) {
   prob = code >> 24;
   const int t = code & 0xFFFFFF;
-  const int mt = p.prob[prob].m_tiles;
-  tm = t % mt;
-  tn = t / mt;
+  const ProblemDesc& P = p.prob[prob];
+  tm = t % P.m_tiles;
+  tn0 = (t / P.m_tiles) * P.nblk;
+  nb = min(P.nblk, P.n_tiles - tn0);
 }
+
+// Position in a ring of `n` barrier-guarded entries; the phase flips on wrap.
+struct RingPos {
+  int idx;
+  uint32_t phase;
+  __device__ __forceinline__ void next(int n) {
+    if (++idx == n) {
+      idx = 0;
+      phase ^= 1;
+    }
+  }
+  // The entry j positions further on (j < n), without moving.
+  __device__ __forceinline__ RingPos at(int j, int n) const {
+    const int i = idx + j;
+    return i >= n ? RingPos{i - n, phase ^ 1u} : RingPos{i, phase};
+  }
+  __device__ __forceinline__ void advance(int j, int n) { *this = at(j, n); }
+};
 
 // ------------------------------------------------------------ epilogues
 namespace epi {
@@ -645,15 +677,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     mst_grouped_gemm_kernel(const __grid_constant__ GemmParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* smem_a = smem;
-  uint8_t* smem_b = smem + kStages * kABytes;
-  uint8_t* smem_epi = smem + kStages * kStageBytes;
+  uint8_t* smem_slots = smem;
+  uint8_t* smem_epi = smem + kSlots * kSlotBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_epi + kEpiBytes);
-  uint64_t* full = bars;                      // [kStages]   (leader's are used)
-  uint64_t* empty = bars + kStages;           // [kStages]
-  uint64_t* tfull = bars + 2 * kStages;       // [2]
-  uint64_t* tempty = bars + 2 * kStages + 2;  // [2]         (leader's are used)
-  uint64_t* tile_full = bars + 2 * kStages + 4;                // [kTileSlots]
+  uint64_t* full = bars;                      // [kSlots]   (leader's are used)
+  uint64_t* empty = bars + kSlots;            // [kSlots]
+  uint64_t* tfull = bars + 2 * kSlots;        // [2]
+  uint64_t* tempty = bars + 2 * kSlots + 2;   // [2]         (leader's are used)
+  uint64_t* tile_full = bars + 2 * kSlots + 4;                 // [kTileSlots]
   uint64_t* tile_empty = tile_full + kTileSlots;               // [kTileSlots] (leader's are used)
   int32_t* tile_codes = reinterpret_cast<int32_t*>(tile_empty + kTileSlots);  // [kTileSlots]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_codes + kTileSlots);
@@ -667,7 +698,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int i = 0; i < kMaxMaps; ++i) ptx::prefetch_tmap(&p.maps[i]);
   }
   if (warp == 1 && lane == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kSlots; ++s) {
       ptx::mbar_init(ptx::smem_u32(&full[s]), 1);
       ptx::mbar_init(ptx::smem_u32(&empty[s]), 1);
     }
@@ -693,7 +724,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 0 || (MST_SPLIT_PRODUCER && warp == 3)) {
     // ===================== TMA producer(s) =====================
     // With MST_SPLIT_PRODUCER warp 0 issues the A loads (and the expect_tx),
-    // warp 3 the B loads; both follow the same stage ring.
+    // warp 3 the B loads; both walk the same stage ring.  Everything the
+    // K-block loop needs is kept in registers: the loop sits on the critical
+    // path whenever the MMA waits for operands.
     const bool do_a = warp == 0;
     const bool do_b = !MST_SPLIT_PRODUCER || warp == 3;
     if (lane == 0) {
@@ -701,61 +734,84 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       pols[0] = ptx::policy_evict_normal();
       pols[1] = ptx::policy_evict_last();
       pols[2] = ptx::policy_evict_first();
-      int stage = 0;
-      uint32_t phase = 0;
+      const int nst = p.num_stages;
+      const uint32_t slots_u32 = ptx::smem_u32(smem_slots);
+      const uint32_t b_region = slots_u32 + nst * kSlotBytes;
+      const uint32_t b_stride = (p.stage_slots - 1) * kSlotBytes;
+      const uint32_t empty_u32 = ptx::smem_u32(empty);
+      const uint32_t full_u32 = ptx::smem_u32(full);
+      const uint32_t full_leader = ptx::mapa(full_u32, 0);
+      const bool arm = rank == 0 && do_a;
+      int sidx = 0;
+      uint32_t sphase = 0, sa = slots_u32, sb = b_region;
       MST_PROF_DECL
       for (;;) {
         const int32_t code = (rank == 0 && warp == 0) ? feed.produce(p) : feed.consume(p, 0);
         if (code < 0) break;
-        int prob, tm, tn;
-        decode_tile(p, code, prob, tm, tn);
+        int prob, tm, tn0, nb;
+        decode_tile(p, code, prob, tm, tn0, nb);
         const ProblemDesc& P = p.prob[prob];
         const int arow = tm * 256 + static_cast<int>(rank) * 128;
         for (int ph = 0; ph < P.num_phases; ++ph) {
           const PhaseDesc& d = P.ph[ph];
-          const int nh = d.umma_n >> 1;  // B columns this CTA supplies
-          const uint32_t stage_tx = 2u * (kABytes + nh * kBK * 2);
+          const int nh = d.umma_n >> 1;  // B columns this CTA supplies per N block
+          const uint32_t kblock_tx = 2u * (kABytes + nb * nh * kBK * 2);
           const CUtensorMap* ma = &p.maps[d.map_a];
           const CUtensorMap* mb = &p.maps[rank ? d.map_b1 : d.map_b0];
-          const int nb = tn * P.tile_n + (rank ? d.b_off1 : d.b_off0);
+          const int ncol0 = tn0 * P.tile_n + (rank ? d.b_off1 : d.b_off0);
+          const int ncol1 = ncol0 + P.tile_n;
           const uint64_t pa = pols[d.a_pol], pb = pols[d.b_pol];
-          for (int kb = 0; kb < d.k_blocks; ++kb) {
-            MST_PROF_WAIT(0, ptx::mbar_wait(ptx::smem_u32(&empty[stage]), phase ^ 1));
-            const uint32_t fbar_local = ptx::smem_u32(&full[stage]);
+          const int amode = !d.a_mn ? 0 : (d.a_3d ? 1 : 2);
+          const int bmode = !d.b_mn ? 0 : (d.b_3d ? 1 : 2);
+          const int kbs = d.k_blocks;
+          int k0 = d.k_start * kBK;
+          for (int kb = 0; kb < kbs; ++kb, k0 += kBK) {
+            MST_PROF_WAIT(0, ptx::mbar_wait(empty_u32 + 8 * sidx, sphase ^ 1));
+            if (arm) {
 #if MST_DIAG_NO_TMA
-            if (rank == 0 && do_a) ptx::mbar_arrive_local(fbar_local);
-            (void)stage_tx;
-            if (++stage == kStages) {
-              stage = 0;
-              phase ^= 1;
-            }
-            continue;
+              ptx::mbar_arrive_local(full_u32 + 8 * sidx);
+              (void)kblock_tx;
+#else
+              ptx::mbar_arrive_expect_tx(full_u32 + 8 * sidx, kblock_tx);
 #endif
-            if (rank == 0 && do_a) ptx::mbar_arrive_expect_tx(fbar_local, stage_tx);
-            const uint32_t fbar = ptx::mapa(fbar_local, 0);
-            const uint32_t sa = ptx::smem_u32(smem_a + stage * kABytes);
-            const uint32_t sb = ptx::smem_u32(smem_b + stage * kBBytes);
-            const int k0 = (d.k_start + kb) * kBK;
-            if (!do_a) {
-            } else if (!d.a_mn) {
-              ptx::tma_load_2d_cg2(ma, sa, fbar, k0, arow, pa);
-            } else if (d.a_3d) {
-              ptx::tma_load_3d_cg2(ma, sa, fbar, 0, k0, arow >> 6, pa);
-            } else {
-              ptx::tma_load_2d_cg2(ma, sa, fbar, arow, k0, pa);
-              ptx::tma_load_2d_cg2(ma, sa + 8192, fbar, arow + 64, k0, pa);
             }
-            if (!do_b) {
-            } else if (!d.b_mn) {
-              ptx::tma_load_2d_cg2(mb, sb, fbar, k0, nb, pb);
-            } else if (d.b_3d) {
-              ptx::tma_load_3d_cg2(mb, sb, fbar, 0, k0, nb >> 6, pb);
-            } else {
-              for (int j = 0; j < nh; j += 64) ptx::tma_load_2d_cg2(mb, sb + j * 128, fbar, nb + j, k0, pb);
+#if !MST_DIAG_NO_TMA
+            const uint32_t fbar = full_leader + 8 * sidx;
+            if (do_a) {
+              if (amode == 0) {
+                ptx::tma_load_2d_cg2(ma, sa, fbar, k0, arow, pa);
+              } else if (amode == 1) {
+                ptx::tma_load_3d_cg2(ma, sa, fbar, 0, k0, arow >> 6, pa);
+              } else {
+                ptx::tma_load_2d_cg2(ma, sa, fbar, arow, k0, pa);
+                ptx::tma_load_2d_cg2(ma, sa + 8192, fbar, arow + 64, k0, pa);
+              }
             }
-            if (++stage == kStages) {
-              stage = 0;
-              phase ^= 1;
+            if (do_b) {
+#pragma unroll
+              for (int j = 0; j < kMaxNBlk; ++j) {
+                if (j < nb) {
+                  const uint32_t sbj = sb + j * kSlotBytes;
+                  const int ncol = j ? ncol1 : ncol0;
+                  if (bmode == 0) {
+                    ptx::tma_load_2d_cg2(mb, sbj, fbar, k0, ncol, pb);
+                  } else if (bmode == 1) {
+                    ptx::tma_load_3d_cg2(mb, sbj, fbar, 0, k0, ncol >> 6, pb);
+                  } else {
+                    for (int c = 0; c < nh; c += 64) ptx::tma_load_2d_cg2(mb, sbj + c * 128, fbar, ncol + c, k0, pb);
+                  }
+                }
+              }
+            }
+#endif
+            if (++sidx == nst) {
+              sidx = 0;
+              sphase ^= 1;
+              sa = slots_u32;
+              sb = b_region;
+            } else {
+              sa += kSlotBytes;
+              sb += b_stride;
             }
           }
         }
@@ -765,60 +821,85 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA) =====================
     if (rank == 0 && lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
+      const int nst = p.num_stages;
+      const uint32_t slots_u32 = ptx::smem_u32(smem_slots);
+      const uint32_t b_region = slots_u32 + nst * kSlotBytes;
+      const uint32_t b_stride = (p.stage_slots - 1) * kSlotBytes;
+      const uint32_t empty_u32 = ptx::smem_u32(empty);
+      const uint32_t full_u32 = ptx::smem_u32(full);
+      const int acc_stages = p.acc_stages;
+      const uint32_t acc_stride = p.acc_stride;
+      int sidx = 0;
+      uint32_t sphase = 0, sa = slots_u32, sb = b_region;
+      RingPos ap{0, 0};  // TMEM accumulator ring (acc_stages entries of acc_stride columns)
       MST_PROF_DECL
       for (;;) {
         const int32_t code = feed.consume(p, 0);
         if (code < 0) break;
-        int prob, tm, tn;
-        decode_tile(p, code, prob, tm, tn);
+        int prob, tm, tn0, nb;
+        decode_tile(p, code, prob, tm, tn0, nb);
         const ProblemDesc& P = p.prob[prob];
-        MST_PROF_WAIT(1, ptx::mbar_wait(ptx::smem_u32(&tempty[acc]), acc_phase ^ 1));
+        const RingPos acc0 = ap;  // N block b accumulates in ring entry acc0 + b
+        const int acc1 = acc0.at(1 % acc_stages, acc_stages).idx;
+        for (int b = 0; b < nb; ++b) {
+          const RingPos e = ap.at(b, acc_stages);
+          MST_PROF_WAIT(1, ptx::mbar_wait(ptx::smem_u32(&tempty[e.idx]), e.phase ^ 1));
+        }
+        ap.advance(nb, acc_stages);
         ptx::tc_fence_after();
-        const uint32_t d_base = tmem_base + acc * p.acc_stride;
         for (int ph = 0; ph < P.num_phases; ++ph) {
           const PhaseDesc& d = P.ph[ph];
           const uint32_t idesc = ptx::idesc_bf16(256, d.umma_n, d.a_mn, d.b_mn);
-          const uint32_t d_tmem = d_base + d.tmem_col;
-          for (int kb = 0; kb < d.k_blocks; ++kb) {
-            MST_PROF_WAIT(0, ptx::mbar_wait(ptx::smem_u32(&full[stage]), phase));
+          // Descriptor constant parts; the start-address field (bits 0-13,
+          // address >> 4) is added per MMA.  K-major: +32 B per 16-deep step
+          // inside the swizzled row; MN-major: +2048 B (2 atoms of 8 k-rows).
+          const uint64_t a_hi = d.a_mn ? ptx::sdesc_sw128(0, 8192, 1024) : ptx::sdesc_sw128(0, 16, 1024);
+          const uint64_t b_hi = d.b_mn ? ptx::sdesc_sw128(0, 8192, 1024) : ptx::sdesc_sw128(0, 16, 1024);
+          const uint32_t a_step = d.a_mn ? (2048 >> 4) : (32 >> 4);
+          const uint32_t b_step = d.b_mn ? (2048 >> 4) : (32 >> 4);
+          const uint32_t dt0 = tmem_base + acc0.idx * acc_stride + d.tmem_col;
+          const uint32_t dt1 = tmem_base + acc1 * acc_stride + d.tmem_col;
+          uint32_t accum0 = d.acc_continue ? 1u : 0u;
+          const int kbs = d.k_blocks;
+          for (int kb = 0; kb < kbs; ++kb) {
+            MST_PROF_WAIT(0, ptx::mbar_wait(full_u32 + 8 * sidx, sphase));
             ptx::tc_fence_after();
-            const uint32_t sa = ptx::smem_u32(smem_a + stage * kABytes);
-            const uint32_t sb = ptx::smem_u32(smem_b + stage * kBBytes);
+            const uint32_t a4 = sa >> 4, b4 = sb >> 4;
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k) {
-              // K-major: advance 16 elements (32 B) inside the swizzled row.
-              // MN-major: advance 16 k-rows (2 atoms of 8 rows = 2048 B).
-              const uint64_t adesc =
-                  d.a_mn ? ptx::sdesc_sw128(sa + k * 2048, 8192, 1024) : ptx::sdesc_sw128(sa + k * 32, 16, 1024);
-              const uint64_t bdesc =
-                  d.b_mn ? ptx::sdesc_sw128(sb + k * 2048, 8192, 1024) : ptx::sdesc_sw128(sb + k * 32, 16, 1024);
-              const uint32_t accum = (kb > 0 || k > 0 || d.acc_continue) ? 1u : 0u;
-              if (!MST_DIAG_NO_MMA) ptx::umma_bf16_cg2(d_tmem, adesc, bdesc, idesc, accum);
+            for (int b = 0; b < kMaxNBlk; ++b) {
+              if (b < nb) {
+                const uint32_t dt = b ? dt1 : dt0;
+                const uint32_t bb4 = b4 + b * (kSlotBytes >> 4);
+#pragma unroll
+                for (int k = 0; k < kBK / 16; ++k) {
+                  const uint64_t adesc = a_hi | (a4 + k * a_step);
+                  const uint64_t bdesc = b_hi | (bb4 + k * b_step);
+                  if (!MST_DIAG_NO_MMA) ptx::umma_bf16_cg2(dt, adesc, bdesc, idesc, k ? 1u : accum0);
+                }
+              }
             }
-            ptx::umma_commit_cg2_mc(ptx::smem_u32(&empty[stage]), 0x3);
-            if (++stage == kStages) {
-              stage = 0;
-              phase ^= 1;
+            accum0 = 1u;
+            ptx::umma_commit_cg2_mc(empty_u32 + 8 * sidx, 0x3);
+            if (++sidx == nst) {
+              sidx = 0;
+              sphase ^= 1;
+              sa = slots_u32;
+              sb = b_region;
+            } else {
+              sa += kSlotBytes;
+              sb += b_stride;
             }
           }
         }
-        ptx::umma_commit_cg2_mc(ptx::smem_u32(&tfull[acc]), 0x3);
-        if (++acc == p.acc_stages) {
-          acc = 0;
-          acc_phase ^= 1;
-        }
+        ptx::umma_commit_cg2_mc(ptx::smem_u32(&tfull[acc0.idx]), 0x3);
+        if (nb > 1) ptx::umma_commit_cg2_mc(ptx::smem_u32(&tfull[acc1]), 0x3);
       }
       MST_PROF_FLUSH(2, 2);
     }
   } else if (warp >= 4) {
     // ===================== epilogue =====================
     const int q = warp & 3;
-    int acc = 0;
-    uint32_t acc_phase = 0;
+    RingPos ap{0, 0};
     const uint32_t tempty_leader0 = ptx::mapa(ptx::smem_u32(&tempty[0]), 0);
     const uint32_t tempty_leader1 = ptx::mapa(ptx::smem_u32(&tempty[1]), 0);
     epi::Stager st{smem_epi, lane, 0, q, false};
@@ -826,22 +907,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (;;) {
       const int32_t code = feed.consume(p, lane);
       if (code < 0) break;
-      int prob, tm, tn;
-      decode_tile(p, code, prob, tm, tn);
+      int prob, tm, tn0, nb;
+      decode_tile(p, code, prob, tm, tn0, nb);
       const ProblemDesc& P = p.prob[prob];
-      MST_PROF_WAIT(0, ptx::mbar_wait(ptx::smem_u32(&tfull[acc]), acc_phase));
-      ptx::tc_fence_after();
       const int row0 = tm * 256 + static_cast<int>(rank) * 128 + q * 32;
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * p.acc_stride;
-      MST_PROF_WAIT(1, run_epilogue(p, P, tn, row0, taddr, st));
-      // All TMEM reads of this tile are complete (tcgen05.wait::ld); release
-      // the accumulator to the MMA warp of the pair leader.
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
-      if (++acc == p.acc_stages) {
-        acc = 0;
-        acc_phase ^= 1;
+      for (int b = 0; b < nb; ++b) {
+        MST_PROF_WAIT(0, ptx::mbar_wait(ptx::smem_u32(&tfull[ap.idx]), ap.phase));
+        ptx::tc_fence_after();
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + ap.idx * p.acc_stride;
+        MST_PROF_WAIT(1, run_epilogue(p, P, tn0 + b, row0, taddr, st));
+        // All TMEM reads of this N block are complete (tcgen05.wait::ld);
+        // release the accumulator to the MMA warp of the pair leader.
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(ap.idx ? tempty_leader1 : tempty_leader0);
+        ap.next(p.acc_stages);
       }
     }
     st.drain();

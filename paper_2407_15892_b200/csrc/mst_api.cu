@@ -119,6 +119,11 @@ struct mst_ctx {
   int ksplit9 = 1;     // MLP dX GEMM (K9): 1 = two-phase accumulate, 2 = one problem per phase + combine
   int fused_head = 1;  // block_step: single-pass LM-Head forward+backward (mst_lmhead_fused)
   int chunked_block = 1;  // block_step with M_mlp == M_head: chunk-wise MLP -> head -> MLP-backward schedule
+  int wide = 1;           // allow wide tiles (two N blocks per scheduled tile) where a builder asks for them
+  // Which GEMMs of the chunk-wise block use wide tiles (bit mask, tuning key
+  // "wide_mask"): 1 K3', 2 K5 (with ksplit5), 4 K2, 8 K9, 16 K7a, 32 K1.
+  int wide_mask = 0;
+  int debug_nblk = 1;     // N blocks per tile of mst_debug_gemm
 };
 
 namespace {
@@ -267,7 +272,7 @@ int add_phase(mst_ctx* c, Launch& L, ProblemDesc& P, const PhaseSpec& s) {
 // Estimated tile cost in SM cycles (for LPT scheduling only).
 double tile_cost(const ProblemDesc& P) {
   double mma = 0;
-  for (int i = 0; i < P.num_phases; ++i) mma += double(P.ph[i].k_blocks) * P.ph[i].umma_n * 2.0;
+  for (int i = 0; i < P.num_phases; ++i) mma += double(P.ph[i].k_blocks) * P.ph[i].umma_n * 2.0 * P.nblk;
   double bytes = 0;
   switch (P.epi) {
     case mst::kEpiStoreBf16: bytes = 256.0 * P.ph[0].umma_n * 2; break;
@@ -277,7 +282,7 @@ double tile_cost(const ProblemDesc& P) {
     case mst::kEpiCeFwd: bytes = 256.0 * 16; break;
     case mst::kEpiCeBwd: bytes = 256.0 * 256 * 2; break;
   }
-  const double epi = bytes / 46.0;
+  const double epi = bytes * P.nblk / 46.0;
   return std::max(mma, epi) + 800.0;
 }
 
@@ -287,7 +292,7 @@ int get_schedule(mst_ctx* c, const GemmParams& p, const int32_t** sched, const i
   for (int i = 0; i < p.num_problems; ++i) {
     const ProblemDesc& P = p.prob[i];
     char buf[160];
-    snprintf(buf, sizeof(buf), "%d:%d:%d:%d:%d:%d:%d|", P.m_tiles, P.n_tiles, P.epi, P.beta, P.num_phases,
+    snprintf(buf, sizeof(buf), "%d:%d/%d:%d:%d:%d:%d:%d|", P.m_tiles, P.n_tiles, P.nblk, P.epi, P.beta, P.num_phases,
              P.ph[0].k_blocks * 1000 + P.ph[0].umma_n, P.num_phases > 1 ? P.ph[1].k_blocks * 1000 + P.ph[1].umma_n : 0);
     key += buf;
   }
@@ -302,7 +307,7 @@ int get_schedule(mst_ctx* c, const GemmParams& p, const int32_t** sched, const i
     for (int i = 0; i < p.num_problems; ++i) {
       const ProblemDesc& P = p.prob[i];
       const double cst = tile_cost(P);
-      const int nt = P.m_tiles * P.n_tiles;
+      const int nt = P.m_tiles * P.n_wide;
       for (int t = 0; t < nt; ++t) tiles.push_back({cst, (i << 24) | t, (int)tiles.size()});
     }
     std::stable_sort(tiles.begin(), tiles.end(), [](const T& a, const T& b) { return a.cost > b.cost; });
@@ -368,8 +373,6 @@ int launch(mst_ctx* c, cudaStream_t st, Launch& L) {
   GemmParams& p = L.p;
   if (L.acc_cols > mst::kTmemCols) return fail(MST_ERR_INTERNAL, "accumulator needs %d TMEM columns", L.acc_cols);
   int tiles = 0;
-  for (int i = 0; i < p.num_problems; ++i) tiles += p.prob[i].m_tiles * p.prob[i].n_tiles;
-  if (tiles == 0) return MST_OK;
   if (L.acc_cols <= 256) {
     p.acc_stages = 2;
     p.acc_stride = 256;
@@ -377,6 +380,18 @@ int launch(mst_ctx* c, cudaStream_t st, Launch& L) {
     p.acc_stages = 1;
     p.acc_stride = 0;
   }
+  for (int i = 0; i < p.num_problems; ++i) {
+    ProblemDesc& P = p.prob[i];
+    if (P.nblk <= 0 || c->wide == 0) P.nblk = 1;
+    if (P.nblk > mst::kMaxNBlk || P.nblk > p.acc_stages)
+      return fail(MST_ERR_INTERNAL, "problem %d: %d N blocks per tile with %d accumulator stages", i, P.nblk,
+                  p.acc_stages);
+    P.n_wide = (int)cdiv(P.n_tiles, P.nblk);
+    tiles += P.m_tiles * P.n_wide;
+    p.stage_slots = std::max(p.stage_slots, 1 + P.nblk);
+  }
+  p.num_stages = mst::kSlots / p.stage_slots;
+  if (tiles == 0) return MST_OK;
   MST_TRY(get_schedule(c, p, &p.sched, &p.sched_off, &p.order, &p.total_tiles));
   p.dynamic = c->dynamic;
   p.tile_counter = reinterpret_cast<int32_t*>(c->scratch_dev);
@@ -693,8 +708,9 @@ int build_k1(mst_ctx* c, Launch& L, const void* x, const void* wg, const void* w
 
 // Plain C[rows, cols] = A B with B split {0,128} over the pair; STORE_BF16 or ACC_F32.
 int build_plain(mst_ctx* c, Launch& L, const Operand& a, const Operand& b, void* out, int64_t ld_out, int epi,
-                int beta) {
+                int beta, int nblk = 1) {
   ProblemDesc& P = L.p.prob[L.p.num_problems++];
+  P.nblk = nblk;
   PhaseSpec s{};
   s.a = a;
   s.b0 = b;
@@ -728,13 +744,14 @@ int build_plain(mst_ctx* c, Launch& L, const Operand& a, const Operand& b, void*
 // few-tile dX GEMMs (K5: K = V, K9: K = 2I) so they interleave with the
 // short-K dW tiles of the same launch instead of dominating its tail.
 int build_plain_splitk(mst_ctx* c, Launch& L, const Operand& a, const Operand& b, float* part, int64_t ldp,
-                       int splits) {
+                       int splits, int nblk = 1) {
   const int kb = (int)cdiv(a.k, mst::kBK);
   const int kps = (int)cdiv(kb, splits);
   for (int s = 0; s < splits; ++s) {
     const int k0 = s * kps;
     if (k0 >= kb) break;
     ProblemDesc& P = L.p.prob[L.p.num_problems++];
+    P.nblk = nblk;
     PhaseSpec ps{};
     ps.a = a;
     ps.b0 = b;
@@ -802,6 +819,7 @@ int add_mlp_grads(mst_ctx* c, Launch& L, const void* dg, const void* du, const v
                                h, 1));
   } else {  // K9: one accumulator over both phases (B K-major)
     ProblemDesc& P = L.p.prob[L.p.num_problems++];
+    P.nblk = (c->wide_mask & 8) ? 2 : 1;
     PhaseSpec q0{};
     q0.a = {dg, rows, i, i, false};
     q0.b0 = {wg, h, i, i, false};
@@ -999,6 +1017,13 @@ int mst_ctx_set_tuning(mst_ctx* c, const char* key, int value) {
     c->fused_head = value != 0;
   } else if (std::strcmp(key, "chunked_block") == 0) {
     c->chunked_block = value != 0;
+  } else if (std::strcmp(key, "wide") == 0) {
+    c->wide = value != 0;
+  } else if (std::strcmp(key, "wide_mask") == 0) {
+    c->wide_mask = value;
+  } else if (std::strcmp(key, "debug_nblk") == 0) {
+    if (value < 1 || value > mst::kMaxNBlk) return fail(MST_ERR_CONFIG, "debug_nblk must be 1..%d", mst::kMaxNBlk);
+    c->debug_nblk = value;
   } else if (std::strcmp(key, "pairs") == 0) {  // diagnostics: run GEMMs on fewer CTA pairs
     if (value < 1 || value > c->max_pairs) return fail(MST_ERR_CONFIG, "pairs must be 1..%d", c->max_pairs);
     c->num_pairs = value;
@@ -1473,6 +1498,7 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
   auto add_k1s = [&](Launch& L, int j) -> int {  // K1 saving G, U (fp32) and h (bf16)
     const int64_t rows = rows_of(j);
     ProblemDesc& P = L.p.prob[L.p.num_problems++];
+    P.nblk = (c->wide_mask & 32) ? 2 : 1;
     PhaseSpec s{};
     s.a = {bptr(x, b[j] * h), rows, h, h, false};
     s.b0 = {wg, i, h, i, true};
@@ -1510,7 +1536,7 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
     {  // K2(j) + the weight/input gradients of chunk j-1
       Launch L;
       MST_TRY(build_plain(c, L, Operand{hb, rows, i, i, false}, Operand{wd, h, i, h, true}, oj, h, mst::kEpiStoreBf16,
-                          0));
+                          0, (c->wide_mask & 4) ? 2 : 1));
       if (j > 0) MST_TRY(add_grads(L, j - 1));
       MST_TRY(launch(c, st, L));
       if (j > 0 && c->ksplit9 > 1)
@@ -1520,7 +1546,7 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
     {  // K3': logits GEMM, partials + softmax numerators
       Launch L;
       MST_TRY(build_plain(c, L, Operand{oj, rows, h, h, false}, Operand{wout, v, h, v, true}, dl, v,
-                          mst::kEpiCeFwdNum, 0));
+                          mst::kEpiCeFwdNum, 0, (c->wide_mask & 1) ? 2 : 1));
       ProblemDesc& P = L.p.prob[0];
       P.labels = labels + r0;
       P.part = part;
@@ -1536,16 +1562,21 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
     c->launches += 3;
     {  // K5 + K6
       Launch L;
-      MST_TRY(build_plain(c, L, Operand{dl, rows, v, v, false}, Operand{wout, h, v, v, false}, doj, h,
-                          mst::kEpiStoreBf16, 0));
+      const Operand a5{dl, rows, v, v, false}, b5{wout, h, v, v, false};
+      const int nb5 = (c->wide_mask & 2) ? 2 : 1;
+      if (c->ksplit5 > 1)
+        MST_TRY(build_plain_splitk(c, L, a5, b5, part5, h, c->ksplit5, nb5));
+      else
+        MST_TRY(build_plain(c, L, a5, b5, doj, h, mst::kEpiStoreBf16, 0, nb5));
       MST_TRY(build_plain(c, L, Operand{ot, h, rows, ldt, false}, Operand{dl, v, rows, v, true}, dwout, v,
                           mst::kEpiAccF32, beta));
       MST_TRY(launch(c, st, L));
+      if (c->ksplit5 > 1) MST_TRY(splitk_combine(c, st, part5, c->ksplit5, rows, h, doj, h));
     }
     {  // K7a: dh = dO_j W_d^T (fp32)
       Launch L;
       MST_TRY(build_plain(c, L, Operand{doj, rows, h, h, false}, Operand{wd, i, h, h, false}, dhb, i,
-                          mst::kEpiAccF32, 0));
+                          mst::kEpiAccF32, 0, (c->wide_mask & 16) ? 2 : 1));
       MST_TRY(launch(c, st, L));
     }
     {  // SwiGLU backward from the saved accumulators
@@ -1622,6 +1653,7 @@ int mst_debug_gemm(mst_ctx* c, void* stream, const void* a, const void* b, void*
   Operand oa = a_mn ? Operand{a, m, k, m, true} : Operand{a, m, k, k, false};
   Operand ob = b_mn ? Operand{b, n, k, n, true} : Operand{b, n, k, k, false};
   MST_TRY(build_plain(c, L, oa, ob, out, n, out_f32 ? mst::kEpiAccF32 : mst::kEpiStoreBf16, beta));
+  L.p.prob[0].nblk = c->debug_nblk;
   MST_TRY(launch(c, static_cast<cudaStream_t>(stream), L));
   MST_CUDA(cudaGetLastError());
   return MST_OK;

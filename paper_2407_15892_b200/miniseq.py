@@ -182,6 +182,10 @@ class Context:
             self._ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=f"cuda:{self.device}")
         return self._ws
 
+    def set_tuning(self, key: str, value: int) -> None:
+        """Engine tuning / diagnostic knobs (mst_ctx_set_tuning in mst.h)."""
+        _check(self.lib.mst_ctx_set_tuning(self.handle, key.encode(), int(value)))
+
     @property
     def num_pairs(self) -> int:
         return self.lib.mst_ctx_num_pairs(self.handle)

@@ -190,17 +190,27 @@ def test_error_behaviour():
         ms.check_lmhead_stats(hs)
 
 
+@pytest.mark.parametrize("nblk", [1, 2])
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
-def test_engine_gemm_all_operand_majorness(a_mn, b_mn):
+def test_engine_gemm_all_operand_majorness(a_mn, b_mn, nblk):
+    """Every operand orientation, ragged extents, normal (256x256 per CTA
+    pair) and wide (256x512: two N blocks sharing the A slot) tiles; N=768
+    makes the last wide tile a single N block."""
     torch.manual_seed(0)
-    for (M, N, K) in [(256, 256, 64), (296, 200, 136), (512, 768, 4096)]:
-        A = torch.randn(M, K, device="cuda").bfloat16()
-        B = torch.randn(K, N, device="cuda").bfloat16()
-        ref = A.double() @ B.double()
-        out = torch.zeros(M, N, device="cuda", dtype=torch.float32)
-        ms.debug_gemm(A.t().contiguous() if a_mn else A, B if b_mn else B.t().contiguous(), M, N, K, a_mn, b_mn,
-                      out)
-        assert rel(out, ref.cpu().numpy()) <= 1e-5
+    ctx = ms.Context.get(0)
+    ctx.set_tuning("debug_nblk", nblk)
+    try:
+        for (M, N, K) in [(256, 256, 64), (296, 200, 136), (512, 768, 4096), (256, 1024, 192)]:
+            A = torch.randn(M, K, device="cuda").bfloat16()
+            B = torch.randn(K, N, device="cuda").bfloat16()
+            ref = A.double() @ B.double()
+            for f32 in (True, False):
+                out = torch.zeros(M, N, device="cuda", dtype=torch.float32 if f32 else torch.bfloat16)
+                ms.debug_gemm(A.t().contiguous() if a_mn else A, B if b_mn else B.t().contiguous(), M, N, K, a_mn,
+                              b_mn, out)
+                assert rel(out.float(), ref.cpu().numpy()) <= (1e-5 if f32 else 4e-3), (M, N, K, f32)
+    finally:
+        ctx.set_tuning("debug_nblk", 1)
 
 
 def test_llama3_8b_shapes_against_torch_fp32():

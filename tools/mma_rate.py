@@ -11,6 +11,7 @@ from bench import ClockSampler
 dev = 'cuda'
 import os
 PAIRS = [int(x) for x in os.environ.get('PAIRS', '0').split(',')]
+NBLK = [int(x) for x in os.environ.get('NBLK', '1').split(',')]
 SHAPES = os.environ.get('SHAPES', 'square 8192,K3-like,K6T-like').split(',')
 libs = {}
 for p in sys.argv[1].split(','):
@@ -31,11 +32,12 @@ for name, M, N, K, amn, bmn in [("square 8192", 8192, 8192, 8192, 0, 1), ("K3-li
     C = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
     fl = 2 * M * N * K
     tiles = (M // 256) * ((N + 255) // 256)
-    for (tag, (lib, h)), pairs in [(kv, pr) for kv in libs.items() for pr in PAIRS]:
+    for (tag, (lib, h)), pairs, nbk in [(kv, pr, nb) for kv in libs.items() for pr in PAIRS for nb in NBLK]:
         if pairs:
             assert lib.mst_ctx_set_tuning(h, b"pairs", pairs) == 0
+        assert lib.mst_ctx_set_tuning(h, b"debug_nblk", nbk) == 0
         npairs = lib.mst_ctx_num_pairs(h)
-        tag = f"{tag} pairs={npairs}"
+        tag = f"{tag} pairs={npairs} nblk={nbk}"
         f = lambda: lib.mst_debug_gemm(h, st, A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K, amn, bmn, 0, 0)
         t0 = time.time()
         while time.time() - t0 < 1.0:
@@ -50,7 +52,7 @@ for name, M, N, K, amn, bmn in [("square 8192", 8192, 8192, 8192, 0, 1), ("K3-li
         t = e0.elapsed_time(e1)
         c = buf.view(64, 8)[0].tolist()
         mma_tot = c[4] / npairs
-        kb_per_pair = tiles * (K // 64) / npairs
+        kb_per_pair = tiles * (K // 64) / npairs  # in 256-column K blocks (a wide K block counts twice)
         print(f"{name:11s} {tag:32s} {t:.3f} ms {fl/t/1e9:6.0f} TF/s | MMA cycles/pair {mma_tot:9.0f} "
               f"-> {mma_tot/kb_per_pair:6.1f} cyc/kblock (floor 512), wait-full {100*c[2]/max(c[4],1):4.1f}% "
               f"| clock {mma_tot/(t*1e3):6.0f} MHz (nvml {clk.summary()['sm_mhz']})", flush=True)

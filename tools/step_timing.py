@@ -23,6 +23,10 @@ Wo = (0.02 * torch.randn(H, V, device=dev)).bfloat16()
 L = torch.randint(0, V, (S,), device=dev, dtype=torch.int32)
 mlp, head = ms.MlpWeights(Wg, Wu, Wd), ms.LmHeadWeights(Wo)
 ctx = ms.Context.get(0)
+import os
+for kv in filter(None, os.environ.get('MST_TUNE', '').split(',')):
+    k, v = kv.split('=')
+    ctx.set_tuning(k, int(v))
 st, gr = ms.block_step(X, L, mlp, head, M, M)
 t0 = time.time()
 while time.time() - t0 < 2.0:
