@@ -19,6 +19,10 @@
 #include "mst/mst.h"
 
 #if defined(__has_include)
+#if __has_include("minitrain/memtrack.hpp") && !defined(MST_STANDALONE_ERRORS)
+#include "minitrain/memtrack.hpp"
+#define MST_HAVE_MINITRAIN_MEMTRACK 1
+#endif
 #if __has_include("minitrain/error.hpp") && !defined(MST_STANDALONE_ERRORS)
 #include "minitrain/error.hpp"
 #define MST_HAVE_MINITRAIN_ERRORS 1
@@ -177,6 +181,44 @@ inline void miniseq_lmhead_backward(Context& ctx, void* stream, const mst_lmhead
   throw_on(mst_lmhead_backward(ctx.get(), stream, &saved, w.W_out, global_stats, grad_loss, dX, dW_out,
                                accumulate ? 1 : 0, ws.data, ws.bytes));
 }
+
+// Op counters of the context (memtrack.hpp:19-35 conventions; mst.h "memtrack").
+inline mst_counters counters(const Context& ctx) {
+  mst_counters c{};
+  throw_on(mst_ctx_get_counters(ctx.get(), &c));
+  return c;
+}
+
+#ifdef MST_HAVE_MINITRAIN_MEMTRACK
+namespace detail {
+inline void mem_to_minitrain(void*, int kind, uint64_t bytes, const char* label) {
+  minitrain::MemTracker& t = minitrain::MemTracker::current();
+  if (kind == 0)
+    t.on_alloc(bytes, label);
+  else
+    t.on_free(bytes, label);
+}
+inline void count_to_minitrain(void*, int kind, int64_t a, int64_t b, int64_t c, uint64_t w) {
+  minitrain::MemTracker& t = minitrain::MemTracker::current();
+  if (kind == 0)
+    t.count_matmul(a, b, c, w);
+  else
+    t.count_op(static_cast<uint64_t>(a), static_cast<uint64_t>(b));
+}
+}  // namespace detail
+
+// Route the library's chunk-buffer events and op counts into the calling
+// thread's current minitrain::MemTracker (memtrack.hpp:143-151), so
+// TrackedRegion / export_timeline work unchanged on the GPU path.
+inline void attach_current_tracker(Context& ctx) {
+  throw_on(mst_ctx_set_mem_hook(ctx.get(), &detail::mem_to_minitrain, nullptr));
+  throw_on(mst_ctx_set_count_hook(ctx.get(), &detail::count_to_minitrain, nullptr));
+}
+inline void detach_tracker(Context& ctx) {
+  throw_on(mst_ctx_set_mem_hook(ctx.get(), nullptr, nullptr));
+  throw_on(mst_ctx_set_count_hook(ctx.get(), nullptr, nullptr));
+}
+#endif
 
 // mask_labels_for_chunk(L, range) — SPEC.md:331-339: a pointer offset.
 inline const int32_t* mask_labels_for_chunk(const int32_t* L, int64_t N, std::pair<int64_t, int64_t> r) {

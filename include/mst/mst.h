@@ -137,6 +137,37 @@ MST_API int mst_ctx_set_profile_buffer(mst_ctx* ctx, void* dev_counters);
  * Unknown keys are MST_ERR_CONFIG.  Changing a knob clears the schedule cache. */
 MST_API int mst_ctx_set_tuning(mst_ctx* ctx, const char* key, int value);
 
+/* ---------------------------------------------------------------- memtrack
+ * The library's side of the reference's MemTracker (memtrack.hpp:138-228):
+ *
+ *  * Counters follow the fixed counting conventions of memtrack.hpp:19-35
+ *    for the logical operations a call executes (every GEMM as
+ *    count_matmul(N, K, P) with operands that are weight tensors added to
+ *    weight_read_elements; SiLU / Hadamard / cross-entropy as count_op).
+ *    Fused epilogues are counted as the ops they implement; zero-copy chunk
+ *    slices count nothing (the reference's slice_rows copies 2*n*H).
+ *    Accumulated per context at enqueue time, read with
+ *    mst_ctx_get_counters, zeroed with mst_ctx_reset_counters.
+ *  * Memory events: the chunk buffers a call carves from its workspace are
+ *    reported with their logical lifetime (alloc when a chunk's buffer comes
+ *    into use, free when it is dead) and the reference's label classes:
+ *    "inter.mlp.*", "inter.head.*" (the [S/M, I] / [S/M, V] intermediates),
+ *    "act.*" (activations the block step keeps: O, dO, lse, operand
+ *    transposes).  Install a hook with mst_ctx_set_mem_hook; kind 0 = alloc
+ *    (MemTracker::on_alloc), 1 = free (on_free).  The count hook, when set,
+ *    receives every counted op as it is counted (kind 0: count_matmul(a, b,
+ *    c, w); kind 1: count_op(flops = a, hbm = b)), so a C++ caller can
+ *    forward both into minitrain::MemTracker::current(). */
+typedef struct mst_counters {
+  uint64_t flops, matmul_flops, hbm_elements, weight_read_elements;
+} mst_counters;
+typedef void (*mst_mem_hook)(void* user, int kind, uint64_t bytes, const char* label);
+typedef void (*mst_count_hook)(void* user, int kind, int64_t a, int64_t b, int64_t c, uint64_t w);
+MST_API int mst_ctx_get_counters(const mst_ctx* ctx, mst_counters* out);
+MST_API int mst_ctx_reset_counters(mst_ctx* ctx);
+MST_API int mst_ctx_set_mem_hook(mst_ctx* ctx, mst_mem_hook fn, void* user);
+MST_API int mst_ctx_set_count_hook(mst_ctx* ctx, mst_count_hook fn, void* user);
+
 /* make_chunk_plan(N, M) — SPEC.md:286-294.  Writes min(M,N)+1 row bounds
  * into `bounds` (capacity >= min(M,N)+1): chunk c is [bounds[c], bounds[c+1]).
  * Balanced rule: the first N mod M chunks hold ceil(N/M) rows. */

@@ -124,12 +124,60 @@ struct mst_ctx {
   // "wide_mask"): 1 K3', 2 K5 (with ksplit5), 4 K2, 8 K9, 16 K7a, 32 K1.
   int wide_mask = 0;
   int debug_nblk = 1;     // N blocks per tile of mst_debug_gemm
+  // memtrack side (mst.h): counters per memtrack.hpp:19-35, event hooks
+  mst_counters ctr{};
+  mst_mem_hook mem_fn = nullptr;
+  void* mem_user = nullptr;
+  mst_count_hook cnt_fn = nullptr;
+  void* cnt_user = nullptr;
+  const void* weights[4] = {nullptr, nullptr, nullptr, nullptr};  // weight tensors of the current call
 };
 
 namespace {
 
 // MN-major operands as 3-D tensor maps (one TMA per slab); tuning knob "tma3d".
 bool c3d_enabled = true;
+
+// ------------------------------------------------------------ memtrack side
+// count_matmul / count_op of memtrack.hpp:163-175 (conventions at :19-35).
+void cnt_mm(mst_ctx* c, int64_t n, int64_t k, int64_t p, uint64_t weight_elems) {
+  const uint64_t f = 2ull * (uint64_t)n * (uint64_t)k * (uint64_t)p;
+  c->ctr.flops += f;
+  c->ctr.matmul_flops += f;
+  c->ctr.hbm_elements += (uint64_t)n * k + (uint64_t)k * p + (uint64_t)n * p;
+  c->ctr.weight_read_elements += weight_elems;
+  if (c->cnt_fn) c->cnt_fn(c->cnt_user, 0, n, k, p, weight_elems);
+}
+void cnt_op(mst_ctx* c, uint64_t flops, uint64_t hbm) {
+  c->ctr.flops += flops;
+  c->ctr.hbm_elements += hbm;
+  if (c->cnt_fn) c->cnt_fn(c->cnt_user, 1, (int64_t)flops, (int64_t)hbm, 0, 0);
+}
+bool is_weight(const mst_ctx* c, const void* p) {
+  for (const void* w : c->weights)
+    if (w && w == p) return true;
+  return false;
+}
+// MemTracker::on_alloc / on_free (memtrack.hpp:153-167) for a chunk buffer.
+void mem_alloc(mst_ctx* c, uint64_t bytes, const char* label) {
+  if (c->mem_fn) c->mem_fn(c->mem_user, 0, bytes, label);
+}
+void mem_free(mst_ctx* c, uint64_t bytes, const char* label) {
+  if (c->mem_fn) c->mem_fn(c->mem_user, 1, bytes, label);
+}
+// Weight tensors of the current call (operands equal to one of them count
+// as weight reads, memtrack.hpp:25-26).
+struct WeightScope {
+  mst_ctx* c;
+  WeightScope(mst_ctx* ctx, const void* a, const void* b = nullptr, const void* d = nullptr, const void* e = nullptr)
+      : c(ctx) {
+    c->weights[0] = a;
+    c->weights[1] = b;
+    c->weights[2] = d;
+    c->weights[3] = e;
+  }
+  ~WeightScope() { c->weights[0] = c->weights[1] = c->weights[2] = c->weights[3] = nullptr; }
+};
 
 // ------------------------------------------------------------ tensor maps
 int tmap_2d(mst_ctx* c, CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t ld_elems,
@@ -703,6 +751,8 @@ int build_k1(mst_ctx* c, Launch& L, const void* x, const void* wg, const void* w
   P.epi = mst::kEpiSwiglu;
   MST_TRY(add_out_map(c, L, h, I, rows, I, false, &P.map_out0));
   L.flops += 2.0 * rows * (2.0 * I) * H;
+  cnt_mm(c, rows, H, I, (uint64_t)(H * I));  // G = X W_g
+  cnt_mm(c, rows, H, I, (uint64_t)(H * I));  // U = X W_u
   return MST_OK;
 }
 
@@ -735,6 +785,8 @@ int build_plain(mst_ctx* c, Launch& L, const Operand& a, const Operand& b, void*
   P.col_off0 = 0;
   P.col_off1 = 128;
   L.flops += 2.0 * a.mn * b.mn * a.k;
+  cnt_mm(c, a.mn, a.k, b.mn,
+         (is_weight(c, a.base) ? (uint64_t)(a.mn * a.k) : 0) + (is_weight(c, b.base) ? (uint64_t)(b.mn * b.k) : 0));
   return MST_OK;
 }
 
@@ -747,6 +799,8 @@ int build_plain_splitk(mst_ctx* c, Launch& L, const Operand& a, const Operand& b
                        int splits, int nblk = 1) {
   const int kb = (int)cdiv(a.k, mst::kBK);
   const int kps = (int)cdiv(kb, splits);
+  cnt_mm(c, a.mn, a.k, b.mn,
+         (is_weight(c, a.base) ? (uint64_t)(a.mn * a.k) : 0) + (is_weight(c, b.base) ? (uint64_t)(b.mn * b.k) : 0));
   for (int s = 0; s < splits; ++s) {
     const int k0 = s * kps;
     if (k0 >= kb) break;
@@ -844,7 +898,10 @@ int add_mlp_grads(mst_ctx* c, Launch& L, const void* dg, const void* du, const v
     P.col_off0 = 0;
     P.col_off1 = 128;
     L.flops += 2.0 * 2.0 * rows * h * i;
+    cnt_mm(c, rows, i, h, (uint64_t)(h * i));  // dG W_g^T
+    cnt_mm(c, rows, i, h, (uint64_t)(h * i));  // dU W_u^T
   }
+  cnt_op(c, (uint64_t)(rows * h), 3ull * rows * h);  // dX' + dX'' (fused: one K = 2I accumulation)
   // K8: dW_d[I,H] += h^T dO_j (A = h^T, K-major)
   MST_TRY(build_plain(c, L, Operand{ht, i, rows, ldt, false}, Operand{doj, h, rows, h, true}, dwd, h, mst::kEpiAccF32,
                       beta));
@@ -870,6 +927,8 @@ int add_mlp_grads(mst_ctx* c, Launch& L, const void* dg, const void* du, const v
     P.ld0 = P.ld1 = i;
     P.col_off0 = P.col_off1 = 0;
     L.flops += 2.0 * h * (2.0 * i) * rows;
+    cnt_mm(c, h, rows, i, 0);  // dW_g += X^T dG
+    cnt_mm(c, h, rows, i, 0);  // dW_u += X^T dU
   }
   return MST_OK;
 }
@@ -1038,6 +1097,29 @@ int mst_ctx_set_tuning(mst_ctx* c, const char* key, int value) {
 }
 
 int mst_ctx_num_pairs(const mst_ctx* c) { return c ? c->num_pairs : 0; }
+
+int mst_ctx_get_counters(const mst_ctx* c, mst_counters* out) {
+  if (!c || !out) return fail(MST_ERR_STATE, "NULL context or output");
+  *out = c->ctr;
+  return MST_OK;
+}
+int mst_ctx_reset_counters(mst_ctx* c) {
+  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  c->ctr = mst_counters{};
+  return MST_OK;
+}
+int mst_ctx_set_mem_hook(mst_ctx* c, mst_mem_hook fn, void* user) {
+  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  c->mem_fn = fn;
+  c->mem_user = user;
+  return MST_OK;
+}
+int mst_ctx_set_count_hook(mst_ctx* c, mst_count_hook fn, void* user) {
+  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  c->cnt_fn = fn;
+  c->cnt_user = user;
+  return MST_OK;
+}
 int64_t mst_ctx_launch_count(const mst_ctx* c) { return c ? c->launches : 0; }
 
 int mst_make_chunk_plan(int64_t n, int64_t m, int64_t* bounds, int64_t* num_chunks) {
@@ -1147,9 +1229,11 @@ int mst_mlp_forward(mst_ctx* c, void* stream, const void* x, const void* wg, con
   carve_mlp(cv, n, h, i, m, &hb[0], &hb[1], &unused);
   const std::vector<int64_t> b = plan_bounds(n, m);
   const int nch = (int)b.size() - 1;
+  WeightScope ws_(c, wg, wu, wd);
   // Software pipeline over chunks: launch j runs K2(j-1) and K1(j) together
   // (independent: different h buffers), so the long-K down GEMM of one chunk
   // fills the tail of the next chunk's gate/up GEMM (Alg. 1 loop).
+  // Two h chunk buffers are live across that launch.
   for (int j = 0; j <= nch; ++j) {
     Launch L;
     if (j >= 1) {
@@ -1160,9 +1244,13 @@ int mst_mlp_forward(mst_ctx* c, void* stream, const void* x, const void* wg, con
     }
     if (j < nch) {
       const int64_t r0 = b[j], rows = b[j + 1] - b[j];
+      mem_alloc(c, (uint64_t)rows * i * 2, "inter.mlp.h");
       MST_TRY(build_k1(c, L, bptr(x, r0 * h), wg, wu, hb[j & 1], rows, h, i));
+      cnt_op(c, 4ull * rows * i, 2ull * rows * i);  // silu (fused into the K1 epilogue)
+      cnt_op(c, 1ull * rows * i, 3ull * rows * i);  // hadamard
     }
     MST_TRY(launch(c, st, L));
+    if (j >= 1) mem_free(c, (uint64_t)(b[j] - b[j - 1]) * i * 2, "inter.mlp.h");
   }
   MST_CUDA(cudaGetLastError());
   if (saved) {
@@ -1200,9 +1288,11 @@ int mst_mlp_backward(mst_ctx* c, void* stream, const void* dout, const mst_mlp_s
   const int64_t ldt = ld_t(n, m);
   const std::vector<int64_t> b = plan_bounds(n, m);
   const int nch = (int)b.size() - 1;
+  WeightScope ws_(c, wg, wu, wd);
   // K7a(j): dh = dO_j W_d^T, fp32 (B[k=h, n=i] = W_d[i, h]: K-major).
   auto add_k7a = [&](Launch& L, int j) -> int {
     const int64_t r0 = b[j], rows = b[j + 1] - b[j];
+    mem_alloc(c, (uint64_t)rows * i * 4, "inter.mlp.dh");
     return build_plain(c, L, Operand{bptr(dout, r0 * h), rows, h, h, false}, Operand{wd, i, h, h, false}, dhb, i,
                        mst::kEpiAccF32, 0);
   };
@@ -1237,9 +1327,19 @@ int mst_mlp_backward(mst_ctx* c, void* stream, const void* dout, const mst_mlp_s
       MST_TRY(add_out_map(c, L, dg, i, rows, i, false, &P.map_out1));
       MST_TRY(add_out_map(c, L, du, i, rows, i, false, &P.map_out2));
       L.flops += 2.0 * rows * (2.0 * i) * h;
+      mem_alloc(c, (uint64_t)rows * i * 2, "inter.mlp.h");
+      mem_alloc(c, (uint64_t)rows * i * 2, "inter.mlp.dG");
+      mem_alloc(c, (uint64_t)rows * i * 2, "inter.mlp.dU");
+      cnt_mm(c, rows, h, i, (uint64_t)(h * i));      // G recompute
+      cnt_mm(c, rows, h, i, (uint64_t)(h * i));      // U recompute
+      cnt_op(c, 4ull * rows * i, 3ull * rows * i);   // silu + silu_backward (fused epilogue)
+      cnt_op(c, 2ull * rows * i, 6ull * rows * i);   // dG, dU products
       MST_TRY(launch(c, st, L));
+      mem_free(c, (uint64_t)rows * i * 4, "inter.mlp.dh");
     }
     // K-major A operands for the dW GEMMs: h^T (K8) and X_j^T (K10).
+    mem_alloc(c, (uint64_t)rows * i * 2, "inter.mlp.hT");
+    mem_alloc(c, (uint64_t)rows * h * 2, "act.xT");
     MST_TRY(transpose_bf16(c, st, hb, i, ht, ldt, rows, i));
     MST_TRY(transpose_bf16(c, st, xj, h, xt, ldt, rows, h));
     {  // K9 + K8 + K10 (mutually independent) + K7a of the next chunk, one launch.
@@ -1250,6 +1350,11 @@ int mst_mlp_backward(mst_ctx* c, void* stream, const void* dout, const mst_mlp_s
       MST_TRY(launch(c, st, L));
       if (c->ksplit9 > 1) MST_TRY(splitk_combine(c, st, part9, 2, rows, h, const_cast<char*>(bptr(dx, r0 * h)), h));
     }
+    mem_free(c, (uint64_t)rows * h * 2, "act.xT");
+    mem_free(c, (uint64_t)rows * i * 2, "inter.mlp.hT");
+    mem_free(c, (uint64_t)rows * i * 2, "inter.mlp.dU");
+    mem_free(c, (uint64_t)rows * i * 2, "inter.mlp.dG");
+    mem_free(c, (uint64_t)rows * i * 2, "inter.mlp.h");
   }
   MST_CUDA(cudaGetLastError());
   return MST_OK;
@@ -1276,8 +1381,12 @@ int mst_lmhead_forward(mst_ctx* c, void* stream, const void* x, const int32_t* l
   const int nch = (int)b.size() - 1;
   const int nparts = (int)cdiv(v, 256);
   MST_CUDA(cudaMemsetAsync(stats, 0, sizeof(float) * MST_STATS_LEN(nch), st));
+  WeightScope ws_(c, wout);
   for (int j = 0; j < nch; ++j) {
     const int64_t r0 = b[j], rows = b[j + 1] - b[j];
+    const uint64_t part_bytes = (uint64_t)rows * nparts * 8 + (uint64_t)rows * 8;  // partials + z_target + row loss
+    mem_alloc(c, part_bytes, "inter.head.partials");
+    cnt_op(c, 5ull * rows * v, (uint64_t)(rows * v + 2 * rows));  // cross-entropy forward (fused epilogue)
     Launch L;  // K3: logits GEMM + online-softmax partials
     MST_TRY(build_plain(c, L, Operand{bptr(x, r0 * h), rows, h, h, false}, Operand{wout, v, h, v, true}, nullptr, 0,
                         mst::kEpiCeFwd, 0));
@@ -1293,6 +1402,7 @@ int mst_lmhead_forward(mst_ctx* c, void* stream, const void* x, const int32_t* l
                                                    stats + 3);
     chunk_reduce_kernel<<<1, 1024, 0, st>>>(lrow, labels + r0, (int)rows, (int)v, stats + 4 + j, stats + 4 + nch + j);
     c->launches += 2;
+    mem_free(c, part_bytes, "inter.head.partials");
   }
   finalize_loss_kernel<<<1, 32, 0, st>>>(stats, nch, loss_mode);
   c->launches += 1;
@@ -1338,10 +1448,14 @@ int mst_lmhead_backward(mst_ctx* c, void* stream, const mst_lmhead_saved* s, con
   grad_scale_kernel<<<(nch + 255) / 256, 256, 0, st>>>(global_stats ? global_stats : s->stats, s->stats, nch,
                                                            s->loss_mode, grad_loss, scales);
   c->launches += 1;
+  WeightScope ws_(c, wout);
   for (int j = 0; j < nch; ++j) {
     const int64_t r0 = b[j], rows = b[j + 1] - b[j];
     const int beta = (j > 0 || accumulate) ? 1 : 0;
     const void* xj = bptr(s->x, r0 * h);
+    mem_alloc(c, (uint64_t)rows * h * 2, "act.xT");
+    mem_alloc(c, (uint64_t)rows * v * 2, "inter.head.dlogits");
+    cnt_op(c, 5ull * rows * v, (uint64_t)(2 * rows * v + 2 * rows));  // cross-entropy backward (fused epilogue)
     MST_TRY(transpose_bf16(c, st, xj, h, ot, ldt, rows, h));  // (head input)_j^T: K-major A of K6
     {  // K4: recompute logits, dlogits = (softmax - onehot) * scale -> bf16
       Launch L;
@@ -1366,6 +1480,8 @@ int mst_lmhead_backward(mst_ctx* c, void* stream, const mst_lmhead_saved* s, con
       if (c->ksplit5 > 1)
         MST_TRY(splitk_combine(c, st, part5, c->ksplit5, rows, h, const_cast<char*>(bptr(dx, r0 * h)), h));
     }
+    mem_free(c, (uint64_t)rows * v * 2, "inter.head.dlogits");
+    mem_free(c, (uint64_t)rows * h * 2, "act.xT");
   }
   MST_CUDA(cudaGetLastError());
   return MST_OK;
@@ -1406,10 +1522,17 @@ int mst_lmhead_fused(mst_ctx* c, void* stream, const void* x, const int32_t* lab
   }
   grad_scale_kernel<<<(nch + 255) / 256, 256, 0, st>>>(gstats, stats, nch, loss_mode, grad_loss, scales);
   c->launches += 3;
+  WeightScope ws_(c, wout);
   for (int j = 0; j < nch; ++j) {
     const int64_t r0 = b[j], rows = b[j + 1] - b[j];
     const int beta = (j > 0 || accumulate) ? 1 : 0;
     const void* xj = bptr(x, r0 * h);
+    const uint64_t part_bytes = (uint64_t)rows * nparts * 8 + (uint64_t)rows * 8;
+    mem_alloc(c, (uint64_t)rows * h * 2, "act.xT");
+    mem_alloc(c, part_bytes, "inter.head.partials");
+    mem_alloc(c, (uint64_t)rows * v * 2, "inter.head.dlogits");
+    cnt_op(c, 5ull * rows * v, (uint64_t)(rows * v + 2 * rows));      // cross-entropy forward
+    cnt_op(c, 5ull * rows * v, (uint64_t)(2 * rows * v + 2 * rows));  // cross-entropy backward
     MST_TRY(transpose_bf16(c, st, xj, h, ot, ldt, rows, h));  // (head input)_j^T: K-major A of K6
     {  // K3': logits GEMM; epilogue = online-softmax partials + softmax numerators (bf16)
       Launch L;
@@ -1438,6 +1561,9 @@ int mst_lmhead_fused(mst_ctx* c, void* stream, const void* x, const int32_t* lab
                           mst::kEpiAccF32, beta));
       MST_TRY(launch(c, st, L));
     }
+    mem_free(c, (uint64_t)rows * v * 2, "inter.head.dlogits");
+    mem_free(c, part_bytes, "inter.head.partials");
+    mem_free(c, (uint64_t)rows * h * 2, "act.xT");
   }
   finalize_loss_kernel<<<1, 32, 0, st>>>(stats, nch, loss_mode);
   c->launches += 1;
@@ -1494,7 +1620,28 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
   sum_valid_kernel<<<1, 32, 0, st>>>(stats, nch);
   grad_scale_kernel<<<(nch + 255) / 256, 256, 0, st>>>(stats, stats, nch, loss_mode, grad_loss, scales);
   c->launches += 3;
+  WeightScope ws_(c, wg, wu, wd, wout);
+  const uint64_t act_bytes = (uint64_t)n * h * 2;
+  mem_alloc(c, act_bytes, "act.O");
+  mem_alloc(c, act_bytes, "act.dO");
+  mem_alloc(c, (uint64_t)n * 4, "act.lse");
   auto rows_of = [&](int j) { return b[j + 1] - b[j]; };
+  // Logical lifetimes of the chunk buffers (MemTracker events, mst.h).
+  auto mlp_fwd_live = [&](int j, bool on) {  // h (bf16), G and U (fp32) of chunk j
+    const uint64_t r = (uint64_t)rows_of(j);
+    auto f = on ? mem_alloc : mem_free;
+    f(c, r * i * 2, "inter.mlp.h");
+    f(c, r * i * 4, "inter.mlp.G");
+    f(c, r * i * 4, "inter.mlp.U");
+  };
+  auto grads_live = [&](int j, bool on) {  // dG, dU, h^T, X^T of chunk j (until K8-K10 ran)
+    const uint64_t r = (uint64_t)rows_of(j);
+    auto f = on ? mem_alloc : mem_free;
+    f(c, r * i * 2, "inter.mlp.dG");
+    f(c, r * i * 2, "inter.mlp.dU");
+    f(c, r * i * 2, "inter.mlp.hT");
+    f(c, r * h * 2, "act.xT");
+  };
   auto add_k1s = [&](Launch& L, int j) -> int {  // K1 saving G, U (fp32) and h (bf16)
     const int64_t rows = rows_of(j);
     ProblemDesc& P = L.p.prob[L.p.num_problems++];
@@ -1505,6 +1652,11 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
     s.b1 = {wu, i, h, i, true};
     s.umma_n = 256;
     MST_TRY(add_phase(c, L, P, s));
+    mlp_fwd_live(j, true);
+    cnt_mm(c, rows, h, i, (uint64_t)(h * i));     // G = X_j W_g
+    cnt_mm(c, rows, h, i, (uint64_t)(h * i));     // U = X_j W_u
+    cnt_op(c, 4ull * rows * i, 2ull * rows * i);  // silu
+    cnt_op(c, 1ull * rows * i, 3ull * rows * i);  // hadamard
     P.m_tiles = (int)cdiv(rows, 256);
     P.tile_n = 128;
     P.n_tiles = (int)cdiv(i, 128);
@@ -1541,7 +1693,14 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
       MST_TRY(launch(c, st, L));
       if (j > 0 && c->ksplit9 > 1)
         MST_TRY(splitk_combine(c, st, part9, 2, rows_of(j - 1), h, const_cast<char*>(bptr(dx, b[j - 1] * h)), h));
+      if (j > 0) grads_live(j - 1, false);
     }
+    const uint64_t part_bytes = (uint64_t)rows * nparts * 8 + (uint64_t)rows * 8;
+    mem_alloc(c, (uint64_t)rows * h * 2, "act.oT");
+    mem_alloc(c, part_bytes, "inter.head.partials");
+    mem_alloc(c, (uint64_t)rows * v * 2, "inter.head.dlogits");
+    cnt_op(c, 5ull * rows * v, (uint64_t)(rows * v + 2 * rows));      // cross-entropy forward
+    cnt_op(c, 5ull * rows * v, (uint64_t)(2 * rows * v + 2 * rows));  // cross-entropy backward
     MST_TRY(transpose_bf16(c, st, oj, h, ot, ldt, rows, h));
     {  // K3': logits GEMM, partials + softmax numerators
       Launch L;
@@ -1573,6 +1732,10 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
       MST_TRY(launch(c, st, L));
       if (c->ksplit5 > 1) MST_TRY(splitk_combine(c, st, part5, c->ksplit5, rows, h, doj, h));
     }
+    mem_free(c, (uint64_t)rows * v * 2, "inter.head.dlogits");
+    mem_free(c, part_bytes, "inter.head.partials");
+    mem_free(c, (uint64_t)rows * h * 2, "act.oT");
+    mem_alloc(c, (uint64_t)rows * i * 4, "inter.mlp.dh");
     {  // K7a: dh = dO_j W_d^T (fp32)
       Launch L;
       MST_TRY(build_plain(c, L, Operand{doj, rows, h, h, false}, Operand{wd, i, h, h, false}, dhb, i,
@@ -1584,9 +1747,14 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
       swiglu_bwd_kernel<<<(unsigned)cdiv(n4, 256), 256, 0, st>>>(g32, u32, dhb, static_cast<uint16_t*>(dg),
                                                                  static_cast<uint16_t*>(du), n4);
       c->launches += 1;
+      cnt_op(c, 4ull * rows * i, 3ull * rows * i);  // silu_backward
+      cnt_op(c, 2ull * rows * i, 6ull * rows * i);  // dG, dU products
     }
+    grads_live(j, true);
+    mem_free(c, (uint64_t)rows * i * 4, "inter.mlp.dh");
     MST_TRY(transpose_bf16(c, st, hb, i, ht, ldt, rows, i));
     MST_TRY(transpose_bf16(c, st, bptr(x, r0 * h), h, xt, ldt, rows, h));
+    mlp_fwd_live(j, false);
     if (j + 1 < nch) {
       Launch L;
       MST_TRY(add_k1s(L, j + 1));
@@ -1599,7 +1767,11 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
     MST_TRY(launch(c, st, L));
     if (c->ksplit9 > 1)
       MST_TRY(splitk_combine(c, st, part9, 2, rows_of(nch - 1), h, const_cast<char*>(bptr(dx, b[nch - 1] * h)), h));
+    grads_live(nch - 1, false);
   }
+  mem_free(c, (uint64_t)n * 4, "act.lse");
+  mem_free(c, act_bytes, "act.dO");
+  mem_free(c, act_bytes, "act.O");
   finalize_loss_kernel<<<1, 32, 0, st>>>(stats, nch, loss_mode);
   c->launches += 1;
   MST_CUDA(cudaGetLastError());

@@ -121,7 +121,21 @@ _SIGS = {
     "mst_block_step": ([_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _F32,
                         _VP, _VP, _VP, _VP, _VP, _VP, _I32, _VP, ctypes.c_size_t], ctypes.c_int),
     "mst_debug_gemm": ([_VP, _VP, _VP, _VP, _VP, _I64, _I64, _I64, _I32, _I32, _I32, _I32], ctypes.c_int),
+    "mst_ctx_get_counters": ([_VP, _VP], ctypes.c_int),
+    "mst_ctx_reset_counters": ([_VP], ctypes.c_int),
+    "mst_ctx_set_mem_hook": ([_VP, _VP, _VP], ctypes.c_int),
+    "mst_ctx_set_count_hook": ([_VP, _VP, _VP], ctypes.c_int),
 }
+
+# memtrack hooks (mst.h): kind 0 alloc / 1 free; count kind 0 matmul / 1 op.
+_MEM_HOOK = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int, ctypes.c_uint64, ctypes.c_char_p)
+_COUNT_HOOK = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                               ctypes.c_uint64)
+
+
+class _Counters(ctypes.Structure):
+    _fields_ = [("flops", ctypes.c_uint64), ("matmul_flops", ctypes.c_uint64), ("hbm_elements", ctypes.c_uint64),
+                ("weight_read_elements", ctypes.c_uint64)]
 
 _lib = None
 _lib_lock = threading.Lock()
@@ -181,6 +195,40 @@ class Context:
             self._ws = None
             self._ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=f"cuda:{self.device}")
         return self._ws
+
+    def counters(self):
+        """Op counters of this context (memtrack.hpp:19-35 conventions)."""
+        from .memtrack import OpCounters
+
+        c = _Counters()
+        _check(self.lib.mst_ctx_get_counters(self.handle, ctypes.byref(c)))
+        return OpCounters(c.flops, c.matmul_flops, c.hbm_elements, c.weight_read_elements)
+
+    def reset_counters(self) -> None:
+        _check(self.lib.mst_ctx_reset_counters(self.handle))
+
+    def attach_tracker(self, tracker) -> None:
+        """Route the library's memory events and op counts into a
+        memtrack.MemTracker (or anything with on_alloc/on_free/count_matmul/
+        count_op); None detaches."""
+        if tracker is None:
+            _check(self.lib.mst_ctx_set_mem_hook(self.handle, None, None))
+            _check(self.lib.mst_ctx_set_count_hook(self.handle, None, None))
+            self._hooks = None
+            return
+
+        def mem(_user, kind, nbytes, label):
+            (tracker.on_alloc if kind == 0 else tracker.on_free)(int(nbytes), label.decode())
+
+        def cnt(_user, kind, a, b, c, w):
+            if kind == 0:
+                tracker.count_matmul(int(a), int(b), int(c), int(w))
+            else:
+                tracker.count_op(int(a), int(b))
+
+        self._hooks = (_MEM_HOOK(mem), _COUNT_HOOK(cnt))  # keep the trampolines alive
+        _check(self.lib.mst_ctx_set_mem_hook(self.handle, ctypes.cast(self._hooks[0], ctypes.c_void_p), None))
+        _check(self.lib.mst_ctx_set_count_hook(self.handle, ctypes.cast(self._hooks[1], ctypes.c_void_p), None))
 
     def set_tuning(self, key: str, value: int) -> None:
         """Engine tuning / diagnostic knobs (mst_ctx_set_tuning in mst.h)."""

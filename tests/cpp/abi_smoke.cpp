@@ -43,6 +43,25 @@ int main() {
     threw = true;
   }
   expect(threw, "bad range -> BoundsError");
+#ifdef MST_HAVE_MINITRAIN_MEMTRACK
+  // hooks forwarding into minitrain::MemTracker::current() exist and have the ABI's types
+  mst_mem_hook mh = &mst::detail::mem_to_minitrain;
+  mst_count_hook ch = &mst::detail::count_to_minitrain;
+  (void)mh;
+  (void)ch;
+  (void)&mst::attach_current_tracker;
+  {
+    minitrain::ScopedTracker scope;
+    mst::detail::mem_to_minitrain(nullptr, 0, 4096, "inter.head.dlogits");
+    mst::detail::count_to_minitrain(nullptr, 0, 8, 4, 16, 64);
+    mst::detail::mem_to_minitrain(nullptr, 1, 4096, "inter.head.dlogits");
+    if (scope.tracker().totals().flops != 1024 || scope.tracker().live_bytes() != 0) {
+      std::printf("memtrack forwarding FAILED\n");
+      return 1;
+    }
+  }
+  std::printf("memtrack: forwarded into minitrain::MemTracker\n");
+#endif
 #ifdef MST_HAVE_MINITRAIN_ERRORS
   std::printf("errors: reference minitrain::Error hierarchy\n");
 #else
