@@ -226,6 +226,16 @@ MST_API int mst_lmhead_fused(mst_ctx* ctx, void* stream, const void* x, const in
  * mst_lmhead_fused. */
 MST_API int mst_count_valid(mst_ctx* ctx, void* stream, const int32_t* labels, int64_t n, int64_t v, float* out);
 
+/* Non-finite scan ("all elements finite after any op in this
+ * module (NaN/Inf is an error surfaced, not propagated)"): writes the number
+ * of NaN/Inf elements of a device buffer (bf16 or fp32, any element offset) to
+ * the device counter `count`, asynchronously on `stream`.  Callers that want
+ * the SPEC's NonFiniteError read it after the op and a stream sync (the
+ * Python mirror's `check_finite` / `block_step(check=True)` do exactly that). */
+enum { MST_DTYPE_BF16 = 0, MST_DTYPE_F32 = 1 };
+MST_API int mst_count_nonfinite(mst_ctx* ctx, void* stream, const void* data, int64_t n, int dtype,
+                                unsigned int* count);
+
 /* One fused MLP -> LM-Head block, forward + backward (the bench unit):
  * O = mlp(X); loss = CE(O W_out, L); then dW_out, dO, dX, dW_{gate,up,down}.
  * `stats` as in mst_lmhead_forward (device, MST_STATS_LEN(m_head) floats). */

@@ -1571,6 +1571,61 @@ int mst_lmhead_fused(mst_ctx* c, void* stream, const void* x, const int32_t* lab
   return MST_OK;
 }
 
+// Non-finite scan (NaN/Inf is an error surfaced, not propagated):
+// counts elements whose exponent field is all ones, 16 bytes per thread and
+// iteration, grid-stride over the whole buffer; HBM-bound.
+__global__ void __launch_bounds__(256) nonfinite_count_kernel(const uint8_t* head, int head_bytes,
+                                                              const uint4* __restrict__ p, int64_t n16, const uint8_t* tail,
+                                                              int tail_bytes, int f32, unsigned int* __restrict__ out) {
+  unsigned int bad = 0;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n16; k += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 w = __ldcs(p + k);
+    const uint32_t q[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (f32) {
+        bad += (q[j] & 0x7f800000u) == 0x7f800000u;
+      } else {
+        bad += (q[j] & 0x7f80u) == 0x7f80u;
+        bad += (q[j] & 0x7f800000u) == 0x7f800000u;
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 2) {  // unaligned leading / trailing bytes (< 16 each)
+    const uint8_t* q = threadIdx.x ? tail : head;
+    const int nb = threadIdx.x ? tail_bytes : head_bytes;
+    for (int b = 0; b + (f32 ? 4 : 2) <= nb; b += f32 ? 4 : 2) {
+      uint32_t v = f32 ? *reinterpret_cast<const uint32_t*>(q + b) : *reinterpret_cast<const uint16_t*>(q + b);
+      bad += f32 ? ((v & 0x7f800000u) == 0x7f800000u) : ((v & 0x7f80u) == 0x7f80u);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(out, bad);
+}
+
+int mst_count_nonfinite(mst_ctx* c, void* stream, const void* data, int64_t n, int dtype, unsigned int* count) {
+  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  if (!data || !count) return fail(MST_ERR_CONFIG, "NULL pointer");
+  if (n < 0) return fail(MST_ERR_SHAPE, "negative element count");
+  if (dtype != MST_DTYPE_BF16 && dtype != MST_DTYPE_F32) return fail(MST_ERR_DTYPE, "dtype must be bf16 or f32");
+  const int esz = dtype == MST_DTYPE_F32 ? 4 : 2;
+  if ((reinterpret_cast<uintptr_t>(data) & (esz - 1)) != 0) return fail(MST_ERR_CONFIG, "misaligned element buffer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  MST_CUDA(cudaMemsetAsync(count, 0, sizeof(unsigned int), st));
+  const uint8_t* base = static_cast<const uint8_t*>(data);
+  const int64_t bytes = n * esz;
+  const int64_t head = std::min<int64_t>(bytes, (16 - (reinterpret_cast<uintptr_t>(base) & 15)) & 15);
+  const int64_t n16 = (bytes - head) / 16;
+  const int64_t tail = bytes - head - n16 * 16;
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n16, 256), 4LL * c->num_sms));
+  nonfinite_count_kernel<<<blocks, 256, 0, st>>>(base, (int)head, reinterpret_cast<const uint4*>(base + head), n16,
+                                                   base + head + n16 * 16, (int)tail, dtype == MST_DTYPE_F32, count);
+  c->launches++;
+  MST_CUDA(cudaGetLastError());
+  return MST_OK;
+}
+
 int mst_count_valid(mst_ctx* c, void* stream, const int32_t* labels, int64_t n, int64_t v, float* out) {
   if (!c) return fail(MST_ERR_STATE, "NULL context");
   if (!labels || !out) return fail(MST_ERR_CONFIG, "NULL pointer");

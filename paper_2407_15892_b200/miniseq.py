@@ -18,6 +18,7 @@ the library is missing this module raises on import.
 from __future__ import annotations
 
 import ctypes
+import math
 import threading
 from dataclasses import dataclass
 from pathlib import Path
@@ -122,6 +123,7 @@ _SIGS = {
                         _VP, _VP, _VP, _VP, _VP, _VP, _I32, _VP, ctypes.c_size_t], ctypes.c_int),
     "mst_debug_gemm": ([_VP, _VP, _VP, _VP, _VP, _I64, _I64, _I64, _I32, _I32, _I32, _I32], ctypes.c_int),
     "mst_ctx_get_counters": ([_VP, _VP], ctypes.c_int),
+    "mst_count_nonfinite": ([_VP, _VP, _VP, _I64, _I32, _VP], ctypes.c_int),
     "mst_ctx_reset_counters": ([_VP], ctypes.c_int),
     "mst_ctx_set_mem_hook": ([_VP, _VP, _VP], ctypes.c_int),
     "mst_ctx_set_count_hook": ([_VP, _VP, _VP], ctypes.c_int),
@@ -451,6 +453,8 @@ def check_lmhead_stats(saved: LmHeadSaved) -> None:
         raise DataError(f"{int(s[3])} labels outside [0, V) and != -100")
     if s[1] == 0:
         raise DataError("all labels ignored: loss undefined (SPEC.md:219)")
+    if not math.isfinite(s[2]):
+        raise NonFiniteError(f"non-finite loss {s[2]} (SPEC.md:26)")
 
 
 def miniseq_lmhead_backward(saved: LmHeadSaved, w: LmHeadWeights, plan: ChunkPlan, mode: Optional[int] = None,
@@ -479,6 +483,29 @@ def miniseq_lmhead_backward(saved: LmHeadSaved, w: LmHeadWeights, plan: ChunkPla
                                        gs.data_ptr(), float(grad_loss), dX.data_ptr(), dW_out.data_ptr(),
                                        int(accumulate), ws.data_ptr(), ws.numel()))
     return dX, dW_out
+
+
+def count_nonfinite(t: torch.Tensor) -> torch.Tensor:
+    """Device count of NaN/Inf elements of a bf16 / fp32 tensor (int32, no sync)."""
+    ctx = Context.get(t.device.index)
+    if t.dtype not in (torch.bfloat16, torch.float32):
+        raise DtypeError(f"non-finite scan supports bf16 / fp32, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ShapeError("non-finite scan needs a contiguous tensor")
+    out = torch.empty(1, dtype=torch.int32, device=t.device)
+    _check(ctx.lib.mst_count_nonfinite(ctx.handle, _stream(t), t.data_ptr(), t.numel(),
+                                       1 if t.dtype == torch.float32 else 0, out.data_ptr()))
+    return out
+
+
+def check_finite(**tensors: torch.Tensor) -> None:
+    """Raise NonFiniteError naming every tensor with NaN/Inf elements
+    (SPEC.md:26); one host sync for all of them."""
+    counts = {k: count_nonfinite(t) for k, t in tensors.items() if t is not None and t.numel()}
+    bad = {k: int(v.item()) for k, v in counts.items()}
+    bad = {k: v for k, v in bad.items() if v}
+    if bad:
+        raise NonFiniteError("non-finite elements (SPEC.md:26): " + ", ".join(f"{k}: {v}" for k, v in bad.items()))
 
 
 def count_valid(L: torch.Tensor, V: int) -> torch.Tensor:
@@ -547,9 +574,14 @@ def alloc_block_grads(N: int, H: int, I: int, V: int, device) -> BlockGrads:
 def block_step(X: torch.Tensor, L: torch.Tensor, mlp: MlpWeights, head: LmHeadWeights, M_mlp: int, M_head: int,
                mode: int = TOKEN_WEIGHTED, grad_loss: float = 1.0, grads: Optional[BlockGrads] = None,
                stats: Optional[torch.Tensor] = None, accumulate: bool = False,
-               workspace: Optional[torch.Tensor] = None):
+               workspace: Optional[torch.Tensor] = None, check: bool = False):
     """One MLP -> LM-Head block, forward + backward (the unit the paper times,
-    PAPER.md:475).  Returns (stats, grads); stats[2] is the loss."""
+    PAPER.md:475).  Returns (stats, grads); stats[2] is the loss.
+    check=True surfaces the SPEC's errors synchronously: NonFiniteError for
+    NaN/Inf inputs or outputs, DataError for invalid labels or an
+    all-ignored batch."""
+    if check:
+        check_finite(X=X, W_gate=mlp.W_gate, W_up=mlp.W_up, W_down=mlp.W_down, W_out=head.W_out)
     ctx = Context.get(X.device.index)
     N, H = X.shape
     I = mlp.W_gate.shape[1]
@@ -572,6 +604,14 @@ def block_step(X: torch.Tensor, L: torch.Tensor, mlp: MlpWeights, head: LmHeadWe
                                   M_mlp, M_head, int(mode), float(grad_loss), stats.data_ptr(), grads.dX.data_ptr(),
                                   grads.W_gate.data_ptr(), grads.W_up.data_ptr(), grads.W_down.data_ptr(),
                                   grads.W_out.data_ptr(), int(accumulate), ws.data_ptr(), ws.numel()))
+    if check:
+        s = stats[:4].tolist()
+        if s[3] > 0:
+            raise DataError(f"{int(s[3])} labels outside [0, V) and != -100")
+        if s[1] == 0:
+            raise DataError("all labels ignored: loss undefined (SPEC.md:219)")
+        check_finite(loss=stats[2:3], dX=grads.dX, dW_gate=grads.W_gate, dW_up=grads.W_up, dW_down=grads.W_down,
+                     dW_out=grads.W_out)
     return stats, grads
 
 

@@ -302,3 +302,41 @@ def test_block_step_chunked_matches_op_by_op(shape):
     assert out[1][0] == out[0][0]
     for a, b in zip(out[1][1:], out[0][1:]):
         assert rel(a, b.double().cpu().numpy()) <= 1e-5
+
+
+def test_nonfinite_scan_counts_nan_and_inf():
+    """mst_count_nonfinite: bf16 and fp32, ragged lengths (tail bytes), NaN and
+    +-Inf anywhere."""
+    for dtype in (torch.bfloat16, torch.float32):
+        for n in (1, 7, 8, 1000, 4099, 1 << 20):
+            t = torch.randn(n, device="cuda").to(dtype)
+            assert int(ms.count_nonfinite(t).item()) == 0
+            idx = sorted({0, n // 3, n - 1})
+            vals = [float("nan"), float("inf"), float("-inf")]
+            for k, i in enumerate(idx):
+                t[i] = vals[k % 3]
+            assert int(ms.count_nonfinite(t).item()) == len(idx), (dtype, n)
+            if n > 8:  # unaligned views: leading bytes before the first 16-byte boundary
+                assert int(ms.count_nonfinite(t[1:]).item()) == len(idx) - 1, (dtype, n)
+
+
+def test_nonfinite_inputs_and_loss_raise_nonfinite_error(orc):
+    N, H, I, V = 256, 128, 128, 512
+    c = orc.make_inputs(9, N, H, I, V)
+    g = {k: torch.from_numpy(c[k]).cuda().bfloat16() for k in ("X", "Wg", "Wu", "Wd", "Wout")}
+    L = torch.from_numpy(c["L"]).cuda()
+    mlp, head = ms.MlpWeights(g["Wg"], g["Wu"], g["Wd"]), ms.LmHeadWeights(g["Wout"])
+    ms.block_step(g["X"], L, mlp, head, 2, 2, check=True)  # clean inputs pass
+    X = g["X"].clone()
+    X[17, 5] = float("nan")
+    with pytest.raises(ms.NonFiniteError, match="X"):
+        ms.block_step(X, L, mlp, head, 2, 2, check=True)
+    Wo = g["Wout"].clone()
+    Wo[3, 7] = float("inf")
+    _, hs = ms.miniseq_lmhead_forward(g["X"], L, ms.LmHeadWeights(Wo), ms.make_chunk_plan(N, 2))
+    with pytest.raises(ms.NonFiniteError):
+        ms.check_lmhead_stats(hs)
+    Lbad = L.clone()
+    Lbad[0] = V + 3
+    with pytest.raises(ms.DataError):
+        ms.block_step(g["X"], Lbad, mlp, head, 2, 2, check=True)
