@@ -168,6 +168,48 @@ MST_API int mst_ctx_reset_counters(mst_ctx* ctx);
 MST_API int mst_ctx_set_mem_hook(mst_ctx* ctx, mst_mem_hook fn, void* user);
 MST_API int mst_ctx_set_count_hook(mst_ctx* ctx, mst_count_hook fn, void* user);
 
+/* ---------------------------------------------------------------- optimizer
+ * The reference's `optim` module on the device: fp32
+ * master weights, fp32 moments, fp32 gradients (the dW accumulators), and
+ * the bf16 copy the GEMMs read.  All asynchronous on `stream`.
+ *
+ * mst_adamw_step       adamw_step: w -= lr*wd*w, then the
+ *                      Adam moment update with bias correction for `step`
+ *                      (>= 1); the gradient is multiplied by *grad_scale when
+ *                      non-NULL (device scalar: clip factor / accumulation
+ *                      steps); zero_grad != 0 clears the gradient after use.
+ * mst_grad_sumsq       squared L2 norm of one gradient into the device fp64
+ *                      *sumsq (accumulate != 0 adds to it; call once per
+ *                      tensor for a global norm), deterministic fixed-grid
+ *                      reduction through partial_ws (mst_grad_sumsq_workspace()
+ *                      doubles).  When scale_out != NULL it also writes
+ *                      clip_global_norm's factor times
+ *                      inv_steps: max_norm/||g|| if ||g|| > max_norm else 1
+ *                      (NaN when ||g|| is non-finite), and ||g|| to norm_out.
+ * mst_grad_accumulate  accumulate: into += from; the
+ *                      division by the step count is the 1/steps folded into
+ *                      grad_scale at flush. */
+typedef struct mst_adamw_config { /* doubles: 1 - beta2 must not round through fp32 */
+  double lr, weight_decay, beta1, beta2, eps;
+} mst_adamw_config;
+MST_API int mst_adamw_step(mst_ctx* ctx, void* stream, int64_t n, float* w, void* w_bf16, float* grad, float* m,
+                           float* v, const mst_adamw_config* cfg, int64_t step, const float* grad_scale,
+                           int zero_grad);
+MST_API int mst_grad_sumsq_workspace(void);
+MST_API int mst_grad_sumsq(mst_ctx* ctx, void* stream, const float* grad, int64_t n, double* partial_ws,
+                           double* sumsq, int accumulate, float max_norm, float inv_steps, float* scale_out,
+                           float* norm_out);
+MST_API int mst_grad_accumulate(mst_ctx* ctx, void* stream, float* into, const float* from, int64_t n);
+
+/* Gradient-ready hook (optimizer-in-backward): during
+ * mst_block_step the library calls fn(user, which, stream) at enqueue time
+ * right after the launch that makes a weight gradient final in stream order
+ * (which: 0 W_gate, 1 W_up, 2 W_down, 3 W_out), so the caller can enqueue
+ * that parameter's optimizer step on the same stream and release its
+ * gradient while the rest of the backward is still queued.  NULL disables. */
+typedef void (*mst_grad_ready_hook)(void* user, int which, void* stream);
+MST_API int mst_ctx_set_grad_ready_hook(mst_ctx* ctx, mst_grad_ready_hook fn, void* user);
+
 /* make_chunk_plan(N, M) — SPEC.md:286-294.  Writes min(M,N)+1 row bounds
  * into `bounds` (capacity >= min(M,N)+1): chunk c is [bounds[c], bounds[c+1]).
  * Balanced rule: the first N mod M chunks hold ceil(N/M) rows. */

@@ -24,6 +24,7 @@
 
 #include "gemm.cuh"
 #include "mst/mst.h"
+#include "optim.cuh"
 
 using mst::GemmParams;
 using mst::PhaseDesc;
@@ -131,6 +132,8 @@ struct mst_ctx {
   mst_count_hook cnt_fn = nullptr;
   void* cnt_user = nullptr;
   const void* weights[4] = {nullptr, nullptr, nullptr, nullptr};  // weight tensors of the current call
+  mst_grad_ready_hook ready_fn = nullptr;  // optimizer-in-backward hook (mst.h)
+  void* ready_user = nullptr;
 };
 
 namespace {
@@ -178,6 +181,20 @@ struct WeightScope {
   }
   ~WeightScope() { c->weights[0] = c->weights[1] = c->weights[2] = c->weights[3] = nullptr; }
 };
+
+// Weight-gradient lifetimes for the tracker: "grad.*" is allocated when a
+// block step first writes the gradient; when an optimizer-in-backward hook
+// consumes it (grad_ready below) the library also records its release,
+// otherwise the caller frees it after its optimizer step.
+const char* const kGradLabel[4] = {"grad.W_gate", "grad.W_up", "grad.W_down", "grad.W_out"};
+void grad_alloc(mst_ctx* c, int which, uint64_t bytes) { mem_alloc(c, bytes, kGradLabel[which]); }
+
+// A weight gradient is final in stream order (mst_ctx_set_grad_ready_hook).
+void grad_ready(mst_ctx* c, int which, cudaStream_t st, uint64_t bytes) {
+  if (!c->ready_fn) return;
+  c->ready_fn(c->ready_user, which, st);
+  mem_free(c, bytes, kGradLabel[which]);
+}
 
 // ------------------------------------------------------------ tensor maps
 int tmap_2d(mst_ctx* c, CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t ld_elems,
@@ -1114,6 +1131,61 @@ int mst_ctx_set_mem_hook(mst_ctx* c, mst_mem_hook fn, void* user) {
   c->mem_user = user;
   return MST_OK;
 }
+int mst_ctx_set_grad_ready_hook(mst_ctx* c, mst_grad_ready_hook fn, void* user) {
+  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  c->ready_fn = fn;
+  c->ready_user = user;
+  return MST_OK;
+}
+
+// ------------------------------------------------------------ optimizer (optim.cu)
+int mst_adamw_step(mst_ctx* c, void* stream, int64_t n, float* w, void* w_bf16, float* grad, float* m, float* v,
+                   const mst_adamw_config* cfg, int64_t step, const float* grad_scale, int zero_grad) {
+  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  if (!cfg) return fail(MST_ERR_CONFIG, "NULL AdamW config");
+  if (n < 0) return fail(MST_ERR_SHAPE, "negative parameter count");
+  if (!w || !w_bf16 || !grad || !m || !v) return fail(MST_ERR_CONFIG, "NULL tensor pointer");
+  if (step < 1) return fail(MST_ERR_CONFIG, "step must be >= 1 (bias correction), got %lld", (long long)step);
+  if (!(cfg->lr > 0.0) || !(cfg->beta1 > 0.0 && cfg->beta1 < 1.0) || !(cfg->beta2 > 0.0 && cfg->beta2 < 1.0) ||
+      !(cfg->eps > 0.0) || !(cfg->weight_decay >= 0.0))
+    return fail(MST_ERR_CONFIG, "invalid AdamW config (SPEC.md:477: lr > 0, 0 < betas < 1, eps > 0, wd >= 0)");
+  if (!mst_optim::aligned16(w) || !mst_optim::aligned16(grad) || !mst_optim::aligned16(m) ||
+      !mst_optim::aligned16(v) || (reinterpret_cast<uintptr_t>(w_bf16) & 7) != 0)
+    return fail(MST_ERR_CONFIG, "optimizer tensors must be 16-byte aligned (bf16 copy: 8-byte)");
+  if (n == 0) return MST_OK;
+  MST_CUDA(mst_optim::launch_adamw(static_cast<cudaStream_t>(stream), c->num_sms, n, w, w_bf16, grad, m, v, *cfg, step,
+                                   grad_scale, zero_grad));
+  c->launches++;
+  return MST_OK;
+}
+
+int mst_grad_sumsq_workspace(void) { return mst_optim::kSumsqBlocks; }
+
+int mst_grad_sumsq(mst_ctx* c, void* stream, const float* grad, int64_t n, double* partial_ws, double* sumsq,
+                   int accumulate, float max_norm, float inv_steps, float* scale_out, float* norm_out) {
+  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  if (!grad || !partial_ws || !sumsq) return fail(MST_ERR_CONFIG, "NULL pointer");
+  if (n < 0) return fail(MST_ERR_SHAPE, "negative element count");
+  if (!mst_optim::aligned16(grad)) return fail(MST_ERR_CONFIG, "gradient must be 16-byte aligned");
+  if (scale_out && !(max_norm > 0.f)) return fail(MST_ERR_CONFIG, "clip norm must be > 0 (SPEC.md:477)");
+  MST_CUDA(mst_optim::launch_sumsq(static_cast<cudaStream_t>(stream), grad, n, partial_ws, sumsq, accumulate, max_norm,
+                                   inv_steps, scale_out, norm_out));
+  c->launches += 2;
+  return MST_OK;
+}
+
+int mst_grad_accumulate(mst_ctx* c, void* stream, float* into, const float* from, int64_t n) {
+  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  if (!into || !from) return fail(MST_ERR_CONFIG, "NULL pointer");
+  if (n < 0) return fail(MST_ERR_SHAPE, "negative element count");
+  if (!mst_optim::aligned16(into) || !mst_optim::aligned16(from))
+    return fail(MST_ERR_CONFIG, "gradients must be 16-byte aligned");
+  if (n == 0) return MST_OK;
+  MST_CUDA(mst_optim::launch_accumulate(static_cast<cudaStream_t>(stream), c->num_sms, into, from, n));
+  c->launches++;
+  return MST_OK;
+}
+
 int mst_ctx_set_count_hook(mst_ctx* c, mst_count_hook fn, void* user) {
   if (!c) return fail(MST_ERR_STATE, "NULL context");
   c->cnt_fn = fn;
@@ -1726,6 +1798,8 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
   };
   auto add_grads = [&](Launch& L, int j) -> int {
     const int64_t rows = rows_of(j);
+    if (j == 0)
+      for (int wi = 0; wi < 3; ++wi) grad_alloc(c, wi, (uint64_t)h * i * 4);
     const int beta = (j > 0 || accumulate) ? 1 : 0;
     return add_mlp_grads(c, L, dg, du, ht, xt, bptr(dO, b[j] * h), wg, wu, const_cast<char*>(bptr(dx, b[j] * h)),
                          dwg, dwu, dwd, rows, h, i, ldt, beta, part9);
@@ -1751,6 +1825,7 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
       if (j > 0) grads_live(j - 1, false);
     }
     const uint64_t part_bytes = (uint64_t)rows * nparts * 8 + (uint64_t)rows * 8;
+    if (j == 0) grad_alloc(c, 3, (uint64_t)h * v * 4);
     mem_alloc(c, (uint64_t)rows * h * 2, "act.oT");
     mem_alloc(c, part_bytes, "inter.head.partials");
     mem_alloc(c, (uint64_t)rows * v * 2, "inter.head.dlogits");
@@ -1787,6 +1862,7 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
       MST_TRY(launch(c, st, L));
       if (c->ksplit5 > 1) MST_TRY(splitk_combine(c, st, part5, c->ksplit5, rows, h, doj, h));
     }
+    if (j == nch - 1) grad_ready(c, 3, st, (uint64_t)h * v * 4);  // dW_out complete
     mem_free(c, (uint64_t)rows * v * 2, "inter.head.dlogits");
     mem_free(c, part_bytes, "inter.head.partials");
     mem_free(c, (uint64_t)rows * h * 2, "act.oT");
@@ -1824,6 +1900,7 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
       MST_TRY(splitk_combine(c, st, part9, 2, rows_of(nch - 1), h, const_cast<char*>(bptr(dx, b[nch - 1] * h)), h));
     grads_live(nch - 1, false);
   }
+  for (int wi = 0; wi < 3; ++wi) grad_ready(c, wi, st, (uint64_t)h * i * 4);  // dW_gate, dW_up, dW_down complete
   mem_free(c, (uint64_t)n * 4, "act.lse");
   mem_free(c, act_bytes, "act.dO");
   mem_free(c, act_bytes, "act.O");
@@ -1859,6 +1936,7 @@ int mst_block_step(mst_ctx* c, void* stream, const void* x, const int32_t* label
   mst_mlp_saved ms;
   mst_lmhead_saved hs;
   MST_TRY(mst_mlp_forward(c, stream, x, wg, wu, wd, o, n, h, i, m_mlp, rest, rest_bytes, &ms));
+  grad_alloc(c, 3, (uint64_t)h * v * 4);
   if (c->fused_head) {
     MST_TRY(mst_lmhead_fused(c, stream, o, labels, wout, n, h, v, m_head, loss_mode, grad_loss, nullptr, stats, lse,
                              dO, dwout, accumulate, rest, rest_bytes));
@@ -1867,7 +1945,10 @@ int mst_block_step(mst_ctx* c, void* stream, const void* x, const int32_t* label
                                &hs));
     MST_TRY(mst_lmhead_backward(c, stream, &hs, wout, stats, grad_loss, dO, dwout, accumulate, rest, rest_bytes));
   }
+  grad_ready(c, 3, static_cast<cudaStream_t>(stream), (uint64_t)h * v * 4);
+  for (int wi = 0; wi < 3; ++wi) grad_alloc(c, wi, (uint64_t)h * i * 4);
   MST_TRY(mst_mlp_backward(c, stream, dO, &ms, wg, wu, wd, dx, dwg, dwu, dwd, accumulate, rest, rest_bytes));
+  for (int wi = 0; wi < 3; ++wi) grad_ready(c, wi, static_cast<cudaStream_t>(stream), (uint64_t)h * i * 4);
   return MST_OK;
 }
 

@@ -135,6 +135,21 @@ _COUNT_HOOK = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int, ctypes.c_int
                                ctypes.c_uint64)
 
 
+class _AdamCfg(ctypes.Structure):  # mst_adamw_config
+    _fields_ = [("lr", ctypes.c_double), ("weight_decay", ctypes.c_double), ("beta1", ctypes.c_double),
+                ("beta2", ctypes.c_double), ("eps", ctypes.c_double)]
+
+
+_SIGS.update({  # optimizer, used by optim.py
+    "mst_adamw_step": ([_VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP, ctypes.POINTER(_AdamCfg), _I64, _VP, _I32],
+                       ctypes.c_int),
+    "mst_grad_sumsq_workspace": ([], ctypes.c_int),
+    "mst_grad_sumsq": ([_VP, _VP, _VP, _I64, _VP, _VP, _I32, ctypes.c_float, ctypes.c_float, _VP, _VP], ctypes.c_int),
+    "mst_grad_accumulate": ([_VP, _VP, _VP, _VP, _I64], ctypes.c_int),
+    "mst_ctx_set_grad_ready_hook": ([_VP, _VP, _VP], ctypes.c_int),
+})
+
+
 class _Counters(ctypes.Structure):
     _fields_ = [("flops", ctypes.c_uint64), ("matmul_flops", ctypes.c_uint64), ("hbm_elements", ctypes.c_uint64),
                 ("weight_read_elements", ctypes.c_uint64)]

@@ -69,8 +69,11 @@ def _block_counts(M, tracker=None):
     try:
         if tracker is not None:
             tracker.region_begin("block")
-        ms.block_step(g["X"], L, ms.MlpWeights(g["Wg"], g["Wu"], g["Wd"]), ms.LmHeadWeights(g["Wout"]), M, M)
+        _, gr = ms.block_step(g["X"], L, ms.MlpWeights(g["Wg"], g["Wu"], g["Wd"]), ms.LmHeadWeights(g["Wout"]), M, M)
         torch.cuda.synchronize()
+        if tracker is not None:  # deferred optimizer: the caller releases the gradients
+            for k, t in (("W_gate", gr.W_gate), ("W_up", gr.W_up), ("W_down", gr.W_down), ("W_out", gr.W_out)):
+                tracker.on_free(t.numel() * 4, f"grad.{k}")
         region = tracker.region_end("block") if tracker is not None else None
     finally:
         ctx.attach_tracker(None)
