@@ -240,15 +240,22 @@ def main() -> None:
     import torch.distributed as dist
 
     from paper_2407_15892_b200 import miniseq as ms
-    from paper_2407_15892_b200.parallel import GpuOps, sp_block_step
+    from paper_2407_15892_b200.parallel import GpuOps, sp_block_step_fused
 
     world, rank, local = dist_env()
     if world != args.gpus and rank == 0:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # MST_SAME_DEVICE=1 + MST_DIST_BACKEND=gloo: every rank on cuda:0 (exercises
+    # the N>1 code path on a one-GPU box; never used for reported numbers)
+    gpu = 0 if os.environ.get("MST_SAME_DEVICE") == "1" else local
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
+    backend = os.environ.get("MST_DIST_BACKEND", "nccl")
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     S, Mm, Mh = args.seq, args.m_mlp, args.m_head
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
@@ -261,7 +268,7 @@ def main() -> None:
     L = torch.randint(0, V, (S,), device=dev, generator=g, dtype=torch.int32)
     L[torch.rand(S, device=dev, generator=g) < 0.05] = -100
     mlp, head = ms.MlpWeights(Wg, Wu, Wd), ms.LmHeadWeights(Wo)
-    ctx = ms.Context.get(local)
+    ctx = ms.Context.get(gpu)
     grads = ms.alloc_block_grads(S, H, I, V, dev)
     nch = min(S, Mh)
     stats = torch.empty(ms.stats_len(nch), dtype=torch.float32, device=dev)
@@ -270,16 +277,26 @@ def main() -> None:
     if world == 1:
         def step():
             ms.block_step(X, L, mlp, head, Mm, Mh, grads=grads, stats=stats, workspace=ws)
+            return stats[2:3]
     else:
         ops = GpuOps()
-        gtuple = (grads.W_gate, grads.W_up, grads.W_down, grads.W_out)
+        # N>1: the op-by-op block schedule finishes dW_out after the LM-Head, so
+        # its 2.1 GB all-reduce (issued from the gradient-ready hook) overlaps
+        # the whole MLP backward; the chunk-wise schedule (N=1 default) would
+        # expose most of it.  MST_SP_CHUNKED=1 selects the chunk-wise one.
+        sp_chunked = os.environ.get("MST_SP_CHUNKED") == "1"
+        ctx.set_tuning("chunked_block", 1 if sp_chunked else 0)
 
-        def step():
-            sp_block_step(ops, X, L, (Wg, Wu, Wd), Wo, Mm, Mh, gtuple)
+        def step():  # global valid count -> fused block (global scale) -> hook-driven dW all-reduces -> loss
+            return sp_block_step_fused(ops, X, L, (Wg, Wu, Wd), Wo, Mm, Mh, grads, workspace=ws,
+                                       stats=stats).loss.reshape(1)
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if backend == "nccl":
+                dist.barrier(device_ids=[gpu])
+            else:
+                dist.barrier()
 
     stream = torch.cuda.current_stream(dev)
     torch.cuda.reset_peak_memory_stats(dev)
@@ -295,7 +312,7 @@ def main() -> None:
     barrier()
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(gpu) as clk:
         e0.record(stream)
         for _ in range(args.steps):
             step()
@@ -307,7 +324,7 @@ def main() -> None:
     launches = ctx.launch_count - launches0
     ms_total = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([ms_total], device=dev)
+        t = torch.tensor([ms_total], device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t)
     ms_step = ms_total / args.steps
@@ -324,8 +341,7 @@ def main() -> None:
         def step_e2e():
             X.copy_(Xh, non_blocking=True)
             L.copy_(Lh, non_blocking=True)
-            step()
-            loss_h.copy_(stats[2:3] if world == 1 else stats[2:3], non_blocking=True)
+            loss_h.copy_(step(), non_blocking=True)
 
         for _ in range(2):
             step_e2e()
@@ -338,13 +354,13 @@ def main() -> None:
         barrier()
         dt = (time.perf_counter() - t0) / args.steps
         if world > 1:
-            t = torch.tensor([dt], device=dev)
+            t = torch.tensor([dt], device=dev if backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t)
         e2e = {"value": tokens_step / dt, "unit": UNIT, "h2d_bytes_per_step": Xh.numel() * 2 + Lh.numel() * 4,
                "d2h_bytes_per_step": 4, "ms_per_step": dt * 1e3,
                "path": "pinned host X/labels -> H2D, miniseq.block_step (C ABI mst_block_step) "
-                       "[sp_block_step + NCCL for N>1], loss D2H; wall clock with synchronize"}
+                       "[sp_block_step_fused: mst_block_step_sp + NCCL for N>1], loss D2H; wall clock with synchronize"}
 
     if rank != 0:
         if world > 1:
@@ -368,6 +384,9 @@ def main() -> None:
                                f"S={S} tokens/GPU, M_mlp={Mm} M_head={Mh}",
                    "H": H, "I": I, "V": V, "seq_len": S, "global_tokens": tokens_step, "M_mlp": Mm, "M_head": Mh,
                    "parallelism": f"sp{world}" if world > 1 else "single",
+                   "schedule": "chunk-wise (MLP fwd -> head -> MLP bwd per chunk)" if world == 1 or
+                               os.environ.get("MST_SP_CHUNKED") == "1" else
+                               "op-by-op (MLP fwd, head fwd+bwd, MLP bwd; dW_out all-reduce overlaps the MLP backward)",
                    "l2": "no flush: every step streams 1.4 GB of bf16 weights and 2.8 GB of fp32 dW (>> 126 MB L2)"},
         "tflops_per_gpu": tflops_step,
         "executed_flops_per_token": executed_fpt,

@@ -287,6 +287,18 @@ MST_API int mst_block_step(mst_ctx* ctx, void* stream, const void* x, const int3
                    void* grad_x, float* grad_w_gate, float* grad_w_up, float* grad_w_down, float* grad_w_out,
                    int accumulate, void* workspace, size_t workspace_bytes);
 
+/* Sequence-parallel variant: identical, except that the
+ * token-weighted dlogits scale uses the device scalar *global_valid (the
+ * valid-label count all-reduced over the ranks, mst_count_valid + SUM) so
+ * the per-rank weight gradients sum to the single-device gradient.  `stats`
+ * keeps the rank-local loss sum / count (entries 0..1, additive).  NULL
+ * global_valid == mst_block_step.  Paper-mean mode ignores it. */
+MST_API int mst_block_step_sp(mst_ctx* ctx, void* stream, const void* x, const int32_t* labels, const void* w_gate,
+                   const void* w_up, const void* w_down, const void* w_out, int64_t n, int64_t h, int64_t i,
+                   int64_t v, int64_t m_mlp, int64_t m_head, int loss_mode, float grad_loss, float* stats,
+                   void* grad_x, float* grad_w_gate, float* grad_w_up, float* grad_w_down, float* grad_w_out,
+                   int accumulate, void* workspace, size_t workspace_bytes, const float* global_valid);
+
 /* Diagnostic single GEMM through the same engine: C[M,N] = A[M,K] B[K,N].
  * a_mn=0: A row-major [M,K]; a_mn=1: A given as row-major [K,M] (A^T).
  * b_mn=1: B row-major [K,N]; b_mn=0: B given as row-major [N,K] (B^T).

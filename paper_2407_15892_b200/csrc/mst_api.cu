@@ -1723,7 +1723,8 @@ int mst_count_valid(mst_ctx* c, void* stream, const int32_t* labels, int64_t n, 
 static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const int32_t* labels, const void* wg,
                               const void* wu, const void* wd, const void* wout, int64_t n, int64_t h, int64_t i,
                               int64_t v, int64_t m, int loss_mode, float grad_loss, float* stats, void* dx, float* dwg,
-                              float* dwu, float* dwd, float* dwout, int accumulate, void* ws, size_t ws_bytes) {
+                              float* dwu, float* dwd, float* dwout, int accumulate, void* ws, size_t ws_bytes,
+                              const float* global_valid) {
   char* base = static_cast<char*>(ws);
   const size_t ob = align_up(size_t(n) * h * 2, 256);
   void* o = base;
@@ -1745,7 +1746,12 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
   MST_CUDA(cudaMemsetAsync(stats, 0, sizeof(float) * MST_STATS_LEN(nch), st));
   chunk_valid_kernel<<<nch, 256, 0, st>>>(labels, n, nch, (int)v, stats);
   sum_valid_kernel<<<1, 32, 0, st>>>(stats, nch);
-  grad_scale_kernel<<<(nch + 255) / 256, 256, 0, st>>>(stats, stats, nch, loss_mode, grad_loss, scales);
+  float* gstats = stats;
+  if (global_valid) {  // sequence-parallel caller: dlogits scaled by the all-reduced token count
+    gstats = c->scratch_dev + 64;
+    MST_CUDA(cudaMemcpyAsync(gstats + 1, global_valid, sizeof(float), cudaMemcpyDeviceToDevice, st));
+  }
+  grad_scale_kernel<<<(nch + 255) / 256, 256, 0, st>>>(gstats, stats, nch, loss_mode, grad_loss, scales);
   c->launches += 3;
   WeightScope ws_(c, wg, wu, wd, wout);
   const uint64_t act_bytes = (uint64_t)n * h * 2;
@@ -1914,6 +1920,14 @@ int mst_block_step(mst_ctx* c, void* stream, const void* x, const int32_t* label
                    const void* wd, const void* wout, int64_t n, int64_t h, int64_t i, int64_t v, int64_t m_mlp,
                    int64_t m_head, int loss_mode, float grad_loss, float* stats, void* dx, float* dwg, float* dwu,
                    float* dwd, float* dwout, int accumulate, void* ws, size_t ws_bytes) {
+  return mst_block_step_sp(c, stream, x, labels, wg, wu, wd, wout, n, h, i, v, m_mlp, m_head, loss_mode, grad_loss,
+                           stats, dx, dwg, dwu, dwd, dwout, accumulate, ws, ws_bytes, nullptr);
+}
+
+int mst_block_step_sp(mst_ctx* c, void* stream, const void* x, const int32_t* labels, const void* wg, const void* wu,
+                      const void* wd, const void* wout, int64_t n, int64_t h, int64_t i, int64_t v, int64_t m_mlp,
+                      int64_t m_head, int loss_mode, float grad_loss, float* stats, void* dx, float* dwg, float* dwu,
+                      float* dwd, float* dwout, int accumulate, void* ws, size_t ws_bytes, const float* global_valid) {
   if (!c) return fail(MST_ERR_STATE, "NULL context");
   size_t need = 0;
   MST_TRY(mst_block_workspace(n, h, i, v, m_mlp, m_head, &need));
@@ -1924,7 +1938,8 @@ int mst_block_step(mst_ctx* c, void* stream, const void* x, const int32_t* label
     return fail(MST_ERR_CONFIG, "NULL tensor pointer");
   if (c->chunked_block && c->fused_head && m_mlp == m_head)
     return block_step_chunked(c, static_cast<cudaStream_t>(stream), x, labels, wg, wu, wd, wout, n, h, i, v, m_mlp,
-                              loss_mode, grad_loss, stats, dx, dwg, dwu, dwd, dwout, accumulate, ws, ws_bytes);
+                              loss_mode, grad_loss, stats, dx, dwg, dwu, dwd, dwout, accumulate, ws, ws_bytes,
+                              global_valid);
   char* base = static_cast<char*>(ws);
   const size_t ob = align_up(size_t(n) * h * 2, 256);
   void* o = base;
@@ -1938,9 +1953,10 @@ int mst_block_step(mst_ctx* c, void* stream, const void* x, const int32_t* label
   MST_TRY(mst_mlp_forward(c, stream, x, wg, wu, wd, o, n, h, i, m_mlp, rest, rest_bytes, &ms));
   grad_alloc(c, 3, (uint64_t)h * v * 4);
   if (c->fused_head) {
-    MST_TRY(mst_lmhead_fused(c, stream, o, labels, wout, n, h, v, m_head, loss_mode, grad_loss, nullptr, stats, lse,
+    MST_TRY(mst_lmhead_fused(c, stream, o, labels, wout, n, h, v, m_head, loss_mode, grad_loss, global_valid, stats, lse,
                              dO, dwout, accumulate, rest, rest_bytes));
   } else {
+    if (global_valid) return fail(MST_ERR_CONFIG, "global_valid needs the fused LM-Head (tuning fused_head=1)");
     MST_TRY(mst_lmhead_forward(c, stream, o, labels, wout, n, h, v, m_head, loss_mode, stats, lse, rest, rest_bytes,
                                &hs));
     MST_TRY(mst_lmhead_backward(c, stream, &hs, wout, stats, grad_loss, dO, dwout, accumulate, rest, rest_bytes));

@@ -121,6 +121,8 @@ _SIGS = {
     "mst_count_valid": ([_VP, _VP, _VP, _I64, _I64, _VP], ctypes.c_int),
     "mst_block_step": ([_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _F32,
                         _VP, _VP, _VP, _VP, _VP, _VP, _I32, _VP, ctypes.c_size_t], ctypes.c_int),
+    "mst_block_step_sp": ([_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _F32,
+                           _VP, _VP, _VP, _VP, _VP, _VP, _I32, _VP, ctypes.c_size_t, _VP], ctypes.c_int),
     "mst_debug_gemm": ([_VP, _VP, _VP, _VP, _VP, _I64, _I64, _I64, _I32, _I32, _I32, _I32], ctypes.c_int),
     "mst_ctx_get_counters": ([_VP, _VP], ctypes.c_int),
     "mst_count_nonfinite": ([_VP, _VP, _VP, _I64, _I32, _VP], ctypes.c_int),
@@ -148,6 +150,9 @@ _SIGS.update({  # optimizer, used by optim.py
     "mst_grad_accumulate": ([_VP, _VP, _VP, _VP, _I64], ctypes.c_int),
     "mst_ctx_set_grad_ready_hook": ([_VP, _VP, _VP], ctypes.c_int),
 })
+
+
+_GRAD_READY_HOOK = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p)
 
 
 class _Counters(ctypes.Structure):
@@ -589,12 +594,18 @@ def alloc_block_grads(N: int, H: int, I: int, V: int, device) -> BlockGrads:
 def block_step(X: torch.Tensor, L: torch.Tensor, mlp: MlpWeights, head: LmHeadWeights, M_mlp: int, M_head: int,
                mode: int = TOKEN_WEIGHTED, grad_loss: float = 1.0, grads: Optional[BlockGrads] = None,
                stats: Optional[torch.Tensor] = None, accumulate: bool = False,
-               workspace: Optional[torch.Tensor] = None, check: bool = False):
+               workspace: Optional[torch.Tensor] = None, check: bool = False,
+               global_valid: Optional[torch.Tensor] = None, grad_ready=None):
     """One MLP -> LM-Head block, forward + backward (the unit the paper times,
     PAPER.md:475).  Returns (stats, grads); stats[2] is the loss.
     check=True surfaces the SPEC's errors synchronously: NonFiniteError for
     NaN/Inf inputs or outputs, DataError for invalid labels or an
-    all-ignored batch."""
+    all-ignored batch.
+    global_valid: device fp32 [1] valid-label count all-reduced over a
+    sequence-parallel group (mst_block_step_sp).  grad_ready(which): called
+    while the step is enqueued, right after the launch that makes gradient
+    `which` (0 W_gate, 1 W_up, 2 W_down, 3 W_out) final in stream order
+    (mst_ctx_set_grad_ready_hook)."""
     if check:
         check_finite(X=X, W_gate=mlp.W_gate, W_up=mlp.W_up, W_down=mlp.W_down, W_out=head.W_out)
     ctx = Context.get(X.device.index)
@@ -614,11 +625,22 @@ def block_step(X: torch.Tensor, L: torch.Tensor, mlp: MlpWeights, head: LmHeadWe
         stats = torch.empty(stats_len(nch), dtype=torch.float32, device=X.device)
     need = block_workspace_bytes(N, H, I, V, M_mlp, M_head)
     ws = workspace if workspace is not None else ctx.workspace(need)
-    _check(ctx.lib.mst_block_step(ctx.handle, _stream(X), X.data_ptr(), L.data_ptr(), mlp.W_gate.data_ptr(),
-                                  mlp.W_up.data_ptr(), mlp.W_down.data_ptr(), head.W_out.data_ptr(), N, H, I, V,
-                                  M_mlp, M_head, int(mode), float(grad_loss), stats.data_ptr(), grads.dX.data_ptr(),
-                                  grads.W_gate.data_ptr(), grads.W_up.data_ptr(), grads.W_down.data_ptr(),
-                                  grads.W_out.data_ptr(), int(accumulate), ws.data_ptr(), ws.numel()))
+    if global_valid is not None:
+        _req(global_valid, "global_valid", torch.float32, (1,))
+    hook = None
+    if grad_ready is not None:
+        hook = _GRAD_READY_HOOK(lambda _u, which, _s: grad_ready(int(which)))
+        _check(ctx.lib.mst_ctx_set_grad_ready_hook(ctx.handle, ctypes.cast(hook, ctypes.c_void_p), None))
+    try:
+        _check(ctx.lib.mst_block_step_sp(ctx.handle, _stream(X), X.data_ptr(), L.data_ptr(), mlp.W_gate.data_ptr(),
+                                         mlp.W_up.data_ptr(), mlp.W_down.data_ptr(), head.W_out.data_ptr(), N, H, I,
+                                         V, M_mlp, M_head, int(mode), float(grad_loss), stats.data_ptr(),
+                                         grads.dX.data_ptr(), grads.W_gate.data_ptr(), grads.W_up.data_ptr(),
+                                         grads.W_down.data_ptr(), grads.W_out.data_ptr(), int(accumulate),
+                                         ws.data_ptr(), ws.numel(), _ptr(global_valid)))
+    finally:
+        if hook is not None:
+            _check(ctx.lib.mst_ctx_set_grad_ready_hook(ctx.handle, None, None))
     if check:
         s = stats[:4].tolist()
         if s[3] > 0:

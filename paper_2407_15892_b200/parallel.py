@@ -76,6 +76,51 @@ class GpuOps:
         g = self.ms.MlpGrads(*grads)
         return self.ms.miniseq_mlp_backward(dO, saved, self.ms.MlpWeights(*w), saved.plan, grads=g)[0]
 
+    def block_step(self, X, L, w, Wout, M_mlp, M_head, grads, global_valid, grad_ready, workspace=None, stats=None):
+        """The whole fused block (mst_block_step_sp, chunk-wise schedule) with the
+        global valid count; grad_ready(which) fires as each dW becomes final."""
+        ms = self.ms
+        N, H = X.shape
+        bg = ms.BlockGrads(dX=torch.empty(N, H, device=X.device, dtype=torch.bfloat16), W_gate=grads[0],
+                           W_up=grads[1], W_down=grads[2], W_out=grads[3]) if not isinstance(grads, ms.BlockGrads) \
+            else grads
+        stats, bg = ms.block_step(X, L, ms.MlpWeights(*w), ms.LmHeadWeights(Wout), M_mlp, M_head, grads=bg,
+                                  stats=stats, workspace=workspace, global_valid=global_valid, grad_ready=grad_ready)
+        return stats, bg.dX
+
+
+def sp_block_step_fused(ops, X: torch.Tensor, L: torch.Tensor, w: tuple, Wout: torch.Tensor, M_mlp: int,
+                        M_head: int, grads: tuple, group=None, overlap: bool = True, **kw) -> StepResult:
+    """Sequence-parallel step on the fused chunk-wise block (the fast path):
+    one all-reduce of the valid count before the step, the block itself with
+    the global count (mst_block_step_sp), each weight gradient's SUM
+    all-reduce issued from the library's gradient-ready hook the moment it is
+    final (dW_out after the LM-Head backward of the last chunk, overlapping
+    that chunk's MLP backward; the MLP gradients at the end), then the loss
+    pair.  Same results as sp_block_step (tests/test_dist_gloo.py)."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    valid = ops.count_valid(L, Wout.shape[1])
+    if world > 1:
+        dist.all_reduce(valid, op=dist.ReduceOp.SUM, group=group)
+    works = []
+    gl = (grads.W_gate, grads.W_up, grads.W_down, grads.W_out) if hasattr(grads, "W_out") else tuple(grads)
+
+    def ready(which: int) -> None:
+        if world > 1:
+            works.append(dist.all_reduce(gl[which], op=dist.ReduceOp.SUM, group=group, async_op=overlap))
+
+    stats, dX = ops.block_step(X, L, w, Wout, M_mlp, M_head, grads, valid, ready, **kw)
+    gstats = stats.clone()
+    if world > 1:
+        head = gstats[:2].contiguous()
+        dist.all_reduce(head, op=dist.ReduceOp.SUM, group=group)
+        gstats[:2] = head
+    for wk in works:
+        if wk is not None:
+            wk.wait()
+    loss = gstats[0] / gstats[1]
+    return StepResult(loss=loss, stats=gstats, dX=dX, dW_gate=gl[0], dW_up=gl[1], dW_down=gl[2], dW_out=gl[3])
+
 
 def sp_block_step(ops, X: torch.Tensor, L: torch.Tensor, w: tuple, Wout: torch.Tensor, M_mlp: int, M_head: int,
                   grads: tuple, group=None, overlap: bool = True, fused: bool = True) -> StepResult:

@@ -55,6 +55,17 @@ class OracleOps:
             g.copy_(torch.from_numpy(v))
         return torch.from_numpy(dX)
 
+    def block_step(self, X, L, w, Wout, M_mlp, M_head, grads, global_valid, grad_ready):
+        """Stand-in for GpuOps.block_step (mst_block_step_sp): same call order
+        of the gradient-ready hook (W_out after the head, MLP weights at the end)."""
+        O, ms = self.mlp_forward(X, w, M_mlp)
+        stats, dO = self.lmhead_fused(O, L, Wout, M_head, global_valid, grads[3])
+        grad_ready(3)
+        dX = self.mlp_backward(dO, ms, w, grads[:3])
+        for k in range(3):
+            grad_ready(k)
+        return stats, dX
+
 
 def _inputs(orc):
     c = orc.make_inputs(31, N, H, I, V, p_ignore=0.15, w_std=0.3)
@@ -62,12 +73,12 @@ def _inputs(orc):
     return c
 
 
-def _worker(rank, world, port, ret, fused):
+def _worker(rank, world, port, ret, mode):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from oracle import oracle as orc
-        from paper_2407_15892_b200.parallel import shard_rows, sp_block_step
+        from paper_2407_15892_b200.parallel import shard_rows, sp_block_step, sp_block_step_fused
 
         c = _inputs(orc)
         s, e = shard_rows(N, world, rank)
@@ -75,7 +86,10 @@ def _worker(rank, world, port, ret, fused):
         X, L = f(c["X"][s:e]), torch.from_numpy(c["L"][s:e].copy())
         w = (f(c["Wg"]), f(c["Wu"]), f(c["Wd"]))
         grads = tuple(torch.zeros_like(t) for t in (*w, f(c["Wout"])))
-        r = sp_block_step(OracleOps(orc), X, L, w, f(c["Wout"]), M_MLP, M_HEAD, grads, fused=fused)
+        if mode == "block":  # the bench's fast path: whole fused block + hook-driven gradient all-reduces
+            r = sp_block_step_fused(OracleOps(orc), X, L, w, f(c["Wout"]), M_MLP, M_HEAD, grads)
+        else:
+            r = sp_block_step(OracleOps(orc), X, L, w, f(c["Wout"]), M_MLP, M_HEAD, grads, fused=mode == "fused")
         ref = orc.block(c["X"], c["L"], c["Wg"], c["Wu"], c["Wd"], c["Wout"], M_MLP, M_HEAD, round_bf16=False)
         errs = dict(loss=abs(float(r.loss) - ref["loss"]),
                     dX=float(np.abs(r.dX.numpy() - ref["dX"][s:e]).max()),
@@ -94,11 +108,12 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world,fused", [(1, True), (2, True), (4, True), (2, False)])
-def test_sequence_parallel_matches_single_process(world, fused, orc):
+@pytest.mark.parametrize("world,mode", [(1, "fused"), (2, "fused"), (4, "fused"), (2, "separate"), (1, "block"),
+                                        (2, "block"), (4, "block")])
+def test_sequence_parallel_matches_single_process(world, mode, orc):
     mgr = mp.Manager()
     ret = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), ret, fused), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), ret, mode), nprocs=world, join=True)
     assert len(ret) == world
     for rank, errs in ret.items():
         assert errs["loss"] <= 1e-12, (rank, errs)

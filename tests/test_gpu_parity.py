@@ -340,3 +340,24 @@ def test_nonfinite_inputs_and_loss_raise_nonfinite_error(orc):
     Lbad[0] = V + 3
     with pytest.raises(ms.DataError):
         ms.block_step(g["X"], Lbad, mlp, head, 2, 2, check=True)
+
+
+def test_block_step_sp_global_valid_scaling(orc):
+    """mst_block_step_sp: global_valid == the local count reproduces
+    block_step bitwise; twice the count halves every gradient exactly
+    (the scale is a power of two, so bf16 dlogits and fp32 sums are exact)."""
+    N, H, I, V = 512, 128, 256, 1024
+    c = orc.make_inputs(21, N, H, I, V)
+    g = to_gpu(c)
+    mlp, head = ms.MlpWeights(g["Wg"], g["Wu"], g["Wd"]), ms.LmHeadWeights(g["Wout"])
+    _, ref = ms.block_step(g["X"], g["L"], mlp, head, 4, 4)
+    ref = {k: getattr(ref, k).clone() for k in ("dX", "W_gate", "W_up", "W_down", "W_out")}
+    nv = ms.count_valid(g["L"], V)
+    calls = []
+    _, same = ms.block_step(g["X"], g["L"], mlp, head, 4, 4, global_valid=nv.clone(), grad_ready=calls.append)
+    assert calls == [3, 0, 1, 2]  # W_out after the head, the MLP weights at the end
+    for k, t in ref.items():
+        assert torch.equal(getattr(same, k), t), k
+    _, half = ms.block_step(g["X"], g["L"], mlp, head, 4, 4, global_valid=2 * nv)
+    for k, t in ref.items():
+        assert torch.equal(getattr(half, k).float(), t.float() * 0.5), k
