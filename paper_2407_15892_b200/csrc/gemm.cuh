@@ -171,12 +171,18 @@ struct TileFeed {
   int slot;
   uint32_t phase;
 
-  // Leader producer (dynamic) / any role (static).
+  // Leader producer (dynamic) / any role (static).  tile_counter[0] is the
+  // claim counter, [1] counts pairs that are done claiming; the last such
+  // pair re-zeroes both for the next launch on the stream (no memset).
   __device__ __forceinline__ int32_t produce(const GemmParams& p) {
     if (!p.dynamic) return it < n ? list[it++] : -1;
     ptx::mbar_wait(ptx::smem_u32(&empty[slot]), phase ^ 1);
     const int32_t t = atomicAdd(p.tile_counter, 1);
     const int32_t code = t < p.total_tiles ? __ldg(p.order + t) : -1;
+    if (code < 0 && atomicAdd(p.tile_counter + 1, 1) == static_cast<int32_t>(gridDim.x / 2) - 1) {
+      atomicExch(p.tile_counter, 0);
+      atomicExch(p.tile_counter + 1, 0);
+    }
     codes[slot] = code;
     ptx::st_shared_cluster_u32(ptx::mapa(ptx::smem_u32(&codes[slot]), 1), static_cast<uint32_t>(code));
     ptx::mbar_arrive_local(ptx::smem_u32(&full[slot]));

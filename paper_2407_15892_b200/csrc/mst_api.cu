@@ -460,7 +460,8 @@ int launch(mst_ctx* c, cudaStream_t st, Launch& L) {
   MST_TRY(get_schedule(c, p, &p.sched, &p.sched_off, &p.order, &p.total_tiles));
   p.dynamic = c->dynamic;
   p.tile_counter = reinterpret_cast<int32_t*>(c->scratch_dev);
-  if (p.dynamic) MST_CUDA(cudaMemsetAsync(p.tile_counter, 0, sizeof(int32_t), st));
+  // p.tile_counter[0..1] are zero here: zeroed at context creation, and every
+  // dynamic launch re-zeroes them on exit (gemm.cuh TileFeed::produce).
   // profile slots: 8 counters per launch, 64 slots round robin
   p.prof = c->prof ? c->prof + 8 * (c->prof_slot++ % 64) : nullptr;
   cudaLaunchConfig_t cfg;
@@ -1008,6 +1009,7 @@ int mst_ctx_create(int device, mst_ctx** out) {
   c->num_pairs = std::min(clusters, c->num_sms / 2);
   c->max_pairs = c->num_pairs;
   e = cudaMalloc(&c->scratch_dev, 4096);
+  if (e == cudaSuccess) e = cudaMemset(c->scratch_dev, 0, 4096);
   if (e != cudaSuccess) {
     delete c;
     return fail(MST_ERR_CUDA, "cudaMalloc: %s", cudaGetErrorString(e));
