@@ -299,6 +299,40 @@ MST_API int mst_block_step_sp(mst_ctx* ctx, void* stream, const void* x, const i
                    void* grad_x, float* grad_w_gate, float* grad_w_up, float* grad_w_down, float* grad_w_out,
                    int accumulate, void* workspace, size_t workspace_bytes, const float* global_valid);
 
+/* ---------------------------------------------------------------- decoder layer
+ * The plumbing around the MsT blocks in the reference's Llama-style decoder
+ * (model module SPEC.md:410-469, blocks-std rmsnorm SPEC.md:242-250):
+ *
+ * mst_gemm             C[M,N] = A[M,K] B[K,N] (+ C) on the tcgen05 engine,
+ *                      any operand majorness (semantics of mst_debug_gemm below)
+ * mst_rmsnorm_forward  s = x + residual (bf16, written to sum_out; residual may
+ *                      be NULL: s = x), y = s * gain / sqrt(mean(s^2) + eps),
+ *                      rstd[n] fp32 saved for the backward.  bf16 x/y, fp32 gain.
+ * mst_rmsnorm_backward dx = d(rmsnorm)/ds * dy (+ dres, the residual branch's
+ *                      gradient), dgain (+)= sum over rows (fp32, fixed-order
+ *                      block partials: deterministic); workspace from
+ *                      mst_rmsnorm_workspace.
+ * mst_embedding_forward  out[t] = table[tokens[t]]; tokens outside [0, vocab)
+ *                      are counted into the device int *bad_count (the caller
+ *                      raises DataError, "token out of range").
+ * mst_embedding_backward dtable[v] (+)= sum of dx rows of the positions holding
+ *                      token v, positions grouped by token (order = positions
+ *                      stably sorted by token, seg = nseg+1 group starts, uniq =
+ *                      the token of each group): fixed summation order. */
+MST_API int mst_gemm(mst_ctx* ctx, void* stream, const void* a, const void* b, void* c, int64_t m, int64_t n, int64_t k,
+                     int a_mn, int b_mn, int out_f32, int beta);
+MST_API int mst_rmsnorm_forward(mst_ctx* ctx, void* stream, const void* x, const void* residual, const float* gain,
+                                void* y, void* sum_out, float* rstd, int64_t n, int64_t d, float eps);
+MST_API int mst_rmsnorm_workspace(const mst_ctx* ctx, int64_t n, int64_t d, size_t* bytes);
+MST_API int mst_rmsnorm_backward(mst_ctx* ctx, void* stream, const void* s, const float* gain, const float* rstd,
+                                 const void* dy, const void* dres, void* dx, float* dgain, int accumulate, int64_t n,
+                                 int64_t d, void* workspace, size_t workspace_bytes);
+MST_API int mst_embedding_forward(mst_ctx* ctx, void* stream, const void* table, const int32_t* tokens, void* out,
+                                  int64_t n, int64_t d, int64_t vocab, int* bad_count);
+MST_API int mst_embedding_backward(mst_ctx* ctx, void* stream, const int32_t* order, const int32_t* seg,
+                                   const int32_t* uniq, int64_t nseg, const void* dx, float* dtable, int64_t d,
+                                   int64_t vocab, int accumulate);
+
 /* Diagnostic single GEMM through the same engine: C[M,N] = A[M,K] B[K,N].
  * a_mn=0: A row-major [M,K]; a_mn=1: A given as row-major [K,M] (A^T).
  * b_mn=1: B row-major [K,N]; b_mn=0: B given as row-major [N,K] (B^T).

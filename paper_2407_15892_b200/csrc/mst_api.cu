@@ -24,6 +24,7 @@
 
 #include "gemm.cuh"
 #include "mst/mst.h"
+#include "layers.cuh"
 #include "optim.cuh"
 
 using mst::GemmParams;
@@ -1967,6 +1968,84 @@ int mst_block_step_sp(mst_ctx* c, void* stream, const void* x, const int32_t* la
   for (int wi = 0; wi < 3; ++wi) grad_alloc(c, wi, (uint64_t)h * i * 4);
   MST_TRY(mst_mlp_backward(c, stream, dO, &ms, wg, wu, wd, dx, dwg, dwu, dwd, accumulate, rest, rest_bytes));
   for (int wi = 0; wi < 3; ++wi) grad_ready(c, wi, static_cast<cudaStream_t>(stream), (uint64_t)h * i * 4);
+  return MST_OK;
+}
+
+// ------------------------------------------------------------ decoder-layer ops (layers.cu)
+int mst_gemm(mst_ctx* c, void* stream, const void* a, const void* b, void* out, int64_t m, int64_t n, int64_t k,
+             int a_mn, int b_mn, int out_f32, int beta) {
+  return mst_debug_gemm(c, stream, a, b, out, m, n, k, a_mn, b_mn, out_f32, beta);
+}
+
+static int check_rows(int64_t n, int64_t d) {
+  if (n <= 0 || d <= 0) return fail(MST_ERR_SHAPE, "extents must be positive (n=%lld d=%lld)", (long long)n, (long long)d);
+  if (d % 8) return fail(MST_ERR_SHAPE, "hidden size must be a multiple of 8 (d=%lld)", (long long)d);
+  if (d > 16384) return fail(MST_ERR_BOUNDS, "hidden size %lld > 16384", (long long)d);
+  return MST_OK;
+}
+
+int mst_rmsnorm_forward(mst_ctx* c, void* stream, const void* x, const void* residual, const float* gain, void* y,
+                        void* sum_out, float* rstd, int64_t n, int64_t d, float eps) {
+  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  MST_TRY(check_rows(n, d));
+  if (!x || !gain || !y || !rstd || (residual && !sum_out)) return fail(MST_ERR_CONFIG, "NULL tensor pointer");
+  if (!(eps > 0.f)) return fail(MST_ERR_CONFIG, "eps must be > 0");
+  MST_CUDA(mst_layers::rmsnorm_fwd(static_cast<cudaStream_t>(stream), c->num_sms, x, residual, gain, y, sum_out, rstd, n,
+                                   (int)d, eps));
+  c->launches++;
+  cnt_op(c, 4ull * n * d, 2ull * n * d);  // rmsnorm fwd (memtrack.hpp:30)
+  if (residual) cnt_op(c, 1ull * n * d, 3ull * n * d);
+  return MST_OK;
+}
+
+int mst_rmsnorm_workspace(const mst_ctx* c, int64_t n, int64_t d, size_t* bytes) {
+  if (!c || !bytes) return fail(MST_ERR_STATE, "NULL context or output");
+  MST_TRY(check_rows(n, d));
+  *bytes = sizeof(float) * (size_t)mst_layers::rmsnorm_bwd_parts(n, c->num_sms) * (size_t)d;
+  return MST_OK;
+}
+
+int mst_rmsnorm_backward(mst_ctx* c, void* stream, const void* s, const float* gain, const float* rstd, const void* dy,
+                         const void* dres, void* dx, float* dgain, int accumulate, int64_t n, int64_t d, void* ws,
+                         size_t ws_bytes) {
+  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  MST_TRY(check_rows(n, d));
+  if (!s || !gain || !rstd || !dy || !dx || !dgain) return fail(MST_ERR_CONFIG, "NULL tensor pointer");
+  if (d > 6144) return fail(MST_ERR_BOUNDS, "rmsnorm backward supports d <= 6144 (per-warp dgain rows in smem)");
+  size_t need = 0;
+  MST_TRY(mst_rmsnorm_workspace(c, n, d, &need));
+  if (!ws || ws_bytes < need) return fail(MST_ERR_CONFIG, "workspace too small (%zu < %zu)", ws_bytes, need);
+  MST_CUDA(mst_layers::rmsnorm_bwd(static_cast<cudaStream_t>(stream), c->num_sms, s, gain, rstd, dy, dres, dx,
+                                   static_cast<float*>(ws), dgain, accumulate, n, (int)d));
+  c->launches += 2;
+  cnt_op(c, 8ull * n * d, 4ull * n * d);  // rmsnorm bwd (memtrack.hpp:30)
+  return MST_OK;
+}
+
+int mst_embedding_forward(mst_ctx* c, void* stream, const void* table, const int32_t* tokens, void* out, int64_t n,
+                          int64_t d, int64_t vocab, int* bad_count) {
+  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  MST_TRY(check_rows(n, d));
+  if (vocab <= 0) return fail(MST_ERR_SHAPE, "vocabulary must be >= 1");
+  if (!table || !tokens || !out || !bad_count) return fail(MST_ERR_CONFIG, "NULL pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  MST_CUDA(cudaMemsetAsync(bad_count, 0, sizeof(int), st));
+  MST_CUDA(mst_layers::embed_fwd(st, c->num_sms, table, tokens, out, n, (int)d, vocab, bad_count));
+  c->launches++;
+  cnt_op(c, 0, 2ull * n * d);
+  return MST_OK;
+}
+
+int mst_embedding_backward(mst_ctx* c, void* stream, const int32_t* order, const int32_t* seg, const int32_t* uniq,
+                           int64_t nseg, const void* dx, float* dtable, int64_t d, int64_t vocab, int accumulate) {
+  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  if (d <= 0 || d % 8 || vocab <= 0 || nseg < 0) return fail(MST_ERR_SHAPE, "bad embedding extents");
+  if (nseg > 0 && (!order || !seg || !uniq || !dx)) return fail(MST_ERR_CONFIG, "NULL pointer");
+  if (!dtable) return fail(MST_ERR_CONFIG, "NULL gradient table");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!accumulate) MST_CUDA(cudaMemsetAsync(dtable, 0, sizeof(float) * (size_t)vocab * (size_t)d, st));
+  MST_CUDA(mst_layers::embed_bwd(st, c->num_sms, order, seg, uniq, (int)nseg, dx, dtable, (int)d, 1));
+  c->launches++;
   return MST_OK;
 }
 

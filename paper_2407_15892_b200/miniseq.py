@@ -152,6 +152,16 @@ _SIGS.update({  # optimizer, used by optim.py
 })
 
 
+_SIGS.update({  # decoder-layer plumbing (model module), used by model.py
+    "mst_gemm": ([_VP, _VP, _VP, _VP, _VP, _I64, _I64, _I64, _I32, _I32, _I32, _I32], ctypes.c_int),
+    "mst_rmsnorm_forward": ([_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, ctypes.c_float], ctypes.c_int),
+    "mst_rmsnorm_workspace": ([_VP, _I64, _I64, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
+    "mst_rmsnorm_backward": ([_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I32, _I64, _I64, _VP, ctypes.c_size_t],
+                             ctypes.c_int),
+    "mst_embedding_forward": ([_VP, _VP, _VP, _VP, _VP, _I64, _I64, _I64, _VP], ctypes.c_int),
+    "mst_embedding_backward": ([_VP, _VP, _VP, _VP, _VP, _I64, _VP, _VP, _I64, _I64, _I32], ctypes.c_int),
+})
+
 _GRAD_READY_HOOK = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p)
 
 

@@ -83,10 +83,14 @@ class OptimState:
     def create(weights: Dict[str, torch.Tensor]) -> "OptimState":
         st = OptimState()
         for k, w in weights.items():
-            if w.dtype != torch.bfloat16 or not w.is_cuda:
-                raise ms.DtypeError(f"{k}: parameters are bf16 CUDA tensors")
-            st.params[k] = ParamState(w, w.float().contiguous(), torch.zeros(w.shape, device=w.device),
-                                      torch.zeros(w.shape, device=w.device))
+            if w.dtype not in (torch.bfloat16, torch.float32) or not w.is_cuda or not w.is_contiguous():
+                raise ms.DtypeError(f"{k}: parameters are contiguous bf16 or fp32 CUDA tensors")
+            if w.dtype == torch.float32:  # fp32 parameter (e.g. RMSNorm gains): it is its own master copy
+                st.params[k] = ParamState(torch.empty(w.shape, device=w.device, dtype=torch.bfloat16), w,
+                                          torch.zeros(w.shape, device=w.device), torch.zeros(w.shape, device=w.device))
+            else:
+                st.params[k] = ParamState(w, w.float().contiguous(), torch.zeros(w.shape, device=w.device),
+                                          torch.zeros(w.shape, device=w.device))
         return st
 
 
