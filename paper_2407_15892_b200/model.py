@@ -226,28 +226,61 @@ class Saved:
 
 
 class Model:
-    """forward / backward of SPEC.md:430-451 over libmst kernels."""
+    """forward / backward of SPEC.md:430-451 over libmst kernels.
 
-    def __init__(self, cfg: ModelConfig, weights: Optional[ModelWeights] = None, device="cuda"):
+    group: a torch.distributed process group over which ONE sequence is
+    sharded (Ulysses sequence parallelism, ulysses.py): cfg.S is then this
+    rank's shard length (B must be 1), attention re-shards to heads with
+    all-to-alls, the LM-Head uses the global valid-label count, the loss is
+    the global token-weighted mean and backward() returns SUM-all-reduced
+    weight gradients."""
+
+    def __init__(self, cfg: ModelConfig, weights: Optional[ModelWeights] = None, device="cuda", group=None):
         cfg.validate()
         self.cfg = cfg
         self.w = weights if weights is not None else init_weights(cfg, device)
+        self.group = group
+        self.world = 1
+        if group is not None:
+            import torch.distributed as dist
+
+            self.world = dist.get_world_size(group)
+            if self.world > 1 and cfg.B != 1:
+                raise ms.ConfigError("sequence parallelism shards one sequence: B must be 1")
 
     # ---------------------------------------------------------------- attention
     def _attention(self, qkv: torch.Tensor, need_grad: bool):
+        """Causal GQA over qkv [N, d + 2d/G] -> (o [N, d], (q, k, v) autograd leaves)."""
         cfg = self.cfg
         B, S, h, hd, kvh = cfg.B, cfg.S, cfg.heads, cfg.head_dim, cfg.heads // cfg.G
+        if self.world > 1:
+            from . import ulysses
+
+            q, k, v = (qkv[:, :cfg.d].contiguous(), qkv[:, cfg.d:cfg.d + cfg.kv].contiguous(),
+                       qkv[:, cfg.d + cfg.kv:].contiguous())
+            if need_grad:
+                q, k, v = (t.requires_grad_(True) for t in (q, k, v))
+            return ulysses.attention(q, k, v, h, kvh, self.group), (q, k, v)
         q = qkv[:, :cfg.d].reshape(B, S, h, hd).transpose(1, 2)
         k = qkv[:, cfg.d:cfg.d + cfg.kv].reshape(B, S, kvh, hd).transpose(1, 2)
         v = qkv[:, cfg.d + cfg.kv:].reshape(B, S, kvh, hd).transpose(1, 2)
         if need_grad:
             q, k, v = (t.detach().requires_grad_(True) for t in (q, k, v))
         o = F.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=kvh != h)
-        return o, (q, k, v)
+        return o.transpose(1, 2).reshape(B * S, cfg.d), (q, k, v)
 
-    def _attn_out(self, o4: torch.Tensor) -> torch.Tensor:
+    def _grad_qkv(self, leaves, N: int) -> torch.Tensor:
+        """Assemble d qkv [N, d + 2d/G] from the autograd leaves of _attention."""
         cfg = self.cfg
-        return o4.transpose(1, 2).reshape(cfg.B * cfg.S, cfg.d).contiguous()
+        q, k, v = leaves
+        if self.world > 1:
+            return torch.cat([q.grad, k.grad, v.grad], dim=1)
+        kvh = cfg.heads // cfg.G
+        dqkv = torch.empty(N, cfg.d + 2 * cfg.kv, device=q.device, dtype=torch.bfloat16)
+        dqkv[:, :cfg.d] = q.grad.transpose(1, 2).reshape(N, cfg.d)
+        dqkv[:, cfg.d:cfg.d + cfg.kv] = k.grad.transpose(1, 2).reshape(N, kvh * cfg.head_dim)
+        dqkv[:, cfg.d + cfg.kv:] = v.grad.transpose(1, 2).reshape(N, kvh * cfg.head_dim)
+        return dqkv
 
     # ---------------------------------------------------------------- forward
     def _layer_forward(self, lw: LayerWeights, x: torch.Tensor, resid: Optional[torch.Tensor]):
@@ -260,8 +293,8 @@ class Model:
         qkv = torch.empty(N, cfg.d + 2 * cfg.kv, device=x.device, dtype=torch.bfloat16)
         gemm(a, lw.W_qkv, N, cfg.d + 2 * cfg.kv, cfg.d, False, True, qkv)
         with torch.no_grad():
-            o4, _ = self._attention(qkv, need_grad=False)
-        o = self._attn_out(o4)
+            o, _ = self._attention(qkv, need_grad=False)
+        o = o.contiguous()
         ao = torch.empty_like(o)
         gemm(o, lw.W_o, N, cfg.d, cfg.d, False, True, ao)
         b, x2, rstd2 = rmsnorm_forward(ao, lw.g_mlp, cfg.eps, residual=xs)
@@ -293,8 +326,19 @@ class Model:
             x, resid = m, x2
         f, x_last, rstd_f = rmsnorm_forward(x, self.w.g_final, cfg.eps, residual=resid)
         dW_out = torch.empty(cfg.d, cfg.V, device=f.device, dtype=torch.float32)
+        gv = None
+        if self.world > 1:  # token-weighted loss over the whole sequence
+            gv = ms.count_valid(lab, cfg.V)
+            self._all_reduce(gv)
         loss, stats, _, dF, _ = ms.miniseq_lmhead_fused(f, lab, ms.LmHeadWeights(self.w.W_out),
-                                                        ms.make_chunk_plan(N, cfg.M_head), dW_out=dW_out)
+                                                        ms.make_chunk_plan(N, cfg.M_head), dW_out=dW_out,
+                                                        global_valid=gv)
+        if self.world > 1:
+            pair = stats[:2].clone()
+            self._all_reduce(pair)
+            stats = stats.clone()
+            stats[:2] = pair
+            loss = pair[0] / pair[1]
         if check:
             s = stats[:4].tolist()
             if s[1] == 0:
@@ -320,7 +364,21 @@ class Model:
         dE = torch.empty(cfg.V, cfg.d, device=dx.device, dtype=torch.float32)
         embedding_backward(saved.tokens, dx, dE, accumulate=False)
         grads["embedding"] = dE
+        if self.world > 1:
+            from . import ulysses
+
+            ulysses.all_reduce_grads(grads, self.group)
         return grads
+
+    def _all_reduce(self, t: torch.Tensor) -> None:
+        import torch.distributed as dist
+
+        if dist.get_backend(self.group) == "gloo" and t.is_cuda:
+            c = t.cpu()
+            dist.all_reduce(c, group=self.group)
+            t.copy_(c)
+        else:
+            dist.all_reduce(t, group=self.group)
 
     def _layer_backward(self, li: int, lw: LayerWeights, sv: _LayerSaved, dx3: torch.Tensor, grads) -> torch.Tensor:
         cfg = self.cfg
@@ -331,8 +389,8 @@ class Model:
             qkv = torch.empty(N, cfg.d + 2 * cfg.kv, device=a.device, dtype=torch.bfloat16)
             gemm(a, lw.W_qkv, N, cfg.d + 2 * cfg.kv, cfg.d, False, True, qkv)
             with torch.no_grad():
-                o4, _ = self._attention(qkv, need_grad=False)
-            o = self._attn_out(o4)
+                o, _ = self._attention(qkv, need_grad=False)
+            o = o.contiguous()
             ao = torch.empty_like(o)
             gemm(o, lw.W_o, N, cfg.d, cfg.d, False, True, ao)
             b, x2, rstd2 = rmsnorm_forward(ao, lw.g_mlp, cfg.eps, residual=sv.x)
@@ -354,14 +412,10 @@ class Model:
         grads[f"{p}.W_o"] = dWo
         do = torch.empty_like(o)
         gemm(dx2, lw.W_o, N, cfg.d, cfg.d, False, False, do)              # dx2 W_o^T
-        # attention backward (library kernel through autograd)
-        o4, (q, k, v) = self._attention(qkv, need_grad=True)
-        o4.backward(do.reshape(cfg.B, cfg.S, cfg.heads, cfg.head_dim).transpose(1, 2))
-        dqkv = torch.empty_like(qkv)
-        kvh = cfg.heads // cfg.G
-        dqkv[:, :cfg.d] = q.grad.transpose(1, 2).reshape(N, cfg.d)
-        dqkv[:, cfg.d:cfg.d + cfg.kv] = k.grad.transpose(1, 2).reshape(N, kvh * cfg.head_dim)
-        dqkv[:, cfg.d + cfg.kv:] = v.grad.transpose(1, 2).reshape(N, kvh * cfg.head_dim)
+        # attention backward (library kernel through autograd; Ulysses all-to-alls when sharded)
+        o_re, leaves = self._attention(qkv, need_grad=True)
+        o_re.backward(do)
+        dqkv = self._grad_qkv(leaves, N).contiguous()
         dWqkv = torch.empty(cfg.d, cfg.d + 2 * cfg.kv, device=a.device, dtype=torch.float32)
         gemm(a, dqkv, cfg.d, cfg.d + 2 * cfg.kv, N, True, True, dWqkv)    # a^T dqkv
         grads[f"{p}.W_qkv"] = dWqkv
