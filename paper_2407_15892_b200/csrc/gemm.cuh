@@ -92,6 +92,7 @@ enum EpiKind : int32_t {
   kEpiCeBwd = 5,      // dlogits = (softmax - onehot) * scale              (TMA store)
   kEpiCeFwdNum = 6,   // kEpiCeFwd + softmax numerator 2^(z log2e - m_tile) (TMA store, bf16)
   kEpiSwigluSave = 7, // kEpiSwiglu + G, U saved in fp32 (chunk-wise block: no backward recompute)
+  kEpiDhSwigluBwd = 8,// acc = dh; G, U (fp32, global: aux / aux2) -> dG, dU bf16 (TMA stores)
 };
 
 struct PhaseDesc {
@@ -125,7 +126,8 @@ struct ProblemDesc {
   void* out0;          // kEpiAccF32 with red.global: output base pointers (halves g = 0, 1)
   void* out1;
   int64_t ld0, ld1;
-  const float* aux;    // kEpiSwigluBwd: dh [rows, ld_aux] fp32
+  const float* aux;    // kEpiSwigluBwd: dh [rows, ld_aux] fp32; kEpiDhSwigluBwd: G
+  const float* aux2;   // kEpiDhSwigluBwd: U [rows, ld_aux] fp32
   const int32_t* labels;
   const float* lse;    // kEpiCeBwd: log-sum-exp per row (natural log)
   const float* scale;  // kEpiCeBwd: device scalar gradient scale
@@ -559,6 +561,56 @@ __device__ __forceinline__ void run_epilogue(const GemmParams& p, const ProblemD
         st.put_bf16x32(bu, 0, du_keep[0]);
         st.put_bf16x32(bu, 1, du_keep[1]);
         st.issue(bu, &p.maps[P.map_out2], tn * 128 + c, row0, false);
+      }
+      break;
+    }
+    case kEpiDhSwigluBwd: {
+      // D = dh (256 columns of I per CTA row block); the forward's fp32 G, U of
+      // the same elements come from global memory (one 128-byte line per
+      // thread and 32 columns).  Same arithmetic as the stand-alone SwiGLU
+      // backward, so the result is bitwise that of the unfused schedule.
+      const int half = P.ph[0].umma_n >> 1;
+      for (int g = 0; g < 2; ++g) {
+        const int colb = tn * P.tile_n + (g ? P.col_off1 : P.col_off0);
+        for (int c = 0; c < half; c += 64) {
+          const int bg = st.acquire();
+          const int bu = st.acquire_second();
+#pragma unroll
+          for (int s2 = 0; s2 < 2; ++s2) {
+            float dh[32], gv[32], uv[32];
+            epi::load32(taddr + g * half + c + 32 * s2, dh);
+            const int col = colb + c + 32 * s2;
+            if (row_ok && col + 32 <= P.cols) {
+              const float4* sg = reinterpret_cast<const float4*>(P.aux + static_cast<int64_t>(row) * P.ld_aux + col);
+              const float4* su = reinterpret_cast<const float4*>(P.aux2 + static_cast<int64_t>(row) * P.ld_aux + col);
+#pragma unroll
+              for (int q4 = 0; q4 < 8; ++q4) {
+                const float4 a = __ldcs(sg + q4), b = __ldcs(su + q4);
+                gv[4 * q4] = a.x, gv[4 * q4 + 1] = a.y, gv[4 * q4 + 2] = a.z, gv[4 * q4 + 3] = a.w;
+                uv[4 * q4] = b.x, uv[4 * q4 + 1] = b.y, uv[4 * q4 + 2] = b.z, uv[4 * q4 + 3] = b.w;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const bool ok = row_ok && col + j < P.cols;
+                gv[j] = ok ? P.aux[static_cast<int64_t>(row) * P.ld_aux + col + j] : 0.f;
+                uv[j] = ok ? P.aux2[static_cast<int64_t>(row) * P.ld_aux + col + j] : 0.f;
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float s_ = epi::sigmoid(gv[j]);
+              const float act = gv[j] * s_;
+              const float dgv = dh[j] * uv[j] * (s_ * (1.0f + gv[j] * (1.0f - s_)));
+              uv[j] = dh[j] * act;
+              gv[j] = dgv;
+            }
+            st.put_bf16x32(bg, s2, gv);
+            st.put_bf16x32(bu, s2, uv);
+          }
+          st.issue(bg, &p.maps[P.map_out0], colb + c, row0, false);
+          st.issue(bu, &p.maps[P.map_out1], colb + c, row0, false);
+        }
       }
       break;
     }

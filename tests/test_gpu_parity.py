@@ -292,16 +292,22 @@ def test_block_step_chunked_matches_op_by_op(shape):
     mlp, head = ms.MlpWeights(*W[:3]), ms.LmHeadWeights(W[3])
     ctx = ms.Context.get(0)
     out = {}
-    for chunked in (1, 0):
+    for key, (chunked, fused) in {1: (1, 0), 0: (0, 0), "f": (1, 1)}.items():
         ms._check(ctx.lib.mst_ctx_set_tuning(ctx.handle, b"chunked_block", chunked))
+        ms._check(ctx.lib.mst_ctx_set_tuning(ctx.handle, b"fuse_swiglu_bwd", fused))
         st, gr = ms.block_step(X, L, mlp, head, M, M)
         torch.cuda.synchronize()
-        out[chunked] = (float(st[2]), gr.dX.clone(), gr.W_gate.clone(), gr.W_up.clone(), gr.W_down.clone(),
-                        gr.W_out.clone())
+        out[key] = (float(st[2]), gr.dX.clone(), gr.W_gate.clone(), gr.W_up.clone(), gr.W_down.clone(),
+                    gr.W_out.clone())
     ms._check(ctx.lib.mst_ctx_set_tuning(ctx.handle, b"chunked_block", 1))
+    ms._check(ctx.lib.mst_ctx_set_tuning(ctx.handle, b"fuse_swiglu_bwd", 0))
     assert out[1][0] == out[0][0]
     for a, b in zip(out[1][1:], out[0][1:]):
         assert rel(a, b.double().cpu().numpy()) <= 1e-5
+    # SwiGLU backward fused into the dh GEMM epilogue (tuning fuse_swiglu_bwd=1): same values
+    assert out["f"][0] == out[1][0]
+    for a, b in zip(out["f"][1:], out[1][1:]):
+        assert rel(a, b.double().cpu().numpy()) <= 1e-6
 
 
 def test_nonfinite_scan_counts_nan_and_inf():
