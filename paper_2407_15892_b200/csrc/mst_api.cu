@@ -116,6 +116,7 @@ struct mst_ctx {
   unsigned long long* prof = nullptr;
   int64_t prof_slot = 0;
   int sched_mode = 0;  // MST_SCHED: 0 plain LPT, 1 LPT + long tile last on alternate pairs, 2 long tile mid-list
+  int interleave_pct = 0;  // dynamic order: long tiles spread over the first pct% of the short ones (0: LPT)
   int dynamic = 1;     // MST_DYNAMIC: pairs pull tiles from the global LPT order (atomic counter)
   int ksplit5 = 1;     // split-K of the LM-Head dX GEMM (K5): 1, 2 or 4
   int ksplit9 = 1;     // MLP dX GEMM (K9): 1 = two-phase accumulate, 2 = one problem per phase + combine
@@ -421,7 +422,25 @@ int get_schedule(mst_ctx* c, const GemmParams& p, const int32_t** sched, const i
     size_t w = np + 1;
     for (int q = 0; q < np; ++q)
       for (int32_t code : per[q]) host[w++] = code;
-    for (const T& t : tiles) host[w++] = t.code;  // global LPT order (dynamic mode)
+    if (c->interleave_pct > 0) {
+      // Dynamic order with the long (compute-bound, e.g. K5 dX) tiles spread
+      // evenly over the first interleave_pct% of the short (e.g. K6 dW
+      // reduce-add, DRAM-heavy) tiles instead of all first, so the short
+      // tiles' DRAM traffic overlaps the long tiles' math.
+      const double med = tiles[tiles.size() / 2].cost;
+      std::vector<int32_t> lng, sht;
+      for (const T& t : tiles) (t.cost > 4.0 * med ? lng : sht).push_back(t.code);
+      const size_t span = std::min(sht.size(), (size_t)(sht.size() * (c->interleave_pct / 100.0)));
+      size_t si = 0;
+      for (size_t li = 0; li < lng.size(); ++li) {
+        host[w++] = lng[li];
+        const size_t upto = lng.empty() ? 0 : span * (li + 1) / lng.size();
+        while (si < upto) host[w++] = sht[si++];
+      }
+      while (si < sht.size()) host[w++] = sht[si++];
+    } else {
+      for (const T& t : tiles) host[w++] = t.code;  // global LPT order (dynamic mode)
+    }
     SchedEntry e;
     e.num_pairs = np;
     e.total = (int32_t)tiles.size();
@@ -1097,6 +1116,9 @@ int mst_ctx_set_tuning(mst_ctx* c, const char* key, int value) {
     c->fused_head = value != 0;
   } else if (std::strcmp(key, "chunked_block") == 0) {
     c->chunked_block = value != 0;
+  } else if (std::strcmp(key, "interleave") == 0) {
+    if (value < 0 || value > 100) return fail(MST_ERR_CONFIG, "interleave must be 0..100");
+    c->interleave_pct = value;
   } else if (std::strcmp(key, "wide") == 0) {
     c->wide = value != 0;
   } else if (std::strcmp(key, "fuse_swiglu_bwd") == 0) {
