@@ -138,3 +138,17 @@ def test_separate_ops_events_balanced_and_timeline():
     assert {"inter.mlp.h", "inter.mlp.dh", "inter.mlp.dG", "inter.head.dlogits", "inter.head.partials"} <= labels
     # the one live [S/M, V] buffer: dlogits of one 128-row chunk
     assert reg.report.peak_for_prefix("inter.head.dlogits") == (N // 4) * V * 2
+
+
+@pytest.mark.parametrize("M", [1, 2, 8])
+def test_estimator_block_peak_matches_tracked_device_allocations(M):
+    """estimator.predict_block_peak == the tracked peaks of a real block step
+    on the device, per label class (SPEC.md:579 'tracker agreement', exact
+    here rather than within 10%)."""
+    from paper_2407_15892_b200 import estimator
+
+    t = mt.MemTracker()
+    _, reg = _block_counts(M, t)
+    pred = estimator.predict_block_peak(N, H, I, V, M)
+    for prefix, b in pred.items():
+        assert reg.report.peak_for_prefix(prefix) == b, (prefix, reg.report.peak_for_prefix(prefix), b)
