@@ -649,8 +649,45 @@ __global__ void __launch_bounds__(256) transpose_bf16_kernel(const uint16_t* __r
   }
 }
 
+// Register-only transpose: each thread moves one 8 x 8 block (8 coalesced
+// 16-byte row loads, 32 byte permutes, 8 16-byte stores); a warp covers 32
+// rows x 64 columns, a 256-thread block 256 rows x 64 columns.  cols % 8 == 0;
+// ragged rows are zero-filled into the destination's padding (ld_dst >= rows
+// rounded up to 8), which the consumers' tensor maps never read.
+__global__ void __launch_bounds__(256) transpose8_bf16_kernel(const uint16_t* __restrict__ src, int64_t ld_src,
+                                                               uint16_t* __restrict__ dst, int64_t ld_dst, int rows,
+                                                               int cols) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r0 = blockIdx.y * 256 + warp * 32 + (lane >> 3) * 8;  // this thread's 8 source rows
+  const int c0 = blockIdx.x * 64 + (lane & 7) * 8;                 // and 8 source columns
+  if (r0 >= rows || c0 >= cols) return;
+  uint32_t in[8][4];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r0 + k < rows) v = __ldcs(reinterpret_cast<const uint4*>(src + static_cast<int64_t>(r0 + k) * ld_src + c0));
+    in[k][0] = v.x, in[k][1] = v.y, in[k][2] = v.z, in[k][3] = v.w;
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {  // output row c0 + j holds source column c0 + j of rows r0..r0+7
+    uint32_t o[4];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) o[w] = __byte_perm(in[2 * w][j >> 1], in[2 * w + 1][j >> 1], (j & 1) ? 0x7632 : 0x5410);
+    *reinterpret_cast<uint4*>(dst + static_cast<int64_t>(c0 + j) * ld_dst + r0) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 int transpose_bf16(mst_ctx* c, cudaStream_t st, const void* src, int64_t ld_src, void* dst, int64_t ld_dst,
                    int64_t rows, int64_t cols) {
+  if (cols % 8 == 0 && ld_dst % 8 == 0 && ld_dst >= (rows + 7) / 8 * 8 && ld_src % 8 == 0 &&
+      (reinterpret_cast<uintptr_t>(src) & 15) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    dim3 grid((unsigned)cdiv(cols, 64), (unsigned)cdiv(rows, 256));
+    transpose8_bf16_kernel<<<grid, 256, 0, st>>>(static_cast<const uint16_t*>(src), ld_src,
+                                                  static_cast<uint16_t*>(dst), ld_dst, (int)rows, (int)cols);
+    c->launches++;
+    MST_CUDA(cudaGetLastError());
+    return MST_OK;
+  }
   dim3 grid((unsigned)cdiv(cols, 64), (unsigned)cdiv(rows, 64));
   transpose_bf16_kernel<<<grid, 256, 0, st>>>(static_cast<const uint16_t*>(src), ld_src, static_cast<uint16_t*>(dst),
                                                ld_dst, (int)rows, (int)cols);

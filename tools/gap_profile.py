@@ -35,7 +35,7 @@ busy = {}
 gaps = []
 prev_end = t_begin
 for e in seg:
-    k = e.name.split('(')[0].split('::')[-1][:40]
+    k = e.name.replace('(anonymous namespace)::', '').split('(')[0].split('::')[-1][:40]
     d = e.time_range.end - e.time_range.start
     busy.setdefault(k, [0, 0.0])
     busy[k][0] += 1
