@@ -203,6 +203,41 @@ struct TileFeed {
     advance();
     return code;
   }
+  // Warp-wide variants (all 32 lanes call; lane 0 performs the single-thread
+  // actions): the returned code is broadcast from lane 0 so everything the
+  // role derives from it stays warp-uniform (uniform-datapath registers, no
+  // per-instruction ELECT/R2UR loops around the TMA and MMA issues).
+  __device__ __forceinline__ int32_t produce_warp(const GemmParams& p, int lane) {
+    int32_t code = -1;
+    if (!p.dynamic) {
+      code = it < n ? list[it] : -1;
+      ++it;
+    } else {
+      ptx::mbar_wait(ptx::smem_u32(&empty[slot]), phase ^ 1);
+      if (lane == 0) {
+        const int32_t t = atomicAdd(p.tile_counter, 1);
+        code = t < p.total_tiles ? __ldg(p.order + t) : -1;
+        if (code < 0 && atomicAdd(p.tile_counter + 1, 1) == static_cast<int32_t>(gridDim.x / 2) - 1) {
+          atomicExch(p.tile_counter, 0);
+          atomicExch(p.tile_counter + 1, 0);
+        }
+        codes[slot] = code;
+        ptx::st_shared_cluster_u32(ptx::mapa(ptx::smem_u32(&codes[slot]), 1), static_cast<uint32_t>(code));
+        ptx::mbar_arrive_local(ptx::smem_u32(&full[slot]));
+        ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&full[slot]), 1));
+      }
+      advance();
+    }
+    return uniform(__shfl_sync(0xffffffffu, code, 0));
+  }
+  __device__ __forceinline__ int32_t consume_warp(const GemmParams& p, int lane) {
+    return uniform(consume(p, lane));
+  }
+  // A warp-wide reduction of identical values: REDUX writes a uniform
+  // register, so ptxas treats everything derived from it as warp-uniform.
+  __device__ __forceinline__ static int32_t uniform(int32_t v) {
+    return static_cast<int32_t>(__reduce_min_sync(0xffffffffu, static_cast<uint32_t>(v)));
+  }
   __device__ __forceinline__ void advance() {
     if (++slot == kTileSlots) {
       slot = 0;
@@ -774,7 +809,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   ptx::tc_fence_before();
   ptx::cluster_sync();
   ptx::tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_base = __reduce_min_sync(0xffffffffu, *tmem_slot);  // uniform register
 
   TileFeed feed{p.sched + p.sched_off[pair], p.sched_off[pair + 1] - p.sched_off[pair], 0, tile_codes,
                 tile_full, tile_empty, 0, 0};
@@ -787,7 +822,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // path whenever the MMA waits for operands.
     const bool do_a = warp == 0;
     const bool do_b = !MST_SPLIT_PRODUCER || warp == 3;
-    if (lane == 0) {
+    {  // the whole warp walks the loop; lane 0 issues the barrier arrivals and TMA loads
+      const bool issuer = lane == 0;
       uint64_t pols[3];
       pols[0] = ptx::policy_evict_normal();
       pols[1] = ptx::policy_evict_last();
@@ -804,7 +840,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t sphase = 0, sa = slots_u32, sb = b_region;
       MST_PROF_DECL
       for (;;) {
-        const int32_t code = (rank == 0 && warp == 0) ? feed.produce(p) : feed.consume(p, 0);
+        const int32_t code = (rank == 0 && warp == 0) ? feed.produce_warp(p, lane) : feed.consume_warp(p, lane);
         if (code < 0) break;
         int prob, tm, tn0, nb;
         decode_tile(p, code, prob, tm, tn0, nb);
@@ -825,7 +861,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           int k0 = d.k_start * kBK;
           for (int kb = 0; kb < kbs; ++kb, k0 += kBK) {
             MST_PROF_WAIT(0, ptx::mbar_wait(empty_u32 + 8 * sidx, sphase ^ 1));
-            if (arm) {
+            if (arm && issuer) {
 #if MST_DIAG_NO_TMA
               ptx::mbar_arrive_local(full_u32 + 8 * sidx);
               (void)kblock_tx;
@@ -835,7 +871,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
 #if !MST_DIAG_NO_TMA
             const uint32_t fbar = full_leader + 8 * sidx;
-            if (do_a) {
+            if (do_a && issuer) {
               if (amode == 0) {
                 ptx::tma_load_2d_cg2(ma, sa, fbar, k0, arow, pa);
               } else if (amode == 1) {
@@ -845,7 +881,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 ptx::tma_load_2d_cg2(ma, sa + 8192, fbar, arow + 64, k0, pa);
               }
             }
-            if (do_b) {
+            if (do_b && issuer) {
 #pragma unroll
               for (int j = 0; j < kMaxNBlk; ++j) {
                 if (j < nb) {
@@ -874,11 +910,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
       }
-      MST_PROF_FLUSH(0, 1);
+      if (issuer) MST_PROF_FLUSH(0, 1);
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA) =====================
-    if (rank == 0 && lane == 0) {
+    if (rank == 0) {  // the whole warp walks the loop; lane 0 issues the MMAs and their commits
+      const bool issuer = lane == 0;
       const int nst = p.num_stages;
       const uint32_t slots_u32 = ptx::smem_u32(smem_slots);
       const uint32_t b_region = slots_u32 + nst * kSlotBytes;
@@ -892,7 +929,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       RingPos ap{0, 0};  // TMEM accumulator ring (acc_stages entries of acc_stride columns)
       MST_PROF_DECL
       for (;;) {
-        const int32_t code = feed.consume(p, 0);
+        const int32_t code = feed.consume_warp(p, lane);
         if (code < 0) break;
         int prob, tm, tn0, nb;
         decode_tile(p, code, prob, tm, tn0, nb);
@@ -925,7 +962,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t a4 = sa >> 4, b4 = sb >> 4;
 #pragma unroll
             for (int b = 0; b < kMaxNBlk; ++b) {
-              if (b < nb) {
+              if (b < nb && issuer) {
                 const uint32_t dt = b ? dt1 : dt0;
                 const uint32_t bb4 = b4 + b * (kSlotBytes >> 4);
 #pragma unroll
@@ -937,7 +974,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               }
             }
             accum0 = 1u;
-            ptx::umma_commit_cg2_mc(empty_u32 + 8 * sidx, 0x3);
+            if (issuer) ptx::umma_commit_cg2_mc(empty_u32 + 8 * sidx, 0x3);
             if (++sidx == nst) {
               sidx = 0;
               sphase ^= 1;
@@ -949,10 +986,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
           }
         }
-        ptx::umma_commit_cg2_mc(ptx::smem_u32(&tfull[acc0.idx]), 0x3);
-        if (nb > 1) ptx::umma_commit_cg2_mc(ptx::smem_u32(&tfull[acc1]), 0x3);
+        if (issuer) {
+          ptx::umma_commit_cg2_mc(ptx::smem_u32(&tfull[acc0.idx]), 0x3);
+          if (nb > 1) ptx::umma_commit_cg2_mc(ptx::smem_u32(&tfull[acc1]), 0x3);
+        }
+        __syncwarp();
       }
-      MST_PROF_FLUSH(2, 2);
+      if (issuer) MST_PROF_FLUSH(2, 2);
     }
   } else if (warp >= 4) {
     // ===================== epilogue =====================

@@ -24,7 +24,8 @@ st = torch.cuda.current_stream().cuda_stream
 buf = torch.zeros(64 * 8, dtype=torch.int64, device=dev)
 torch.manual_seed(0)
 for name, M, N, K, amn, bmn in [("square 8192", 8192, 8192, 8192, 0, 1), ("K3-like", 1024, 128256, 4096, 0, 1),
-                                 ("K6T-like", 4096, 128256, 1024, 0, 1)]:
+                                 ("K6T-like", 4096, 128256, 1024, 0, 1), ("l2res", 1024, 8192, 4096, 0, 1),
+                                 ("l2res-kmaj", 1024, 8192, 4096, 0, 0)]:
     if name not in SHAPES:
         continue
     A = torch.randn(M, K, device=dev).bfloat16()
