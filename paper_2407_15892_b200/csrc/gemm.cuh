@@ -824,17 +824,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const bool do_b = !MST_SPLIT_PRODUCER || warp == 3;
     {  // the whole warp walks the loop; lane 0 issues the barrier arrivals and TMA loads
       const bool issuer = lane == 0;
+      // Values produced by inline asm (policies, mapa) are opaque to ptxas's
+      // uniformity analysis: pass them through a warp reduction once so the
+      // TMA issue below takes uniform-register operands directly.
+      auto uni64 = [](uint64_t v) {
+        return (static_cast<uint64_t>(TileFeed::uniform(static_cast<int32_t>(v >> 32))) << 32) |
+               static_cast<uint32_t>(TileFeed::uniform(static_cast<int32_t>(v & 0xffffffffu)));
+      };
       uint64_t pols[3];
-      pols[0] = ptx::policy_evict_normal();
-      pols[1] = ptx::policy_evict_last();
-      pols[2] = ptx::policy_evict_first();
+      pols[0] = uni64(ptx::policy_evict_normal());
+      pols[1] = uni64(ptx::policy_evict_last());
+      pols[2] = uni64(ptx::policy_evict_first());
       const int nst = p.num_stages;
-      const uint32_t slots_u32 = ptx::smem_u32(smem_slots);
+      const uint32_t slots_u32 = static_cast<uint32_t>(TileFeed::uniform(static_cast<int32_t>(ptx::smem_u32(smem_slots))));
       const uint32_t b_region = slots_u32 + nst * kSlotBytes;
       const uint32_t b_stride = (p.stage_slots - 1) * kSlotBytes;
-      const uint32_t empty_u32 = ptx::smem_u32(empty);
-      const uint32_t full_u32 = ptx::smem_u32(full);
-      const uint32_t full_leader = ptx::mapa(full_u32, 0);
+      const uint32_t empty_u32 = static_cast<uint32_t>(TileFeed::uniform(static_cast<int32_t>(ptx::smem_u32(empty))));
+      const uint32_t full_u32 = static_cast<uint32_t>(TileFeed::uniform(static_cast<int32_t>(ptx::smem_u32(full))));
+      const uint32_t full_leader =
+          static_cast<uint32_t>(TileFeed::uniform(static_cast<int32_t>(ptx::mapa(full_u32, 0))));
       const bool arm = rank == 0 && do_a;
       int sidx = 0;
       uint32_t sphase = 0, sa = slots_u32, sb = b_region;
@@ -1003,7 +1011,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     epi::Stager st{smem_epi, lane, 0, q, false};
     MST_PROF_DECL
     for (;;) {
-      const int32_t code = feed.consume(p, lane);
+      const int32_t code = feed.consume_warp(p, lane);
       if (code < 0) break;
       int prob, tm, tn0, nb;
       decode_tile(p, code, prob, tm, tn0, nb);
