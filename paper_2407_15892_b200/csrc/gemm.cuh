@@ -1021,7 +1021,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         MST_PROF_WAIT(0, ptx::mbar_wait(ptx::smem_u32(&tfull[ap.idx]), ap.phase));
         ptx::tc_fence_after();
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + ap.idx * p.acc_stride;
+#ifndef MST_DIAG_NO_EPI
         MST_PROF_WAIT(1, run_epilogue(p, P, tn0 + b, row0, taddr, st));
+#else  // diagnostic builds: epilogue cost removed (results are garbage); =2 keeps all but the CE-forward one
+        if (MST_DIAG_NO_EPI == 2 && P.epi != kEpiCeFwdNum) MST_PROF_WAIT(1, run_epilogue(p, P, tn0 + b, row0, taddr, st));
+#endif
         // All TMEM reads of this N block are complete (tcgen05.wait::ld);
         // release the accumulator to the MMA warp of the pair leader.
         ptx::tc_fence_before();
