@@ -67,6 +67,7 @@ class ClockSampler:
 
     def __init__(self, device_index: int, interval: float = 0.02):
         self.samples: list[int] = []
+        self.power_w: list[float] = []
         self.reasons: set[str] = set()
         self.max_mhz = None
         self._stop = threading.Event()
@@ -87,6 +88,7 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.power_w.append(nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
                 mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for bit, name in self.REASONS.items():
                     if mask & bit and bit != 0x1:
@@ -108,7 +110,8 @@ class ClockSampler:
 
     def summary(self) -> dict:
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+                "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "power_w_median": statistics.median(self.power_w) if self.power_w else None}
 
 
 # --------------------------------------------------------------------------- helpers
