@@ -1,0 +1,30 @@
+"""Small end-to-end run of every device entry point, for compute-sanitizer
+(dev tool): python -m ... under `compute-sanitizer --tool memcheck`."""
+import sys, torch
+sys.path.insert(0, '.')
+from paper_2407_15892_b200 import miniseq as ms, model as mdl, optim
+
+torch.manual_seed(0)
+N, H, I, V = 300, 64, 136, 520
+X = torch.randn(N, H, device="cuda").bfloat16()
+W = [(0.05 * torch.randn(*s, device="cuda")).bfloat16() for s in ((H, I), (H, I), (I, H), (H, V))]
+L = torch.randint(0, V, (N,), device="cuda", dtype=torch.int32)
+L[::7] = -100
+mlp, head = ms.MlpWeights(*W[:3]), ms.LmHeadWeights(W[3])
+ctx = ms.Context.get(0)
+for chunked in (1, 0):
+    ctx.set_tuning("chunked_block", chunked)
+    st, gr = ms.block_step(X, L, mlp, head, 3, 3, check=True)
+ctx.set_tuning("chunked_block", 1)
+plan = ms.make_chunk_plan(N, 4)
+O, sv = ms.miniseq_mlp_forward(X, mlp, plan)
+loss, hs = ms.miniseq_lmhead_forward(O, L, head, plan)
+dO, _ = ms.miniseq_lmhead_backward(hs, head, plan)
+ms.miniseq_mlp_backward(dO, sv, mlp, plan)
+cfg = mdl.ModelConfig(d=64, I=224, V=512, heads=4, G=2, layers=1, S=128, B=1, M_mlp=2, M_head=4)
+m = mdl.Model(cfg)
+opt = optim.AdamW(m.w.named(), optim.OptimConfig())
+tok = torch.randint(0, 512, (1, 128), device="cuda", dtype=torch.int32)
+m.train_step(tok, tok, opt)
+torch.cuda.synchronize()
+print("sanitize smoke done", float(st[2]))
