@@ -367,3 +367,39 @@ def test_block_step_sp_global_valid_scaling(orc):
     _, half = ms.block_step(g["X"], g["L"], mlp, head, 4, 4, global_valid=2 * nv)
     for k, t in ref.items():
         assert torch.equal(getattr(half, k).float(), t.float() * 0.5), k
+
+
+def test_config2_full_size_properties():
+    """BASELINE config 2 at full size (Llama3-8B widths, S=8192): the bench's
+    M=8 chunk-wise block step against (a) the fp32 torch reference of the
+    same block and (b) itself at M=1 and M=2: dX and the loss are independent
+    of M (chunk boundaries are multiples of the 256-row tile), dW within fp32
+    reassociation; reruns are bitwise."""
+    import torch_ref as R
+
+    torch.manual_seed(5)
+    N, H, I, V = 8192, 4096, 14336, 128256
+    dev = "cuda"
+    X = torch.randn(N, H, device=dev).bfloat16()
+    Wg, Wu = [(0.02 * torch.randn(H, I, device=dev)).bfloat16() for _ in range(2)]
+    Wd = (0.02 * torch.randn(I, H, device=dev)).bfloat16()
+    Wo = (0.02 * torch.randn(H, V, device=dev)).bfloat16()
+    L = torch.randint(0, V, (N,), device=dev, dtype=torch.int32)
+    L[torch.rand(N, device=dev) < 0.05] = -100
+    mlp, head = ms.MlpWeights(Wg, Wu, Wd), ms.LmHeadWeights(Wo)
+    res = {}
+    for M in (8, 2, 1):
+        st, gr = ms.block_step(X, L, mlp, head, M, M)
+        res[M] = (float(st[2]), {k: getattr(gr, k).clone() for k in ("dX", "W_gate", "W_up", "W_down", "W_out")})
+    st, gr = ms.block_step(X, L, mlp, head, 8, 8)
+    for k, t in res[8][1].items():
+        assert torch.equal(getattr(gr, k), t), k  # bitwise rerun
+    for M in (2, 1):
+        assert abs(res[M][0] - res[8][0]) <= 1e-5 * res[8][0]
+        assert torch.equal(res[M][1]["dX"], res[8][1]["dX"])
+        for k in ("W_gate", "W_up", "W_down", "W_out"):
+            assert R.relerr(res[M][1][k], res[8][1][k].float()) <= 1e-5, (M, k)
+    ref = R.block(X, L, Wg, Wu, Wd, Wo)
+    assert abs(res[8][0] - float(ref["loss"])) <= 1e-3 * float(ref["loss"])
+    for k, rk in (("dX", "dX"), ("W_out", "dWout"), ("W_gate", "dWg"), ("W_up", "dWu"), ("W_down", "dWd")):
+        assert R.relerr(res[8][1][k], ref[rk]) <= 1e-2, k
