@@ -220,6 +220,15 @@ def run_reference(args) -> None:
           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
 
 
+def _tracked_peak(S: int, M: int) -> int:
+    """Peak live bytes of the [S/M, I] / [S/M, V] chunk buffers as libmst's
+    memtrack events report them (estimator.predict_block_peak, equal to the
+    tracked device events in tests/test_gpu_memtrack.py)."""
+    from paper_2407_15892_b200 import estimator
+
+    return estimator.predict_block_peak(S, H, I, V, M)["inter."]
+
+
 # --------------------------------------------------------------------------- GPU arm
 def main() -> None:
     ap = argparse.ArgumentParser()
@@ -427,7 +436,9 @@ def main() -> None:
                      "peak_burst": peaks["tflops"], "frac_of_burst": achieved / peaks["tflops"] if achieved else None},
         "gpu_launches": launches,
         "clocks": clk.summary(),
-        "memory": {"workspace_gb": ws.numel() / 1e9, "workspace_gb_at_M1": ws_m1 / 1e9,
+        "memory": {"tracked_peak_intermediate_gb": _tracked_peak(S, Mm) / 1e9,
+                   "tracked_peak_intermediate_gb_at_M1": _tracked_peak(S, 1) / 1e9,
+                   "workspace_gb": ws.numel() / 1e9, "workspace_gb_at_M1": ws_m1 / 1e9,
                    "peak_intermediate_gb": inter(Mm, Mh) / 1e9, "peak_intermediate_gb_at_M1": inter(1, 1) / 1e9,
                    "peak_activation_gb": (ws.numel() + S * H * 2 + stats.numel() * 4) / 1e9,
                    "peak_activation_gb_at_M1": (ws_m1 + S * H * 2 + stats.numel() * 4) / 1e9,

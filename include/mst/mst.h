@@ -120,20 +120,21 @@ MST_API int mst_ctx_take_timing_records(mst_ctx* ctx, int64_t cap, double* ms, d
  * disables.  No effect in product builds. */
 MST_API int mst_ctx_set_profile_buffer(mst_ctx* ctx, void* dev_counters);
 
-/* Tuning knobs (benchmark / A-B use; defaults are the tuned values):
- *   "sched":   0 plain LPT (default), 1 LPT + long tile last on alternate
- *              pairs, 2 long tile placed mid-list (static lists only);
+/* Tuning knobs (benchmark / A-B use; defaults are the tuned values; the
+ * measured effect of each is in DESIGN.md 4.2):
  *   "dynamic": 1 (default) CTA pairs pull tiles from the global LPT order
- *              through an atomic counter; 0 static per-pair lists;
- *   "ksplit5": split-K of the LM-Head dX GEMM (1, 2, 4; deterministic
- *              fixed-order fp32 combine);
- *   "ksplit9": 2 = MLP dX as two fp32 partial GEMMs + combine, 1 = fused;
- *   "tma3d":   MN-major operands as 3-D tensor maps (process-wide);
+ *              through an atomic counter; 0 static per-pair LPT lists;
+ *   "tma3d":   MN-major operands as 3-D tensor maps (process-wide, default 1);
  *   "fused_head": 1 (default) block_step runs mst_lmhead_fused, 0 runs the
  *              separate forward + backward (logits recomputed);
  *   "chunked_block": 1 (default) block_step with M_mlp == M_head runs the
  *              chunk-wise MLP -> head -> MLP-backward schedule (no G,U
- *              recompute; bitwise-equal results), 0 the op-by-op schedule.
+ *              recompute; bitwise-equal results), 0 the op-by-op schedule;
+ *   "fuse_swiglu_bwd": 1 = SwiGLU backward in the dh GEMM epilogue (default 0);
+ *   "wide", "wide_mask": wide tiles (two N blocks per CTA-pair tile) per GEMM
+ *              of the chunk-wise block (default off); "debug_nblk" for
+ *              mst_debug_gemm / mst_gemm;
+ *   "pairs":   run the GEMMs on fewer CTA pairs (diagnostics).
  * Unknown keys are MST_ERR_CONFIG.  Changing a knob clears the schedule cache. */
 MST_API int mst_ctx_set_tuning(mst_ctx* ctx, const char* key, int value);
 

@@ -45,9 +45,6 @@ namespace mst {
 #ifndef MST_SPLIT_PRODUCER
 #define MST_SPLIT_PRODUCER 1  // warp 0 issues A loads, warp 3 issues B loads (0: one producer)
 #endif
-#ifndef MST_DW_RED_GLOBAL
-#define MST_DW_RED_GLOBAL 0  // 1: fp32 dW accumulation with red.global.add.v4.f32 from registers
-#endif
 // Diagnostic builds only (tools/pipe_limits.py): MST_DIAG_NO_MMA skips the
 // tcgen05.mma issue (commits still arrive), MST_DIAG_NO_TMA replaces the
 // operand loads with plain barrier arrivals.  Results are garbage.
@@ -459,37 +456,6 @@ __device__ __forceinline__ void run_epilogue(const GemmParams& p, const ProblemD
     }
     case kEpiAccF32: {
       const int half = P.ph[0].umma_n >> 1;
-#if MST_DW_RED_GLOBAL
-      if (P.beta) {
-        // Accumulate straight from registers: 16-byte vector reductions in
-        // L2, no shared-memory staging (which competes with TMA / UMMA).
-        for (int g = 0; g < 2; ++g) {
-          float* out = static_cast<float*>(g ? P.out1 : P.out0);
-          const int64_t ld = g ? P.ld1 : P.ld0;
-          const int col0 = tn * P.tile_n + (g ? P.col_off1 : P.col_off0);
-          for (int c = 0; c < half; c += 32) {
-            float v[32];
-            epi::load32(taddr + g * half + c, v);
-            const int col = col0 + c;
-            if (row_ok) {
-              float* dst = out + static_cast<int64_t>(row) * ld + col;
-              if (col + 32 <= P.cols) {
-#pragma unroll
-                for (int q = 0; q < 8; ++q)
-                  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * q), "f"(v[4 * q]),
-                               "f"(v[4 * q + 1]), "f"(v[4 * q + 2]), "f"(v[4 * q + 3])
-                               : "memory");
-              } else {
-#pragma unroll
-                for (int j = 0; j < 32; ++j)
-                  if (col + j < P.cols) atomicAdd(dst + j, v[j]);
-              }
-            }
-          }
-        }
-        break;
-      }
-#endif
       for (int g = 0; g < 2; ++g) {
         const CUtensorMap* m = &p.maps[g ? P.map_out1 : P.map_out0];
         const int col0 = tn * P.tile_n + (g ? P.col_off1 : P.col_off0);

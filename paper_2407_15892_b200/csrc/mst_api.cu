@@ -115,16 +115,12 @@ struct mst_ctx {
   size_t ev_used = 0;
   unsigned long long* prof = nullptr;
   int64_t prof_slot = 0;
-  int sched_mode = 0;  // MST_SCHED: 0 plain LPT, 1 LPT + long tile last on alternate pairs, 2 long tile mid-list
-  int interleave_pct = 0;  // dynamic order: long tiles spread over the first pct% of the short ones (0: LPT)
   int dynamic = 1;     // MST_DYNAMIC: pairs pull tiles from the global LPT order (atomic counter)
-  int ksplit5 = 1;     // split-K of the LM-Head dX GEMM (K5): 1, 2 or 4
-  int ksplit9 = 1;     // MLP dX GEMM (K9): 1 = two-phase accumulate, 2 = one problem per phase + combine
   int fused_head = 1;  // block_step: single-pass LM-Head forward+backward (mst_lmhead_fused)
   int chunked_block = 1;  // block_step with M_mlp == M_head: chunk-wise MLP -> head -> MLP-backward schedule
   int wide = 1;           // allow wide tiles (two N blocks per scheduled tile) where a builder asks for them
   // Which GEMMs of the chunk-wise block use wide tiles (bit mask, tuning key
-  // "wide_mask"): 1 K3', 2 K5 (with ksplit5), 4 K2, 8 K9, 16 K7a, 32 K1.
+  // "wide_mask"): 1 K3', 2 K5, 4 K2, 8 K9, 16 K7a, 32 K1.
   int wide_mask = 0;
   int fuse_swiglu_bwd = 0;  // 1: chunk-wise block runs the SwiGLU backward in the dh GEMM epilogue (measured -0.7%: off)
   int debug_nblk = 1;     // N blocks per tile of mst_debug_gemm
@@ -390,28 +386,6 @@ int get_schedule(mst_ctx* c, const GemmParams& p, const int32_t** sched, const i
       per[top.second].push_back(t.code);
       heap.push({top.first + t.cost, top.second});
     }
-    // Mixing: LPT hands the long compute-bound tiles out first, which would
-    // leave every memory-heavy (dW reduce-add) tile for the end of the
-    // launch.  On every other pair that received a tile much longer than its
-    // median, run that long tile last so DRAM traffic spreads over the launch.
-    {
-      std::map<int32_t, double> cost_of;
-      for (const T& t : tiles) cost_of[t.code] = t.cost;
-      int flip = 0;
-      for (int q = 0; q < np && c->sched_mode != 0; ++q) {
-        std::vector<int32_t>& v = per[q];
-        if (v.size() < 3) continue;
-        const double first = cost_of[v.front()], last = cost_of[v.back()];
-        if (first <= 4.0 * last) continue;
-        if (c->sched_mode == 1) {
-          if (flip++ & 1) std::rotate(v.begin(), v.begin() + 1, v.end());
-        } else {
-          // place the long tile after ~(pair rank / pairs) of the short work
-          const size_t pos = 1 + (size_t)((v.size() - 1) * (double)(flip++ % 8) / 8.0);
-          std::rotate(v.begin(), v.begin() + 1, v.begin() + pos);
-        }
-      }
-    }
     std::vector<int32_t> host(np + 1 + 2 * tiles.size());
     int32_t acc = 0;
     for (int q = 0; q < np; ++q) {
@@ -422,25 +396,7 @@ int get_schedule(mst_ctx* c, const GemmParams& p, const int32_t** sched, const i
     size_t w = np + 1;
     for (int q = 0; q < np; ++q)
       for (int32_t code : per[q]) host[w++] = code;
-    if (c->interleave_pct > 0) {
-      // Dynamic order with the long (compute-bound, e.g. K5 dX) tiles spread
-      // evenly over the first interleave_pct% of the short (e.g. K6 dW
-      // reduce-add, DRAM-heavy) tiles instead of all first, so the short
-      // tiles' DRAM traffic overlaps the long tiles' math.
-      const double med = tiles[tiles.size() / 2].cost;
-      std::vector<int32_t> lng, sht;
-      for (const T& t : tiles) (t.cost > 4.0 * med ? lng : sht).push_back(t.code);
-      const size_t span = std::min(sht.size(), (size_t)(sht.size() * (c->interleave_pct / 100.0)));
-      size_t si = 0;
-      for (size_t li = 0; li < lng.size(); ++li) {
-        host[w++] = lng[li];
-        const size_t upto = lng.empty() ? 0 : span * (li + 1) / lng.size();
-        while (si < upto) host[w++] = sht[si++];
-      }
-      while (si < sht.size()) host[w++] = sht[si++];
-    } else {
-      for (const T& t : tiles) host[w++] = t.code;  // global LPT order (dynamic mode)
-    }
+    for (const T& t : tiles) host[w++] = t.code;  // global LPT order (dynamic mode)
     SchedEntry e;
     e.num_pairs = np;
     e.total = (int32_t)tiles.size();
@@ -866,88 +822,13 @@ int build_plain(mst_ctx* c, Launch& L, const Operand& a, const Operand& b, void*
   return MST_OK;
 }
 
-// Split-K: `splits` problems, slice s covers K blocks [s*kps, (s+1)*kps) and
-// stores fp32 partials into part + s*rows*ldp; splitk_combine sums them in
-// slice order (deterministic) into the bf16 output.  Used for the long-K,
-// few-tile dX GEMMs (K5: K = V, K9: K = 2I) so they interleave with the
-// short-K dW tiles of the same launch instead of dominating its tail.
-int build_plain_splitk(mst_ctx* c, Launch& L, const Operand& a, const Operand& b, float* part, int64_t ldp,
-                       int splits, int nblk = 1) {
-  const int kb = (int)cdiv(a.k, mst::kBK);
-  const int kps = (int)cdiv(kb, splits);
-  cnt_mm(c, a.mn, a.k, b.mn,
-         (is_weight(c, a.base) ? (uint64_t)(a.mn * a.k) : 0) + (is_weight(c, b.base) ? (uint64_t)(b.mn * b.k) : 0));
-  for (int s = 0; s < splits; ++s) {
-    const int k0 = s * kps;
-    if (k0 >= kb) break;
-    ProblemDesc& P = L.p.prob[L.p.num_problems++];
-    P.nblk = nblk;
-    PhaseSpec ps{};
-    ps.a = a;
-    ps.b0 = b;
-    ps.b1 = b;
-    ps.umma_n = 256;
-    ps.b_off1 = 128;
-    ps.k_start = k0;
-    ps.k_blocks = std::min(kps, kb - k0);
-    MST_TRY(add_phase(c, L, P, ps));
-    P.m_tiles = (int)cdiv(a.mn, 256);
-    P.tile_n = 256;
-    P.n_tiles = (int)cdiv(b.mn, 256);
-    P.rows = (int)a.mn;
-    P.cols = (int)b.mn;
-    P.epi = mst::kEpiAccF32;
-    P.beta = 0;
-    MST_TRY(add_out_map(c, L, part + (int64_t)s * a.mn * ldp, b.mn, a.mn, ldp, true, &P.map_out0));
-    P.map_out1 = P.map_out0;
-    P.col_off0 = 0;
-    P.col_off1 = 128;
-    L.flops += 2.0 * a.mn * b.mn * std::min<int64_t>(a.k - (int64_t)k0 * mst::kBK, (int64_t)kps * mst::kBK);
-  }
-  return MST_OK;
-}
-
-__global__ void splitk_combine_kernel(const float* __restrict__ part, int splits, int64_t split_stride, int rows,
-                                      int cols, int64_t ldp, uint16_t* __restrict__ out, int64_t ld_out) {
-  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
-  const int64_t r = i / cols, col = i % cols;
-  if (r >= rows) return;
-  const float* p = part + r * ldp + col;
-  float4 acc = *reinterpret_cast<const float4*>(p);
-  for (int s = 1; s < splits; ++s) {
-    const float4 v = *reinterpret_cast<const float4*>(p + s * split_stride);
-    acc.x += v.x;
-    acc.y += v.y;
-    acc.z += v.z;
-    acc.w += v.w;
-  }
-  uint2 w;
-  w.x = ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(acc.y)) << 16) | __bfloat16_as_ushort(__float2bfloat16_rn(acc.x));
-  w.y = ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(acc.w)) << 16) | __bfloat16_as_ushort(__float2bfloat16_rn(acc.z));
-  *reinterpret_cast<uint2*>(out + r * ld_out + col) = w;
-}
-
-int splitk_combine(mst_ctx* c, cudaStream_t st, const float* part, int splits, int64_t rows, int64_t cols, void* out,
-                   int64_t ld_out) {
-  const int64_t n4 = rows * cols / 4;  // cols % 8 == 0
-  splitk_combine_kernel<<<(unsigned)cdiv(n4, 256), 256, 0, st>>>(part, splits, rows * cols, (int)rows, (int)cols,
-                                                                  cols, static_cast<uint16_t*>(out), ld_out);
-  c->launches++;
-  MST_CUDA(cudaGetLastError());
-  return MST_OK;
-}
-
 // K9 (dX_j = dG W_g^T + dU W_u^T), K8 (dW_d += h^T dO_j) and K10
 // ([dW_g | dW_u] += X_j^T [dG | dU]) of one chunk: mutually independent,
 // added to one grouped launch (Alg. 3 lines 5-7).
 int add_mlp_grads(mst_ctx* c, Launch& L, const void* dg, const void* du, const void* ht, const void* xt,
                   const void* doj, const void* wg, const void* wu, void* dxj, float* dwg, float* dwu, float* dwd,
-                  int64_t rows, int64_t h, int64_t i, int64_t ldt, int beta, float* part9) {
-  if (c->ksplit9 > 1) {  // K9 as two fp32 partial GEMMs (dG W_g^T, dU W_u^T) + combine
-    MST_TRY(build_plain_splitk(c, L, Operand{dg, rows, i, i, false}, Operand{wg, h, i, i, false}, part9, h, 1));
-    MST_TRY(build_plain_splitk(c, L, Operand{du, rows, i, i, false}, Operand{wu, h, i, i, false}, part9 + rows * h,
-                               h, 1));
-  } else {  // K9: one accumulator over both phases (B K-major)
+                  int64_t rows, int64_t h, int64_t i, int64_t ldt, int beta) {
+  {  // K9: one accumulator over both phases (B K-major)
     ProblemDesc& P = L.p.prob[L.p.num_problems++];
     P.nblk = (c->wide_mask & 8) ? 2 : 1;
     PhaseSpec q0{};
@@ -1040,7 +921,6 @@ int mst_ctx_create(int device, mst_ctx** out) {
     return fail(MST_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   }
   c->encode = reinterpret_cast<EncodeTiledFn>(fn);
-  if (const char* sm = getenv("MST_SCHED")) c->sched_mode = atoi(sm);
   if (const char* dy = getenv("MST_DYNAMIC")) c->dynamic = atoi(dy) != 0;
   e = cudaFuncSetAttribute(mst::mst_grouped_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            mst::kSmemBytes);
@@ -1138,24 +1018,12 @@ int mst_ctx_set_profile_buffer(mst_ctx* c, void* dev_counters) {
 
 int mst_ctx_set_tuning(mst_ctx* c, const char* key, int value) {
   if (!c || !key) return fail(MST_ERR_STATE, "NULL context or key");
-  if (std::strcmp(key, "sched") == 0) {
-    if (value < 0 || value > 2) return fail(MST_ERR_CONFIG, "sched must be 0..2");
-    c->sched_mode = value;
-  } else if (std::strcmp(key, "dynamic") == 0) {
+  if (std::strcmp(key, "dynamic") == 0) {
     c->dynamic = value != 0;
-  } else if (std::strcmp(key, "ksplit5") == 0) {
-    if (value != 1 && value != 2 && value != 4) return fail(MST_ERR_CONFIG, "ksplit5 must be 1, 2 or 4");
-    c->ksplit5 = value;
-  } else if (std::strcmp(key, "ksplit9") == 0) {
-    if (value != 1 && value != 2) return fail(MST_ERR_CONFIG, "ksplit9 must be 1 or 2");
-    c->ksplit9 = value;
   } else if (std::strcmp(key, "fused_head") == 0) {
     c->fused_head = value != 0;
   } else if (std::strcmp(key, "chunked_block") == 0) {
     c->chunked_block = value != 0;
-  } else if (std::strcmp(key, "interleave") == 0) {
-    if (value < 0 || value > 100) return fail(MST_ERR_CONFIG, "interleave must be 0..100");
-    c->interleave_pct = value;
   } else if (std::strcmp(key, "wide") == 0) {
     c->wide = value != 0;
   } else if (std::strcmp(key, "fuse_swiglu_bwd") == 0) {
@@ -1274,7 +1142,7 @@ int mst_make_chunk_plan(int64_t n, int64_t m, int64_t* bounds, int64_t* num_chun
 static int64_t ld_t(int64_t n, int64_t m) { return (max_chunk(n, m) + 7) / 8 * 8; }
 
 static int carve_mlp(Carve& cv, int64_t n, int64_t h, int64_t i, int64_t m, void** hbuf, void** dg, void** du,
-                     float** dh = nullptr, void** xt = nullptr, void** ht = nullptr, float** part9 = nullptr) {
+                     float** dh = nullptr, void** xt = nullptr, void** ht = nullptr) {
   const int64_t nc = max_chunk(n, m);
   const size_t hb = size_t(nc) * i * 2;
   // forward uses two h buffers (ping-pong across chunks); backward h, dG,
@@ -1289,13 +1157,11 @@ static int carve_mlp(Carve& cv, int64_t n, int64_t h, int64_t i, int64_t m, void
   void* t = cv.take(size_t(i) * ld_t(n, m) * 2);
   if (xt) *xt = x;
   if (ht) *ht = t;
-  float* p9 = static_cast<float*>(cv.take(size_t(2) * nc * h * 4));  // K9 split partials
-  if (part9) *part9 = p9;
   return MST_OK;
 }
 
 static void carve_head(Carve& cv, int64_t n, int64_t h, int64_t v, int64_t m, float2** part, float** zt,
-                       float** lrow, void** dl, float** scales, void** ot = nullptr, float** part5 = nullptr) {
+                       float** lrow, void** dl, float** scales, void** ot = nullptr) {
   const int64_t nc = max_chunk(n, m);
   const int64_t nparts = cdiv(v, 256);
   *part = static_cast<float2*>(cv.take(size_t(nc) * nparts * sizeof(float2)));
@@ -1305,8 +1171,6 @@ static void carve_head(Carve& cv, int64_t n, int64_t h, int64_t v, int64_t m, fl
   *scales = static_cast<float*>(cv.take(size_t(std::min(n, m)) * 4 + 64));
   void* o = cv.take(size_t(h) * ld_t(n, m) * 2);  // X_j^T: K-major A operand of K6
   if (ot) *ot = o;
-  float* p5 = static_cast<float*>(cv.take(size_t(4) * nc * h * 4));  // K5 split-K partials
-  if (part5) *part5 = p5;
 }
 
 int mst_mlp_workspace(int64_t n, int64_t h, int64_t i, int64_t m, size_t* bytes) {
@@ -1420,8 +1284,7 @@ int mst_mlp_backward(mst_ctx* c, void* stream, const void* dout, const mst_mlp_s
   Carve cv{static_cast<char*>(ws), ws_bytes, 0, false};
   void *hb, *dg, *du, *xt, *ht;
   float* dhb;
-  float* part9;
-  carve_mlp(cv, n, h, i, m, &hb, &dg, &du, &dhb, &xt, &ht, &part9);
+  carve_mlp(cv, n, h, i, m, &hb, &dg, &du, &dhb, &xt, &ht);
   const int64_t ldt = ld_t(n, m);
   const std::vector<int64_t> b = plan_bounds(n, m);
   const int nch = (int)b.size() - 1;
@@ -1482,10 +1345,9 @@ int mst_mlp_backward(mst_ctx* c, void* stream, const void* dout, const mst_mlp_s
     {  // K9 + K8 + K10 (mutually independent) + K7a of the next chunk, one launch.
       Launch L;
       MST_TRY(add_mlp_grads(c, L, dg, du, ht, xt, doj, wg, wu, const_cast<char*>(bptr(dx, r0 * h)), dwg, dwu, dwd,
-                            rows, h, i, ldt, beta, part9));
+                            rows, h, i, ldt, beta));
       if (j + 1 < nch) MST_TRY(add_k7a(L, j + 1));
       MST_TRY(launch(c, st, L));
-      if (c->ksplit9 > 1) MST_TRY(splitk_combine(c, st, part9, 2, rows, h, const_cast<char*>(bptr(dx, r0 * h)), h));
     }
     mem_free(c, (uint64_t)rows * h * 2, "act.xT");
     mem_free(c, (uint64_t)rows * i * 2, "inter.mlp.hT");
@@ -1577,8 +1439,7 @@ int mst_lmhead_backward(mst_ctx* c, void* stream, const mst_lmhead_saved* s, con
   float2* part;
   float *zt, *lrow, *scales;
   void *dl, *ot;
-  float* part5;
-  carve_head(cv, n, h, v, m, &part, &zt, &lrow, &dl, &scales, &ot, &part5);
+  carve_head(cv, n, h, v, m, &part, &zt, &lrow, &dl, &scales, &ot);
   const int64_t ldt = ld_t(n, m);
   const std::vector<int64_t> b = plan_bounds(n, m);
   const int nch = (int)b.size() - 1;
@@ -1604,18 +1465,13 @@ int mst_lmhead_backward(mst_ctx* c, void* stream, const mst_lmhead_saved* s, con
       P.scale = scales + j;
       MST_TRY(launch(c, st, L));
     }
-    {  // K5 (dX = dl W_out^T, optionally split-K) + K6 (dW_out += X^T dl), grouped.
+    {  // K5 (dX = dl W_out^T) + K6 (dW_out += X^T dl), grouped.
       Launch L;
-      const Operand a5{dl, rows, v, v, false}, b5{wout, h, v, v, false};
-      if (c->ksplit5 > 1)
-        MST_TRY(build_plain_splitk(c, L, a5, b5, part5, h, c->ksplit5));
-      else
-        MST_TRY(build_plain(c, L, a5, b5, const_cast<char*>(bptr(dx, r0 * h)), h, mst::kEpiStoreBf16, 0));
+      MST_TRY(build_plain(c, L, Operand{dl, rows, v, v, false}, Operand{wout, h, v, v, false},
+                          const_cast<char*>(bptr(dx, r0 * h)), h, mst::kEpiStoreBf16, 0));
       MST_TRY(build_plain(c, L, Operand{ot, h, rows, ldt, false}, Operand{dl, v, rows, v, true}, dwout, v,
                           mst::kEpiAccF32, beta));
       MST_TRY(launch(c, st, L));
-      if (c->ksplit5 > 1)
-        MST_TRY(splitk_combine(c, st, part5, c->ksplit5, rows, h, const_cast<char*>(bptr(dx, r0 * h)), h));
     }
     mem_free(c, (uint64_t)rows * v * 2, "inter.head.dlogits");
     mem_free(c, (uint64_t)rows * h * 2, "act.xT");
@@ -1640,8 +1496,7 @@ int mst_lmhead_fused(mst_ctx* c, void* stream, const void* x, const int32_t* lab
   float2* part;
   float *zt, *lrow, *scales;
   void *dl, *ot;
-  float* part5;
-  carve_head(cv, n, h, v, m, &part, &zt, &lrow, &dl, &scales, &ot, &part5);
+  carve_head(cv, n, h, v, m, &part, &zt, &lrow, &dl, &scales, &ot);
   const int64_t ldt = ld_t(n, m);
   const std::vector<int64_t> b = plan_bounds(n, m);
   const int nch = (int)b.size() - 1;
@@ -1797,10 +1652,10 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
   float* lse = reinterpret_cast<float*>(base + 2 * ob);
   Carve cv{base + block_fixed_bytes(n, h) + 256, ws_bytes, 0, false};
   void *hb, *dg, *du, *xt, *ht, *dl, *ot;
-  float *dhb, *part9, *zt, *lrow, *scales, *part5;
+  float *dhb, *zt, *lrow, *scales;
   float2* part;
-  carve_mlp(cv, n, h, i, m, &hb, &dg, &du, &dhb, &xt, &ht, &part9);
-  carve_head(cv, n, h, v, m, &part, &zt, &lrow, &dl, &scales, &ot, &part5);
+  carve_mlp(cv, n, h, i, m, &hb, &dg, &du, &dhb, &xt, &ht);
+  carve_head(cv, n, h, v, m, &part, &zt, &lrow, &dl, &scales, &ot);
   float* g32 = static_cast<float*>(cv.take(size_t(max_chunk(n, m)) * i * 4));
   float* u32 = static_cast<float*>(cv.take(size_t(max_chunk(n, m)) * i * 4));
   const int64_t ldt = ld_t(n, m);
@@ -1873,7 +1728,7 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
       for (int wi = 0; wi < 3; ++wi) grad_alloc(c, wi, (uint64_t)h * i * 4);
     const int beta = (j > 0 || accumulate) ? 1 : 0;
     return add_mlp_grads(c, L, dg, du, ht, xt, bptr(dO, b[j] * h), wg, wu, const_cast<char*>(bptr(dx, b[j] * h)),
-                         dwg, dwu, dwd, rows, h, i, ldt, beta, part9);
+                         dwg, dwu, dwd, rows, h, i, ldt, beta);
   };
   {
     Launch L;
@@ -1891,8 +1746,6 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
                           0, (c->wide_mask & 4) ? 2 : 1));
       if (j > 0) MST_TRY(add_grads(L, j - 1));
       MST_TRY(launch(c, st, L));
-      if (j > 0 && c->ksplit9 > 1)
-        MST_TRY(splitk_combine(c, st, part9, 2, rows_of(j - 1), h, const_cast<char*>(bptr(dx, b[j - 1] * h)), h));
       if (j > 0) grads_live(j - 1, false);
     }
     const uint64_t part_bytes = (uint64_t)rows * nparts * 8 + (uint64_t)rows * 8;
@@ -1922,16 +1775,11 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
     c->launches += 3;
     {  // K5 + K6
       Launch L;
-      const Operand a5{dl, rows, v, v, false}, b5{wout, h, v, v, false};
-      const int nb5 = (c->wide_mask & 2) ? 2 : 1;
-      if (c->ksplit5 > 1)
-        MST_TRY(build_plain_splitk(c, L, a5, b5, part5, h, c->ksplit5, nb5));
-      else
-        MST_TRY(build_plain(c, L, a5, b5, doj, h, mst::kEpiStoreBf16, 0, nb5));
+      MST_TRY(build_plain(c, L, Operand{dl, rows, v, v, false}, Operand{wout, h, v, v, false}, doj, h,
+                          mst::kEpiStoreBf16, 0, (c->wide_mask & 2) ? 2 : 1));
       MST_TRY(build_plain(c, L, Operand{ot, h, rows, ldt, false}, Operand{dl, v, rows, v, true}, dwout, v,
                           mst::kEpiAccF32, beta));
       MST_TRY(launch(c, st, L));
-      if (c->ksplit5 > 1) MST_TRY(splitk_combine(c, st, part5, c->ksplit5, rows, h, doj, h));
     }
     if (j == nch - 1) grad_ready(c, 3, st, (uint64_t)h * v * 4);  // dW_out complete
     mem_free(c, (uint64_t)rows * v * 2, "inter.head.dlogits");
@@ -1985,8 +1833,6 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
     Launch L;
     MST_TRY(add_grads(L, nch - 1));
     MST_TRY(launch(c, st, L));
-    if (c->ksplit9 > 1)
-      MST_TRY(splitk_combine(c, st, part9, 2, rows_of(nch - 1), h, const_cast<char*>(bptr(dx, b[nch - 1] * h)), h));
     grads_live(nch - 1, false);
   }
   for (int wi = 0; wi < 3; ++wi) grad_ready(c, wi, st, (uint64_t)h * i * 4);  // dW_gate, dW_up, dW_down complete
