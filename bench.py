@@ -83,12 +83,25 @@ class ClockSampler:
             self.nv = None
         self.interval = interval
 
+    def _power(self) -> float:
+        """Instantaneous board power (W).  nvmlDeviceGetPowerUsage is a ~1 s
+        trailing average on this driver: over a sub-second timed region it
+        mixes in the idle time before it."""
+        nv = self.nv
+        try:
+            fv = nv.nvmlDeviceGetFieldValues(self.h, [nv.NVML_FI_DEV_POWER_INSTANT])[0]
+            if fv.nvmlReturn == 0:
+                return fv.value.uiVal / 1000.0
+        except Exception:
+            pass
+        return nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0
+
     def _run(self):
         nv = self.nv
         while not self._stop.is_set():
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
-                self.power_w.append(nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
+                self.power_w.append(self._power())
                 mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for bit, name in self.REASONS.items():
                     if mask & bit and bit != 0x1:
