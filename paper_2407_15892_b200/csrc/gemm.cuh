@@ -26,7 +26,8 @@
 // epilogue thread ever waits on a global store.
 //
 // Warp roles (256 threads): w0 TMA producer for A, w3 TMA producer for B,
-// w1 MMA issuer (leader CTA only), w2 TMEM allocator, w4..w7 epilogue (warp w owns TMEM lanes
+// w1 MMA issuer (leader CTA only), w2 TMEM allocator + tile scheduler (leader CTA,
+// dynamic mode), w4..w7 epilogue (warp w owns TMEM lanes
 // 32*(w%4) .. +31, i.e. 32 output rows, and all accumulator columns).
 #pragma once
 
@@ -152,15 +153,29 @@ struct GemmParams {
   int32_t* tile_counter;
 };
 
-constexpr int kTileSlots = 4;          // tile-code ring between the pair leader's producer and all roles
-// leader MMA + 4 leader epi warps + peer producer + 4 peer epi warps (+ both B producers)
-constexpr int kTileConsumers = 10 + 2 * MST_SPLIT_PRODUCER;
+#ifndef MST_TEMPTY_RELAXED
+#define MST_TEMPTY_RELAXED 1
+#endif
+#ifndef MST_FEED_RELAXED
+#define MST_FEED_RELAXED 1
+#endif
+#ifndef MST_TILE_SLOTS
+#define MST_TILE_SLOTS 8
+#endif
+constexpr int kTileSlots = MST_TILE_SLOTS;  // tile-code ring between the scheduler and all roles
+// both A producers, leader MMA, 4 + 4 epilogue warps (+ both B producers)
+constexpr int kTileConsumers = 11 + 2 * MST_SPLIT_PRODUCER;
 
 // Per-role iterator over this pair's tiles.  Static mode walks the host LPT
-// list; dynamic mode: the leader's producer claims the next tile of the
-// global LPT order with an atomic and publishes its code into a 4-slot ring
-// in both CTAs (st.shared::cluster + release.cluster arrive); every other
-// role reads the ring and releases the slot back to the leader.
+// list.  Dynamic mode: a scheduler (lane 0 of the leader's otherwise idle
+// warp 2) claims the next tile of the global order with an atomic and
+// publishes its code into a kTileSlots ring in both CTAs (st.shared::cluster
+// + release.cluster arrive), up to kTileSlots tiles ahead of the slowest role;
+// every other role reads the ring and releases the slot back to the leader.
+// A claim costs two dependent global round trips (atomicAdd on the counter,
+// then the order list); off the producer's issue path they no longer stall
+// the first K block of every tile (measured: 770 -> 650 cycles per K block on
+// K = 1024 tiles, where the producer used to claim).
 struct TileFeed {
   const int32_t* list;
   int n, it;
@@ -170,11 +185,26 @@ struct TileFeed {
   int slot;
   uint32_t phase;
 
-  // Leader producer (dynamic) / any role (static).  tile_counter[0] is the
-  // claim counter, [1] counts pairs that are done claiming; the last such
-  // pair re-zeroes both for the next launch on the stream (no memset).
-  __device__ __forceinline__ int32_t produce(const GemmParams& p) {
-    if (!p.dynamic) return it < n ? list[it++] : -1;
+  // Consumer (warp-wide: all lanes wait, lane 0 releases the slot).  The
+  // code is reduced across the warp before the release, so the slot is handed
+  // back only after its value has been consumed; a relaxed arrive then
+  // suffices (a release arrive costs an ERRBAR + MEMBAR per tile and role).
+  __device__ __forceinline__ int32_t consume(const GemmParams& p, int lane) {
+    if (!p.dynamic) return uniform(it < n ? list[it++] : -1);
+    ptx::mbar_wait_cluster(ptx::smem_u32(&full[slot]), phase);
+    const int32_t code = uniform(*reinterpret_cast<volatile int32_t*>(&codes[slot]));
+#if MST_FEED_RELAXED
+    if (lane == 0) ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&empty[slot]), 0));
+#else
+    if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&empty[slot]), 0));
+#endif
+    advance();
+    return code;
+  }
+  // Scheduler (one thread).  tile_counter[0] is the claim counter, [1] counts
+  // pairs that are done claiming; the last such pair re-zeroes both for the
+  // next launch on the stream (no memset).
+  __device__ __forceinline__ int32_t claim_publish(const GemmParams& p) {
     ptx::mbar_wait(ptx::smem_u32(&empty[slot]), phase ^ 1);
     const int32_t t = atomicAdd(p.tile_counter, 1);
     const int32_t code = t < p.total_tiles ? __ldg(p.order + t) : -1;
@@ -189,47 +219,10 @@ struct TileFeed {
     advance();
     return code;
   }
-  // Every other role.  `lane0_arrives`: warp-wide consumer (all lanes call,
-  // lane 0 releases the slot); single-thread roles pass true.
-  __device__ __forceinline__ int32_t consume(const GemmParams& p, int lane) {
-    if (!p.dynamic) return it < n ? list[it++] : -1;
-    ptx::mbar_wait_cluster(ptx::smem_u32(&full[slot]), phase);
-    const int32_t code = *reinterpret_cast<volatile int32_t*>(&codes[slot]);
-    __syncwarp(__activemask());
-    if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&empty[slot]), 0));
-    advance();
-    return code;
-  }
-  // Warp-wide variants (all 32 lanes call; lane 0 performs the single-thread
-  // actions): the returned code is broadcast from lane 0 so everything the
-  // role derives from it stays warp-uniform (uniform-datapath registers, no
+  // The code is broadcast through a warp reduction so everything the role
+  // derives from it stays warp-uniform (uniform-datapath registers, no
   // per-instruction ELECT/R2UR loops around the TMA and MMA issues).
-  __device__ __forceinline__ int32_t produce_warp(const GemmParams& p, int lane) {
-    int32_t code = -1;
-    if (!p.dynamic) {
-      code = it < n ? list[it] : -1;
-      ++it;
-    } else {
-      ptx::mbar_wait(ptx::smem_u32(&empty[slot]), phase ^ 1);
-      if (lane == 0) {
-        const int32_t t = atomicAdd(p.tile_counter, 1);
-        code = t < p.total_tiles ? __ldg(p.order + t) : -1;
-        if (code < 0 && atomicAdd(p.tile_counter + 1, 1) == static_cast<int32_t>(gridDim.x / 2) - 1) {
-          atomicExch(p.tile_counter, 0);
-          atomicExch(p.tile_counter + 1, 0);
-        }
-        codes[slot] = code;
-        ptx::st_shared_cluster_u32(ptx::mapa(ptx::smem_u32(&codes[slot]), 1), static_cast<uint32_t>(code));
-        ptx::mbar_arrive_local(ptx::smem_u32(&full[slot]));
-        ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&full[slot]), 1));
-      }
-      advance();
-    }
-    return uniform(__shfl_sync(0xffffffffu, code, 0));
-  }
-  __device__ __forceinline__ int32_t consume_warp(const GemmParams& p, int lane) {
-    return uniform(consume(p, lane));
-  }
+  __device__ __forceinline__ int32_t consume_warp(const GemmParams& p, int lane) { return consume(p, lane); }
   // A warp-wide reduction of identical values: REDUX writes a uniform
   // register, so ptxas treats everything derived from it as warp-uniform.
   __device__ __forceinline__ static int32_t uniform(int32_t v) {
@@ -814,7 +807,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t sphase = 0, sa = slots_u32, sb = b_region;
       MST_PROF_DECL
       for (;;) {
-        const int32_t code = (rank == 0 && warp == 0) ? feed.produce_warp(p, lane) : feed.consume_warp(p, lane);
+        const int32_t code = feed.consume_warp(p, lane);
         if (code < 0) break;
         int prob, tm, tn0, nb;
         decode_tile(p, code, prob, tm, tn0, nb);
@@ -884,6 +877,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
       }
+#if defined(MST_PROFILE) && MST_PROFILE == 2
+      if (false)
+#endif
       if (issuer) MST_PROF_FLUSH(0, 1);
     }
   } else if (warp == 1) {
@@ -903,7 +899,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       RingPos ap{0, 0};  // TMEM accumulator ring (acc_stages entries of acc_stride columns)
       MST_PROF_DECL
       for (;;) {
+#if defined(MST_PROFILE) && MST_PROFILE == 2  // diagnostic: MMA tile-feed waits, reported in slot 1
+        int32_t code;
+        MST_PROF_WAIT(2, code = feed.consume_warp(p, lane));
+#else
         const int32_t code = feed.consume_warp(p, lane);
+#endif
         if (code < 0) break;
         int prob, tm, tn0, nb;
         decode_tile(p, code, prob, tm, tn0, nb);
@@ -967,6 +968,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         __syncwarp();
       }
       if (issuer) MST_PROF_FLUSH(2, 2);
+#if defined(MST_PROFILE) && MST_PROFILE == 2
+      if (issuer && p.prof) atomicAdd(p.prof + 1, prof_acc[2]);
+#endif
+    }
+  } else if (warp == 2) {
+    // ===================== tile scheduler (dynamic mode, leader CTA) =====================
+    if (p.dynamic && rank == 0) {
+      if (lane == 0)
+        while (feed.claim_publish(p) >= 0) {
+        }
+      __syncwarp();
     }
   } else if (warp >= 4) {
     // ===================== epilogue =====================
@@ -996,7 +1008,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // release the accumulator to the MMA warp of the pair leader.
         ptx::tc_fence_before();
         __syncwarp();
+        // tcgen05.wait::ld has returned, so the accumulator is already read:
+        // a relaxed arrive avoids the MEMBAR.ALL.GPU + ERRBAR a release.cluster
+        // arrive compiles to (the fence::before_thread_sync above orders the
+        // tcgen05 reads before it).
+#if MST_TEMPTY_RELAXED
+        if (lane == 0) ptx::mbar_arrive_cluster_relaxed(ap.idx ? tempty_leader1 : tempty_leader0);
+#else
         if (lane == 0) ptx::mbar_arrive_cluster(ap.idx ? tempty_leader1 : tempty_leader0);
+#endif
         ap.next(p.acc_stages);
       }
     }

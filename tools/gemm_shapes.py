@@ -20,6 +20,11 @@ SHAPES = [  # name, M, N, K, a_mn, b_mn, out_f32, beta
     ("K6 K=2048 f32 reduce", 4096, 128256, 2048, 0, 1, 1, 1),
     ("K6 K=4096 f32 reduce", 4096, 128256, 4096, 0, 1, 1, 1),
     ("K8 14336x4096x1024 f32 reduce", 14336, 4096, 1024, 0, 1, 1, 1),
+    ("T K=512 bf16", 4096, 128256, 512, 0, 1, 0, 0),
+    ("T K=2048 bf16", 4096, 128256, 2048, 0, 1, 0, 0),
+    ("T K=4096 bf16", 4096, 65536, 4096, 0, 1, 0, 0),
+    ("T K=1024 bf16 B K-major", 4096, 128256, 1024, 0, 0, 0, 0),
+    ("T K=1024 bf16 A MN-major", 4096, 128256, 1024, 1, 1, 0, 0),
 ]
 only = sys.argv[1:]
 for name, M, N, K, amn, bmn, f32, beta in SHAPES:
