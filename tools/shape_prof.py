@@ -1,9 +1,10 @@
 """Role wait shares of the engine on one GEMM shape (MST_PROFILE build; dev tool).
-usage: MST_LIB=.../libmst_prof.so [MST_TUNE=k=v] python tools/shape_prof.py M N K a_mn b_mn"""
+usage: MST_LIB=.../libmst_prof.so [MST_TUNE=k=v] python tools/shape_prof.py M N K a_mn b_mn [out_f32 beta]"""
 import os, sys, torch
 sys.path.insert(0, '.')
 from paper_2407_15892_b200 import miniseq as ms
 M, N, K, amn, bmn = map(int, sys.argv[1:6])
+f32, beta = (map(int, sys.argv[6:8]) if len(sys.argv) > 7 else (0, 0))
 ctx = ms.Context.get(0)
 for kv in filter(None, os.environ.get('MST_TUNE', '').split(',')):
     k, v = kv.split('=')
@@ -11,9 +12,9 @@ for kv in filter(None, os.environ.get('MST_TUNE', '').split(',')):
 st = torch.cuda.current_stream().cuda_stream
 A = torch.randn(K, M, device='cuda').bfloat16() if amn else torch.randn(M, K, device='cuda').bfloat16()
 B = torch.randn(K, N, device='cuda').bfloat16() if bmn else torch.randn(N, K, device='cuda').bfloat16()
-C = torch.zeros(M, N, device='cuda', dtype=torch.bfloat16)
+C = torch.zeros(M, N, device='cuda', dtype=torch.float32 if f32 else torch.bfloat16)
 f = lambda: ms._check(ctx.lib.mst_debug_gemm(ctx.handle, st, A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K,
-                                             amn, bmn, 0, 0))
+                                             amn, bmn, f32, beta))
 for _ in range(20): f()
 torch.cuda.synchronize()
 buf = torch.zeros(64 * 8, dtype=torch.int64, device='cuda')
