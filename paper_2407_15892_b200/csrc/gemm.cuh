@@ -184,6 +184,7 @@ struct TileFeed {
   uint64_t* empty;     // [kTileSlots] leader's, count kTileConsumers
   int slot;
   uint32_t phase;
+  uint32_t rank;       // CTA rank in the pair: the leader's codes are written locally
 
   // Consumer (warp-wide: all lanes wait, lane 0 releases the slot).  The
   // code is reduced across the warp before the release, so the slot is handed
@@ -191,7 +192,10 @@ struct TileFeed {
   // suffices (a release arrive costs an ERRBAR + MEMBAR per tile and role).
   __device__ __forceinline__ int32_t consume(const GemmParams& p, int lane) {
     if (!p.dynamic) return uniform(it < n ? list[it++] : -1);
-    ptx::mbar_wait_cluster(ptx::smem_u32(&full[slot]), phase);
+    if (rank == 0)  // scheduler in this CTA: CTA-scope acquire (no L1 invalidation)
+      ptx::mbar_wait(ptx::smem_u32(&full[slot]), phase);
+    else
+      ptx::mbar_wait_cluster(ptx::smem_u32(&full[slot]), phase);
     const int32_t code = uniform(*reinterpret_cast<volatile int32_t*>(&codes[slot]));
 #if MST_FEED_RELAXED
     if (lane == 0) ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&empty[slot]), 0));
@@ -771,7 +775,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = __reduce_min_sync(0xffffffffu, *tmem_slot);  // uniform register
 
   TileFeed feed{p.sched + p.sched_off[pair], p.sched_off[pair + 1] - p.sched_off[pair], 0, tile_codes,
-                tile_full, tile_empty, 0, 0};
+                tile_full, tile_empty, 0, 0, rank};
 
   if (warp == 0 || (MST_SPLIT_PRODUCER && warp == 3)) {
     // ===================== TMA producer(s) =====================
