@@ -15,4 +15,5 @@ ncu -i $O/ev_full.ncu-rep --page raw --csv > $O/ev_full_raw.csv 2>/dev/null
 rm -f $O/ev_full.ncu-rep
 timeout 900 python tools/sweep.py sweep-m > $O/ev_sweeps.jsonl 2> $O/ev_sweeps.err
 timeout 900 python tools/sweep.py long >> $O/ev_sweeps.jsonl 2>> $O/ev_sweeps.err
+timeout 900 python tools/sweep.py sweep-m2 > $O/ev_config2_msweep.jsonl 2>> $O/ev_sweeps.err
 timeout 900 python tools/sweep.py max-seq >> $O/ev_sweeps.jsonl 2>> $O/ev_sweeps.err

@@ -1,6 +1,7 @@
 """M-sweep and max-sequence measurements (BASELINE.json configs 3 and 4).
 
   python tools/sweep.py sweep-m   # config 3: Llama2-7B widths, S=16384, M in {1,2,4,8}
+  python tools/sweep.py sweep-m2  # config 2: Llama3-8B widths, S=8192, M in {1,2,4,8,16}
   python tools/sweep.py max-seq   # config 4: Llama3-8B widths, bisection on S under the device budget
   python tools/sweep.py long      # config 4: S=65536, M=16, timed steps
 
@@ -79,6 +80,23 @@ def sweep_m():
                           "device_peak_allocated_gb": peak / 1e9, "loss": loss}), flush=True)
 
 
+def sweep_m2():
+    """Config 2 (the bench workload) across M: the throughput cost of smaller chunks."""
+    dev = torch.device("cuda")
+    H, I, V, S = 4096, 14336, 128256, 8192
+    X, L, W = make(S, H, I, V, dev)
+    for M in (1, 2, 4, 8, 16):
+        torch.cuda.reset_peak_memory_stats()
+        ms_step, loss = timed_steps(X, L, W, M, M)
+        print(json.dumps({"config": "2 (Llama3-8B widths, S=8192)", "M": M, "ms_per_step": ms_step,
+                          "tokens_per_s": S / ms_step * 1e3,
+                          "tflops": S * flops_per_token(H, I, V) / ms_step / 1e9,
+                          "peak_intermediate_gb": intermediate_bytes(S, I, V, M, M) / 1e9,
+                          "workspace_gb": ms.block_workspace_bytes(S, H, I, V, M, M) / 1e9,
+                          "device_peak_allocated_gb": torch.cuda.max_memory_allocated() / 1e9, "loss": loss}),
+              flush=True)
+
+
 def long_context():
     dev = torch.device("cuda")
     H, I, V, S, M = 4096, 14336, 128256, 65536, 16
@@ -131,4 +149,4 @@ def max_seq(chunk=8192):
 
 
 if __name__ == "__main__":
-    {"sweep-m": sweep_m, "max-seq": max_seq, "long": long_context}[sys.argv[1]]()
+    {"sweep-m": sweep_m, "sweep-m2": sweep_m2, "max-seq": max_seq, "long": long_context}[sys.argv[1]]()
