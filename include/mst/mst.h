@@ -123,7 +123,8 @@ MST_API int mst_ctx_set_profile_buffer(mst_ctx* ctx, void* dev_counters);
 /* Tuning knobs (benchmark / A-B use; defaults are the tuned values; the
  * measured effect of each is in DESIGN.md 4.2):
  *   "dynamic": 1 (default) CTA pairs pull tiles from the global LPT order
- *              through an atomic counter; 0 static per-pair LPT lists;
+ *              through an atomic counter (a scheduler thread per pair claims
+ *              up to 8 tiles ahead); 0 static per-pair LPT lists;
  *   "tma3d":   MN-major operands as 3-D tensor maps (process-wide, default 1);
  *   "fused_head": 1 (default) block_step runs mst_lmhead_fused, 0 runs the
  *              separate forward + backward (logits recomputed);
