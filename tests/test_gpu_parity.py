@@ -403,3 +403,39 @@ def test_config2_full_size_properties():
     assert abs(res[8][0] - float(ref["loss"])) <= 1e-3 * float(ref["loss"])
     for k, rk in (("dX", "dX"), ("W_out", "dWout"), ("W_gate", "dWg"), ("W_up", "dWu"), ("W_down", "dWd")):
         assert R.relerr(res[8][1][k], ref[rk]) <= 1e-2, k
+
+
+def test_tile_scheduler_back_to_back_launches():
+    """The dynamic tile scheduler (one claiming thread per CTA pair, an
+    8-entry code ring, a claim counter the last pair re-zeroes on exit):
+    back-to-back launches with fewer tiles than pairs, exactly one tile per
+    pair, and many waves, in both scheduling modes, with no host sync in
+    between.  Results must equal the static per-pair lists bitwise (the tile
+    order does not change any tile's arithmetic)."""
+    torch.manual_seed(5)
+    ctx = ms.Context.get(0)
+    pairs = ctx.lib.mst_ctx_num_pairs(ctx.handle)
+    shapes = [(256, 256, 128), (256, 256 * pairs, 64), (512, 256 * (pairs - 1), 1024), (2048, 4096, 512),
+              (296, 520, 72)]
+    data = []
+    for (M, N, K) in shapes:
+        data.append((torch.randn(M, K, device="cuda").bfloat16(), torch.randn(K, N, device="cuda").bfloat16(),
+                     M, N, K))
+    outs = {}
+    try:
+        for mode in (0, 1):
+            ctx.set_tuning("dynamic", mode)
+            res = []
+            for rep in range(3):
+                for A, B, M, N, K in data:
+                    out = torch.zeros(M, N, device="cuda", dtype=torch.float32)
+                    ms.debug_gemm(A, B, M, N, K, 0, 1, out)
+                    res.append(out)
+            torch.cuda.synchronize()
+            outs[mode] = res
+    finally:
+        ctx.set_tuning("dynamic", 1)
+    for a, b in zip(outs[0], outs[1]):
+        assert torch.equal(a, b)
+    for (A, B, M, N, K), out in zip(data, outs[1]):
+        assert rel(out, (A.double() @ B.double()).cpu().numpy()) <= 1e-5
