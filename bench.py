@@ -297,7 +297,9 @@ def main() -> None:
     grads = ms.alloc_block_grads(S, H, I, V, dev)
     nch = min(S, Mh)
     stats = torch.empty(ms.stats_len(nch), dtype=torch.float32, device=dev)
-    ws = torch.empty(ms.block_workspace_bytes(S, H, I, V, Mm, Mh), dtype=torch.uint8, device=dev)
+    if world > 1:  # the op-by-op schedule overlaps the dW all-reduce (see below)
+        ctx.set_tuning("chunked_block", 1 if os.environ.get("MST_SP_CHUNKED") == "1" else 0)
+    ws = torch.empty(ms.block_workspace_bytes(S, H, I, V, Mm, Mh, ctx), dtype=torch.uint8, device=dev)
 
     if world == 1:
         def run_step(Xs, Ls):
@@ -418,10 +420,16 @@ def main() -> None:
     traffic = ncu_traffic_per_launch()
     executed_fpt = gemm_flops / args.steps / S if gemm_flops else flops_per_token()
     tflops_step = tokens_step / world * executed_fpt / (ms_step / 1e3) / 1e12
-    ws_m1 = ms.block_workspace_bytes(S, H, I, V, 1, 1)
-    # block workspace = O, dO, lse ([S]-sized activations) + the chunk buffers
-    act_fixed = 2 * S * H * 2 + S * 4
-    inter = lambda mm, mh: ms.block_workspace_bytes(S, H, I, V, mm, mh) - act_fixed  # noqa: E731
+    ws_m1 = ms.block_workspace_bytes(S, H, I, V, 1, 1, ctx)
+
+    def act_fixed(mm, mh):
+        """O / dO / lse part of the block workspace: one O and two dO chunks
+        plus lse (chunk-wise schedule), or full [S, H] O and dO (op-by-op)."""
+        if (world == 1 or os.environ.get("MST_SP_CHUNKED") == "1") and mm == mh:
+            return 3 * -(-S // min(S, mm)) * H * 2 + S * 4
+        return 2 * S * H * 2 + S * 4
+
+    inter = lambda mm, mh: ms.block_workspace_bytes(S, H, I, V, mm, mh, ctx) - act_fixed(mm, mh)  # noqa: E731
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",

@@ -221,6 +221,12 @@ MST_API int mst_make_chunk_plan(int64_t n, int64_t m, int64_t* bounds, int64_t* 
 MST_API int mst_mlp_workspace(int64_t n, int64_t h, int64_t i, int64_t m, size_t* bytes);
 MST_API int mst_lmhead_workspace(int64_t n, int64_t h, int64_t v, int64_t m, size_t* bytes);
 MST_API int mst_block_workspace(int64_t n, int64_t h, int64_t i, int64_t v, int64_t m_mlp, int64_t m_head, size_t* bytes);
+/* Workspace of mst_block_step / mst_block_step_sp under this context's
+ * schedule knobs (mst_block_workspace is the maximum over all schedules).
+ * The chunk-wise schedule (default when m_mlp == m_head) keeps only one O
+ * chunk and two dO chunks: 4 bytes of lse per token plus chunk buffers. */
+MST_API int mst_ctx_block_workspace(const mst_ctx* ctx, int64_t n, int64_t h, int64_t i, int64_t v, int64_t m_mlp,
+                                    int64_t m_head, size_t* bytes);
 
 /* miniseq_mlp_forward(X, w, plan) -> (O, saved) — SPEC.md:295-303, Alg. 1.
  * O = (silu(X W_gate) * (X W_up)) W_down per chunk; only X is retained. */

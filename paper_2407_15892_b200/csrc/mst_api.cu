@@ -1194,6 +1194,11 @@ int mst_lmhead_workspace(int64_t n, int64_t h, int64_t v, int64_t m, size_t* byt
 }
 
 static size_t block_fixed_bytes(int64_t n, int64_t h) { return align_up(size_t(n) * h * 2, 256) * 2 + align_up(size_t(n) * 4, 256); }
+// Chunk-wise block: O_j lives only within chunk j, dO_j until chunk j+1's
+// dW_down GEMM (double buffer); lse stays sequence-sized (4 bytes / token).
+static size_t chunked_fixed_bytes(int64_t n, int64_t h, int64_t m) {
+  return align_up(size_t(max_chunk(n, m)) * h * 2, 256) * 3 + align_up(size_t(n) * 4, 256);
+}
 
 // Chunk-wise block (M_mlp == M_head): MLP and head chunk buffers coexist,
 // plus the forward's fp32 G, U accumulators of one chunk.
@@ -1206,8 +1211,25 @@ int mst_block_workspace(int64_t n, int64_t h, int64_t i, int64_t v, int64_t m_ml
   MST_TRY(mst_mlp_workspace(n, h, i, m_mlp, &a));
   MST_TRY(mst_lmhead_workspace(n, h, v, m_head, &b));
   const size_t two_pass = block_fixed_bytes(n, h) + 256 + std::max(a, b);
-  const size_t chunked = m_mlp == m_head ? block_fixed_bytes(n, h) + 256 + a + b + chunked_extra_bytes(n, i, m_mlp) : 0;
+  const size_t chunked =
+      m_mlp == m_head ? chunked_fixed_bytes(n, h, m_mlp) + 256 + a + b + chunked_extra_bytes(n, i, m_mlp) : 0;
   *bytes = std::max(two_pass, chunked);
+  return MST_OK;
+}
+
+static bool uses_chunked_block(const mst_ctx* c, int64_t m_mlp, int64_t m_head) {
+  return c->chunked_block && c->fused_head && m_mlp == m_head;
+}
+
+int mst_ctx_block_workspace(const mst_ctx* c, int64_t n, int64_t h, int64_t i, int64_t v, int64_t m_mlp,
+                            int64_t m_head, size_t* bytes) {
+  if (!c || !bytes) return fail(MST_ERR_STATE, "NULL context or output");
+  size_t a = 0, b = 0;
+  MST_TRY(mst_mlp_workspace(n, h, i, m_mlp, &a));
+  MST_TRY(mst_lmhead_workspace(n, h, v, m_head, &b));
+  *bytes = uses_chunked_block(c, m_mlp, m_head)
+               ? chunked_fixed_bytes(n, h, m_mlp) + 256 + a + b + chunked_extra_bytes(n, i, m_mlp)
+               : block_fixed_bytes(n, h) + 256 + std::max(a, b);
   return MST_OK;
 }
 
@@ -1646,11 +1668,13 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
                               float* dwu, float* dwd, float* dwout, int accumulate, void* ws, size_t ws_bytes,
                               const float* global_valid) {
   char* base = static_cast<char*>(ws);
-  const size_t ob = align_up(size_t(n) * h * 2, 256);
+  // O_j is consumed within chunk j; dO_j also by chunk j's dW_down GEMM,
+  // which runs in chunk j+1's K2 launch: one O chunk, two dO chunks.
+  const size_t ocb = align_up(size_t(max_chunk(n, m)) * h * 2, 256);
   void* o = base;
-  void* dO = base + ob;
-  float* lse = reinterpret_cast<float*>(base + 2 * ob);
-  Carve cv{base + block_fixed_bytes(n, h) + 256, ws_bytes, 0, false};
+  void* dO[2] = {base + ocb, base + 2 * ocb};
+  float* lse = reinterpret_cast<float*>(base + 3 * ocb);
+  Carve cv{base + chunked_fixed_bytes(n, h, m) + 256, ws_bytes, 0, false};
   void *hb, *dg, *du, *xt, *ht, *dl, *ot;
   float *dhb, *zt, *lrow, *scales;
   float2* part;
@@ -1674,9 +1698,9 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
   grad_scale_kernel<<<(nch + 255) / 256, 256, 0, st>>>(gstats, stats, nch, loss_mode, grad_loss, scales);
   c->launches += 3;
   WeightScope ws_(c, wg, wu, wd, wout);
-  const uint64_t act_bytes = (uint64_t)n * h * 2;
+  const uint64_t act_bytes = (uint64_t)max_chunk(n, m) * h * 2;  // one chunk of O, two of dO
   mem_alloc(c, act_bytes, "act.O");
-  mem_alloc(c, act_bytes, "act.dO");
+  mem_alloc(c, 2 * act_bytes, "act.dO");
   mem_alloc(c, (uint64_t)n * 4, "act.lse");
   auto rows_of = [&](int j) { return b[j + 1] - b[j]; };
   // Logical lifetimes of the chunk buffers (MemTracker events, mst.h).
@@ -1727,7 +1751,7 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
     if (j == 0)
       for (int wi = 0; wi < 3; ++wi) grad_alloc(c, wi, (uint64_t)h * i * 4);
     const int beta = (j > 0 || accumulate) ? 1 : 0;
-    return add_mlp_grads(c, L, dg, du, ht, xt, bptr(dO, b[j] * h), wg, wu, const_cast<char*>(bptr(dx, b[j] * h)),
+    return add_mlp_grads(c, L, dg, du, ht, xt, dO[j & 1], wg, wu, const_cast<char*>(bptr(dx, b[j] * h)),
                          dwg, dwu, dwd, rows, h, i, ldt, beta);
   };
   {
@@ -1738,8 +1762,8 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
   for (int j = 0; j < nch; ++j) {
     const int64_t r0 = b[j], rows = rows_of(j);
     const int beta = (j > 0 || accumulate) ? 1 : 0;
-    void* oj = const_cast<char*>(bptr(o, r0 * h));
-    void* doj = const_cast<char*>(bptr(dO, r0 * h));
+    void* oj = o;
+    void* doj = dO[j & 1];
     {  // K2(j) + the weight/input gradients of chunk j-1
       Launch L;
       MST_TRY(build_plain(c, L, Operand{hb, rows, i, i, false}, Operand{wd, h, i, h, true}, oj, h, mst::kEpiStoreBf16,
@@ -1837,7 +1861,7 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
   }
   for (int wi = 0; wi < 3; ++wi) grad_ready(c, wi, st, (uint64_t)h * i * 4);  // dW_gate, dW_up, dW_down complete
   mem_free(c, (uint64_t)n * 4, "act.lse");
-  mem_free(c, act_bytes, "act.dO");
+  mem_free(c, 2 * act_bytes, "act.dO");
   mem_free(c, act_bytes, "act.O");
   finalize_loss_kernel<<<1, 32, 0, st>>>(stats, nch, loss_mode);
   c->launches += 1;
@@ -1859,13 +1883,13 @@ int mst_block_step_sp(mst_ctx* c, void* stream, const void* x, const int32_t* la
                       float* dwd, float* dwout, int accumulate, void* ws, size_t ws_bytes, const float* global_valid) {
   if (!c) return fail(MST_ERR_STATE, "NULL context");
   size_t need = 0;
-  MST_TRY(mst_block_workspace(n, h, i, v, m_mlp, m_head, &need));
+  MST_TRY(mst_ctx_block_workspace(c, n, h, i, v, m_mlp, m_head, &need));
   if (!ws || ws_bytes < need) return fail(MST_ERR_CONFIG, "workspace too small (%zu < %zu)", ws_bytes, need);
   if (loss_mode != MST_LOSS_TOKEN_WEIGHTED && loss_mode != MST_LOSS_PAPER_MEAN)
     return fail(MST_ERR_CONFIG, "unknown loss mode %d", loss_mode);
   if (!x || !labels || !wg || !wu || !wd || !wout || !stats || !dx || !dwg || !dwu || !dwd || !dwout)
     return fail(MST_ERR_CONFIG, "NULL tensor pointer");
-  if (c->chunked_block && c->fused_head && m_mlp == m_head)
+  if (uses_chunked_block(c, m_mlp, m_head))
     return block_step_chunked(c, static_cast<cudaStream_t>(stream), x, labels, wg, wu, wd, wout, n, h, i, v, m_mlp,
                               loss_mode, grad_loss, stats, dx, dwg, dwu, dwd, dwout, accumulate, ws, ws_bytes,
                               global_valid);

@@ -49,12 +49,13 @@ def predict_block_peak(N: int, H: int, I: int, V: int, M: int) -> Dict[str, int]
     report them: the MLP chunk buffers h (bf16), G and U (fp32, kept for the
     backward), dh (fp32), dG, dU, h^T (bf16) -> 20 n I bytes at their common
     peak; the LM-Head chunk's softmax numerators / dlogits (bf16) plus the
-    per-256-column CE partials and two fp32 row scalars; the step-wide
-    activations O, dO (bf16) and lse (fp32)."""
+    per-256-column CE partials and two fp32 row scalars; the activations:
+    one O chunk and two dO chunks (bf16; dO_j is read by chunk j+1's dW_down
+    GEMM) and the sequence-wide lse (fp32)."""
     n = _chunk(N, M)
     head = n * V * 2 + n * (-(-V // 256)) * 8 + n * 8
     mlp = 20 * n * I
     # the head's chunk buffers coexist with the forward MLP buffers of the same chunk (h, G, U = 10 n I)
     inter = max(mlp, 10 * n * I + head)
-    return {"inter.mlp.": mlp, "inter.head.": head, "inter.": inter, "act.O": N * H * 2, "act.dO": N * H * 2,
+    return {"inter.mlp.": mlp, "inter.head.": head, "inter.": inter, "act.O": n * H * 2, "act.dO": 2 * n * H * 2,
             "act.lse": N * 4}

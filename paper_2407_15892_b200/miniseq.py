@@ -108,6 +108,8 @@ _SIGS = {
     "mst_mlp_workspace": ([_I64, _I64, _I64, _I64, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
     "mst_lmhead_workspace": ([_I64, _I64, _I64, _I64, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
     "mst_block_workspace": ([_I64, _I64, _I64, _I64, _I64, _I64, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
+    "mst_ctx_block_workspace": ([_VP, _I64, _I64, _I64, _I64, _I64, _I64, ctypes.POINTER(ctypes.c_size_t)],
+                                ctypes.c_int),
     "mst_mlp_forward": ([_VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _I64, _I64, _VP, ctypes.c_size_t,
                          ctypes.POINTER(_MlpSaved)], ctypes.c_int),
     "mst_mlp_backward": ([_VP, _VP, _VP, ctypes.POINTER(_MlpSaved), _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I32,
@@ -587,9 +589,15 @@ class BlockGrads:
     W_out: torch.Tensor
 
 
-def block_workspace_bytes(N: int, H: int, I: int, V: int, M_mlp: int, M_head: int) -> int:
+def block_workspace_bytes(N: int, H: int, I: int, V: int, M_mlp: int, M_head: int,
+                          ctx: Optional["Context"] = None) -> int:
+    """Workspace of block_step: for `ctx`'s schedule knobs (mst_ctx_block_workspace),
+    else the maximum over all schedules (mst_block_workspace)."""
     nb = ctypes.c_size_t()
-    _check(load_library().mst_block_workspace(N, H, I, V, M_mlp, M_head, ctypes.byref(nb)))
+    if ctx is not None:
+        _check(ctx.lib.mst_ctx_block_workspace(ctx.handle, N, H, I, V, M_mlp, M_head, ctypes.byref(nb)))
+    else:
+        _check(load_library().mst_block_workspace(N, H, I, V, M_mlp, M_head, ctypes.byref(nb)))
     return nb.value
 
 
@@ -633,7 +641,7 @@ def block_step(X: torch.Tensor, L: torch.Tensor, mlp: MlpWeights, head: LmHeadWe
     nch = min(N, M_head)
     if stats is None:
         stats = torch.empty(stats_len(nch), dtype=torch.float32, device=X.device)
-    need = block_workspace_bytes(N, H, I, V, M_mlp, M_head)
+    need = block_workspace_bytes(N, H, I, V, M_mlp, M_head, ctx)
     ws = workspace if workspace is not None else ctx.workspace(need)
     if global_valid is not None:
         _req(global_valid, "global_valid", torch.float32, (1,))

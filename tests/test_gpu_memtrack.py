@@ -106,8 +106,9 @@ def test_tracked_peak_intermediate_scales_as_one_over_M():
         head = reg.report.peak_for_prefix("inter.head.")
         assert head == n * V * 2 + n * ((V + 255) // 256) * 8 + n * 8  # dlogits (bf16) + CE partials
         peaks[M] = (head, reg.report.peak_for_prefix("inter.mlp."), reg.report.peak_for_prefix("inter."))
-        # the tracked act.* (O, dO, lse, operand transposes) do not depend on M except the transposes
-        assert reg.report.peak_for_prefix("act.O") == N * H * 2
+        # the chunk-wise schedule keeps one O chunk and two dO chunks (dO_j feeds chunk j+1's dW_down GEMM)
+        assert reg.report.peak_for_prefix("act.O") == n * H * 2
+        assert reg.report.peak_for_prefix("act.dO") == 2 * n * H * 2
     assert peaks[1][0] == 8 * peaks[8][0]
     assert peaks[1][1] == 8 * peaks[8][1]
     assert peaks[1][2] == 8 * peaks[8][2]

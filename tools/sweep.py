@@ -30,7 +30,7 @@ def flops_per_token(H, I, V):
 
 def make(S, H, I, V, dev, seed=0):
     g = torch.Generator(device=dev).manual_seed(seed)
-    X = torch.randn(S, H, device=dev, generator=g).bfloat16()
+    X = torch.randn(S, H, device=dev, generator=g, dtype=torch.bfloat16)  # no fp32 temporary (max-seq)
     W = [(0.02 * torch.randn(*s, device=dev, generator=g)).bfloat16() for s in ((H, I), (H, I), (I, H), (H, V))]
     L = torch.randint(0, V, (S,), device=dev, generator=g, dtype=torch.int32)
     return X, L, W
@@ -42,7 +42,8 @@ def timed_steps(X, L, W, M_mlp, M_head, steps=3, warmup=2):
     mlp, head = ms.MlpWeights(*W[:3]), ms.LmHeadWeights(W[3])
     grads = ms.alloc_block_grads(S, H, I, V, X.device)
     stats = torch.empty(ms.stats_len(min(S, M_head)), device=X.device)
-    ws = torch.empty(ms.block_workspace_bytes(S, H, I, V, M_mlp, M_head), dtype=torch.uint8, device=X.device)
+    ws = torch.empty(ms.block_workspace_bytes(S, H, I, V, M_mlp, M_head, ms.Context.get(X.device.index)),
+                     dtype=torch.uint8, device=X.device)
     for _ in range(warmup):
         ms.block_step(X, L, mlp, head, M_mlp, M_head, grads=grads, stats=stats, workspace=ws)
     torch.cuda.synchronize()
@@ -76,7 +77,7 @@ def sweep_m():
                           "ms_per_step": ms_step, "tokens_per_s": S / ms_step * 1e3,
                           "tflops": S * flops_per_token(H, I, V) / ms_step / 1e9,
                           "peak_intermediate_gb": intermediate_bytes(S, I, V, M, M) / 1e9,
-                          "workspace_gb": ms.block_workspace_bytes(S, H, I, V, M, M) / 1e9,
+                          "workspace_gb": ms.block_workspace_bytes(S, H, I, V, M, M, ms.Context.get(0)) / 1e9,
                           "device_peak_allocated_gb": peak / 1e9, "loss": loss}), flush=True)
 
 
@@ -92,7 +93,7 @@ def sweep_m2():
                           "tokens_per_s": S / ms_step * 1e3,
                           "tflops": S * flops_per_token(H, I, V) / ms_step / 1e9,
                           "peak_intermediate_gb": intermediate_bytes(S, I, V, M, M) / 1e9,
-                          "workspace_gb": ms.block_workspace_bytes(S, H, I, V, M, M) / 1e9,
+                          "workspace_gb": ms.block_workspace_bytes(S, H, I, V, M, M, ms.Context.get(0)) / 1e9,
                           "device_peak_allocated_gb": torch.cuda.max_memory_allocated() / 1e9, "loss": loss}),
               flush=True)
 
@@ -130,7 +131,7 @@ def max_seq(chunk=8192):
         except (torch.OutOfMemoryError, ms.Error) as e:  # pragma: no cover
             return False, str(e)[:80], 0, None
 
-    lo, hi = 65536, 8 * 1024 * 1024
+    lo, hi = 65536, 16 * 1024 * 1024
     best = None
     t0 = time.time()
     while hi - lo > 65536 and time.time() - t0 < 900:
