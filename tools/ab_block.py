@@ -18,12 +18,12 @@ Wo = (0.02 * torch.randn(H, V, device=dev)).bfloat16()
 L = torch.randint(0, V, (S,), device=dev, dtype=torch.int32)
 g = ms.alloc_block_grads(S, H, I, V, dev)
 stats = torch.empty(ms.stats_len(M), device=dev)
-ws = torch.empty(ms.block_workspace_bytes(S, H, I, V, M, M), dtype=torch.uint8, device=dev)
 handles = []
 for spec in libs:
     p, *opts = spec.split(':')
     lib = ctypes.CDLL(p)
     for name, (args, res) in ms._SIGS.items():
+        if not hasattr(lib, name): continue  # older build (A/B against a previous revision)
         f = getattr(lib, name); f.argtypes = args; f.restype = res
     h = ctypes.c_void_p()
     assert lib.mst_ctx_create(0, ctypes.byref(h)) == 0, lib.mst_last_error()
@@ -31,6 +31,14 @@ for spec in libs:
         k, v = o.split('=')
         assert lib.mst_ctx_set_tuning(h, k.encode(), int(v)) == 0, lib.mst_last_error()
     handles.append((lib, h))
+def ws_bytes(lib):
+    import ctypes as C
+    nb = C.c_size_t()
+    assert lib.mst_block_workspace(S, H, I, V, M, M, C.byref(nb)) == 0
+    return nb.value
+
+
+ws = torch.empty(max(ws_bytes(lib) for lib, _ in handles), dtype=torch.uint8, device=dev)
 st = torch.cuda.current_stream().cuda_stream
 def step(k):
     lib, h = handles[k]

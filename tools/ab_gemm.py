@@ -9,6 +9,7 @@ for spec in sys.argv[1:3]:
     p, *opts = spec.split(':')
     lib = ctypes.CDLL(p)
     for name, (args, res) in ms._SIGS.items():
+        if not hasattr(lib, name): continue  # older build (A/B against a previous revision)
         f = getattr(lib, name); f.argtypes = args; f.restype = res
     h = ctypes.c_void_p(); assert lib.mst_ctx_create(0, ctypes.byref(h)) == 0
     for o in opts:
