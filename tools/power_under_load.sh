@@ -1,3 +1,4 @@
+#!/bin/bash
 # dev: board power / clocks while the config-2 block step runs back to back
 cat > /tmp/loop.py <<'PY'
 import sys, time, torch
