@@ -344,7 +344,8 @@ MST_API int mst_embedding_backward(mst_ctx* ctx, void* stream, const int32_t* or
 /* Diagnostic single GEMM through the same engine: C[M,N] = A[M,K] B[K,N].
  * a_mn=0: A row-major [M,K]; a_mn=1: A given as row-major [K,M] (A^T).
  * b_mn=1: B row-major [K,N]; b_mn=0: B given as row-major [N,K] (B^T).
- * out_f32=0: C bf16; 1: C fp32 with C = beta*C + A B (beta in {0,1}). */
+ * out_f32=0: C bf16; 1: C fp32 with C = beta*C + A B (beta in {0,1});
+ * beta = 1 with the bf16 output is MST_ERR_CONFIG. */
 MST_API int mst_debug_gemm(mst_ctx* ctx, void* stream, const void* a, const void* b, void* c, int64_t m, int64_t n,
                    int64_t k, int a_mn, int b_mn, int out_f32, int beta);
 

@@ -2004,6 +2004,7 @@ int mst_debug_gemm(mst_ctx* c, void* stream, const void* a, const void* b, void*
   if (!c) return fail(MST_ERR_STATE, "NULL context");
   if (m <= 0 || n <= 0 || k <= 0) return fail(MST_ERR_SHAPE, "extents must be positive");
   if (m % 8 || n % 8 || k % 8) return fail(MST_ERR_SHAPE, "extents must be multiples of 8");
+  if (beta && !out_f32) return fail(MST_ERR_CONFIG, "accumulation (beta = 1) needs the fp32 output");
   Launch L;
   Operand oa = a_mn ? Operand{a, m, k, m, true} : Operand{a, m, k, k, false};
   Operand ob = b_mn ? Operand{b, n, k, n, true} : Operand{b, n, k, k, false};
