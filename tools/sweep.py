@@ -2,6 +2,7 @@
 
   python tools/sweep.py sweep-m   # config 3: Llama2-7B widths, S=16384, M in {1,2,4,8}
   python tools/sweep.py sweep-m2  # config 2: Llama3-8B widths, S=8192, M in {1,2,4,8,16}
+  python tools/sweep.py seq       # Llama3-8B widths, S = 8K..128K at chunk 1024 / 4096
   python tools/sweep.py max-seq   # config 4: Llama3-8B widths, bisection on S under the device budget
   python tools/sweep.py long      # config 4: S=65536, M=16, timed steps
 
@@ -98,6 +99,24 @@ def sweep_m2():
               flush=True)
 
 
+def seq_sweep():
+    """Config-2 widths across sequence lengths at fixed chunk lengths (n = 1024
+    and 4096 tokens): throughput and workspace versus S."""
+    dev = torch.device("cuda")
+    H, I, V = 4096, 14336, 128256
+    for S in (8192, 16384, 32768, 65536, 131072):
+        X, L, W = make(S, H, I, V, dev)
+        for n in (1024, 4096):
+            M = S // n
+            ms_step, loss = timed_steps(X, L, W, M, M, steps=2, warmup=1)
+            print(json.dumps({"config": "Llama3-8B widths, sequence sweep", "S": S, "chunk": n, "M": M,
+                              "ms_per_step": ms_step, "tokens_per_s": S / ms_step * 1e3,
+                              "workspace_gb": ms.block_workspace_bytes(S, H, I, V, M, M, ms.Context.get(0)) / 1e9,
+                              "loss": loss}), flush=True)
+        del X, L, W
+        torch.cuda.empty_cache()
+
+
 def long_context():
     dev = torch.device("cuda")
     H, I, V, S, M = 4096, 14336, 128256, 65536, 16
@@ -150,4 +169,5 @@ def max_seq(chunk=8192):
 
 
 if __name__ == "__main__":
-    {"sweep-m": sweep_m, "sweep-m2": sweep_m2, "max-seq": max_seq, "long": long_context}[sys.argv[1]]()
+    {"sweep-m": sweep_m, "sweep-m2": sweep_m2, "seq": seq_sweep, "max-seq": max_seq,
+     "long": long_context}[sys.argv[1]]()
