@@ -17,6 +17,7 @@ Rank 0 prints ONE JSON line.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import math
 import os
@@ -382,15 +383,30 @@ def main() -> None:
                 Lb[k].copy_(Lh, non_blocking=True)
                 ready[k].record(cstream)
 
-        def run_e2e(n):
-            prefetch(0)
-            for it in range(n):
-                k = it & 1
-                stream.wait_event(ready[k])
-                if it + 1 < n:
-                    prefetch(1 - k)
-                loss_h.copy_(run_step(Xb[k], Lb[k]), non_blocking=True)
-                free[k].record(stream)
+        host_abi = world == 1 and Mm == Mh
+        if host_abi:
+            # Through the C ABI with host buffers: mst_block_step_host copies
+            # X_j in and dX_j out chunk by chunk on its copy stream while the
+            # GEMMs run; the loss is read back every step.
+            dXh = torch.empty(S, H, dtype=torch.bfloat16).pin_memory()
+            nb = ctypes.c_size_t()
+            ms._check(ctx.lib.mst_ctx_block_host_workspace(ctx.handle, S, H, I, V, Mm, ctypes.byref(nb)))
+            hws = torch.empty(nb.value, dtype=torch.uint8, device=dev)
+
+            def run_e2e(n):
+                for _ in range(n):
+                    st_, _ = ms.block_step_host(Xh, Lh, mlp, head, Mm, dXh, grads=grads, stats=stats, workspace=hws)
+                    loss_h.copy_(st_[2:3], non_blocking=True)
+        else:
+            def run_e2e(n):
+                prefetch(0)
+                for it in range(n):
+                    k = it & 1
+                    stream.wait_event(ready[k])
+                    if it + 1 < n:
+                        prefetch(1 - k)
+                    loss_h.copy_(run_step(Xb[k], Lb[k]), non_blocking=True)
+                    free[k].record(stream)
 
         run_e2e(2)
         torch.cuda.synchronize(dev)
@@ -405,10 +421,13 @@ def main() -> None:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t)
         e2e = {"value": tokens_step / dt, "unit": UNIT, "h2d_bytes_per_step": Xh.numel() * 2 + Lh.numel() * 4,
-               "d2h_bytes_per_step": 4, "ms_per_step": dt * 1e3,
-               "path": "pinned host X/labels -> H2D (double-buffered, copy stream overlapping the previous step), "
-                       "miniseq.block_step (C ABI mst_block_step) "
-                       "[sp_block_step_fused: mst_block_step_sp + NCCL for N>1], loss D2H; wall clock with synchronize"}
+               "d2h_bytes_per_step": 4 + (S * H * 2 if host_abi else 0), "ms_per_step": dt * 1e3,
+               "path": ("C ABI mst_block_step_host with pinned host X / labels / dX: X_j H2D and dX_j D2H per chunk "
+                        "on a copy stream overlapping the GEMMs, loss D2H every step; wall clock with synchronize"
+                        if host_abi else
+                        "pinned host X/labels -> H2D (double-buffered, copy stream overlapping the previous step), "
+                        "block_step / sp_block_step_fused (mst_block_step[_sp] + NCCL for N>1), loss D2H; "
+                        "wall clock with synchronize")}
 
     if rank != 0:
         if world > 1:

@@ -228,6 +228,23 @@ MST_API int mst_block_workspace(int64_t n, int64_t h, int64_t i, int64_t v, int6
 MST_API int mst_ctx_block_workspace(const mst_ctx* ctx, int64_t n, int64_t h, int64_t i, int64_t v, int64_t m_mlp,
                                     int64_t m_head, size_t* bytes);
 
+/* mst_block_step with host-resident X, labels and dX (pinned host memory for
+ * asynchronous copies): X_j is copied in chunk by chunk on the context's copy
+ * stream while earlier chunks compute, dX_j is copied out as soon as it is
+ * final, so the copies overlap the GEMMs and the device holds only chunk
+ * buffers of X / dX (the sequence is bounded by host memory).  Chunk-wise
+ * schedule only (M_mlp == M_head == m); results are bitwise those of
+ * mst_block_step.  Everything is ordered on `stream` (the copy stream is
+ * joined back before the call's work ends).  Workspace from
+ * mst_ctx_block_host_workspace. */
+MST_API int mst_ctx_block_host_workspace(const mst_ctx* ctx, int64_t n, int64_t h, int64_t i, int64_t v, int64_t m,
+                                         size_t* bytes);
+MST_API int mst_block_step_host(mst_ctx* ctx, void* stream, const void* x_host, const int32_t* labels_host,
+                                const void* w_gate, const void* w_up, const void* w_down, const void* w_out, int64_t n,
+                                int64_t h, int64_t i, int64_t v, int64_t m, int loss_mode, float grad_loss, float* stats,
+                                void* grad_x_host, float* grad_w_gate, float* grad_w_up, float* grad_w_down,
+                                float* grad_w_out, int accumulate, void* workspace, size_t workspace_bytes);
+
 /* miniseq_mlp_forward(X, w, plan) -> (O, saved) — SPEC.md:295-303, Alg. 1.
  * O = (silu(X W_gate) * (X W_up)) W_down per chunk; only X is retained. */
 MST_API int mst_mlp_forward(mst_ctx* ctx, void* stream, const void* x, const void* w_gate, const void* w_up,

@@ -124,6 +124,9 @@ struct mst_ctx {
   int wide_mask = 0;
   int fuse_swiglu_bwd = 0;  // 1: chunk-wise block runs the SwiGLU backward in the dh GEMM epilogue (measured -0.7%: off)
   int debug_nblk = 1;     // N blocks per tile of mst_debug_gemm
+  // mst_block_step_host: copy stream and chunk events (created on first use)
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t io_ev[9] = {};
   // memtrack side (mst.h): counters per memtrack.hpp:19-35, event hooks
   mst_counters ctr{};
   mst_mem_hook mem_fn = nullptr;
@@ -961,6 +964,9 @@ void mst_ctx_destroy(mst_ctx* c) {
   for (auto& kv : c->sched_cache) cudaFree(kv.second.dev);
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   cudaFree(c->scratch_dev);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  for (cudaEvent_t e : c->io_ev)
+    if (e) cudaEventDestroy(e);
   delete c;
 }
 
@@ -1662,11 +1668,30 @@ int mst_count_valid(mst_ctx* c, void* stream, const int32_t* labels, int64_t n, 
 // same values: same tiles, same K order).  K8/K9/K10 of chunk j-1 share a
 // launch with K2 of chunk j.  Chunk buffers of both blocks coexist (peak
 // intermediate = one MLP chunk + one head chunk).
+// Host-resident X / dX for the chunk-wise block (mst_block_step_host): X_j is
+// copied in on the context's copy stream into one of two device chunk
+// buffers while earlier chunks compute, dX_j is copied out as soon as its
+// GEMM (K9, in chunk j+1's K2 launch) has run.  Events: x_ready / x_free /
+// dx_ready / dx_free per buffer, plus `done` joining the copies back into
+// the compute stream.
+struct HostIO {
+  const char* x_host;
+  char* dx_host;
+  void* xbuf[2];
+  void* dxbuf[2];
+  cudaStream_t cs;
+  cudaEvent_t x_ready[2], x_free[2], dx_ready[2], dx_free[2], done;
+};
+
+static size_t host_io_bytes(int64_t n, int64_t h, int64_t m) {  // 2 X + 2 dX chunk buffers, labels, alignment
+  return 4 * align_up(size_t(max_chunk(n, m)) * h * 2, 256) + align_up(size_t(n) * 4, 256) + 2048;
+}
+
 static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const int32_t* labels, const void* wg,
                               const void* wu, const void* wd, const void* wout, int64_t n, int64_t h, int64_t i,
                               int64_t v, int64_t m, int loss_mode, float grad_loss, float* stats, void* dx, float* dwg,
                               float* dwu, float* dwd, float* dwout, int accumulate, void* ws, size_t ws_bytes,
-                              const float* global_valid) {
+                              const float* global_valid, const HostIO* io = nullptr) {
   char* base = static_cast<char*>(ws);
   // O_j is consumed within chunk j; dO_j also by chunk j's dW_down GEMM,
   // which runs in chunk j+1's K2 launch: one O chunk, two dO chunks.
@@ -1719,12 +1744,35 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
     f(c, r * i * 2, "inter.mlp.hT");
     f(c, r * h * 2, "act.xT");
   };
+  // X_j / dX_j: rows of the caller's device tensors, or the streamed chunk buffers
+  auto xdev = [&](int j) -> const void* { return io ? io->xbuf[j & 1] : bptr(x, b[j] * h); };
+  auto dxdev = [&](int j) -> void* { return io ? io->dxbuf[j & 1] : const_cast<char*>(bptr(dx, b[j] * h)); };
+  auto h2d = [&](int j) -> int {  // X_j into buffer j & 1 once chunk j-2 has released it
+    MST_CUDA(cudaStreamWaitEvent(io->cs, io->x_free[j & 1], 0));
+    MST_CUDA(cudaMemcpyAsync(io->xbuf[j & 1], io->x_host + b[j] * h * 2, size_t(rows_of(j)) * h * 2,
+                             cudaMemcpyHostToDevice, io->cs));
+    MST_CUDA(cudaEventRecord(io->x_ready[j & 1], io->cs));
+    return MST_OK;
+  };
+  auto d2h = [&](int j) -> int {  // dX_j out once its GEMM has run
+    MST_CUDA(cudaEventRecord(io->dx_ready[j & 1], st));
+    MST_CUDA(cudaStreamWaitEvent(io->cs, io->dx_ready[j & 1], 0));
+    MST_CUDA(cudaMemcpyAsync(io->dx_host + b[j] * h * 2, io->dxbuf[j & 1], size_t(rows_of(j)) * h * 2,
+                             cudaMemcpyDeviceToHost, io->cs));
+    MST_CUDA(cudaEventRecord(io->dx_free[j & 1], io->cs));
+    return MST_OK;
+  };
+  if (io) {
+    MST_TRY(h2d(0));
+    if (nch > 1) MST_TRY(h2d(1));
+  }
   auto add_k1s = [&](Launch& L, int j) -> int {  // K1 saving G, U (fp32) and h (bf16)
     const int64_t rows = rows_of(j);
+    if (io) MST_CUDA(cudaStreamWaitEvent(st, io->x_ready[j & 1], 0));
     ProblemDesc& P = L.p.prob[L.p.num_problems++];
     P.nblk = (c->wide_mask & 32) ? 2 : 1;
     PhaseSpec s{};
-    s.a = {bptr(x, b[j] * h), rows, h, h, false};
+    s.a = {xdev(j), rows, h, h, false};
     s.b0 = {wg, i, h, i, true};
     s.b1 = {wu, i, h, i, true};
     s.umma_n = 256;
@@ -1751,7 +1799,8 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
     if (j == 0)
       for (int wi = 0; wi < 3; ++wi) grad_alloc(c, wi, (uint64_t)h * i * 4);
     const int beta = (j > 0 || accumulate) ? 1 : 0;
-    return add_mlp_grads(c, L, dg, du, ht, xt, dO[j & 1], wg, wu, const_cast<char*>(bptr(dx, b[j] * h)),
+    if (io) MST_CUDA(cudaStreamWaitEvent(st, io->dx_free[j & 1], 0));  // dX of chunk j-2 copied out
+    return add_mlp_grads(c, L, dg, du, ht, xt, dO[j & 1], wg, wu, dxdev(j),
                          dwg, dwu, dwd, rows, h, i, ldt, beta);
   };
   {
@@ -1771,6 +1820,7 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
       if (j > 0) MST_TRY(add_grads(L, j - 1));
       MST_TRY(launch(c, st, L));
       if (j > 0) grads_live(j - 1, false);
+      if (io && j > 0) MST_TRY(d2h(j - 1));
     }
     const uint64_t part_bytes = (uint64_t)rows * nparts * 8 + (uint64_t)rows * 8;
     if (j == 0) grad_alloc(c, 3, (uint64_t)h * v * 4);
@@ -1845,7 +1895,11 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
       mem_free(c, (uint64_t)rows * i * 4, "inter.mlp.dh");
     }
     MST_TRY(transpose_bf16(c, st, hb, i, ht, ldt, rows, i));
-    MST_TRY(transpose_bf16(c, st, bptr(x, r0 * h), h, xt, ldt, rows, h));
+    MST_TRY(transpose_bf16(c, st, xdev(j), h, xt, ldt, rows, h));
+    if (io) {  // last read of X_j: its buffer takes X_{j+2}
+      MST_CUDA(cudaEventRecord(io->x_free[j & 1], st));
+      if (j + 2 < nch) MST_TRY(h2d(j + 2));
+    }
     mlp_fwd_live(j, false);
     if (j + 1 < nch) {
       Launch L;
@@ -1858,6 +1912,11 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
     MST_TRY(add_grads(L, nch - 1));
     MST_TRY(launch(c, st, L));
     grads_live(nch - 1, false);
+    if (io) {  // the last dX chunk out, and the compute stream joins the copies
+      MST_TRY(d2h(nch - 1));
+      MST_CUDA(cudaEventRecord(io->done, io->cs));
+      MST_CUDA(cudaStreamWaitEvent(st, io->done, 0));
+    }
   }
   for (int wi = 0; wi < 3; ++wi) grad_ready(c, wi, st, (uint64_t)h * i * 4);  // dW_gate, dW_up, dW_down complete
   mem_free(c, (uint64_t)n * 4, "act.lse");
@@ -1867,6 +1926,48 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
   c->launches += 1;
   MST_CUDA(cudaGetLastError());
   return MST_OK;
+}
+
+int mst_ctx_block_host_workspace(const mst_ctx* c, int64_t n, int64_t h, int64_t i, int64_t v, int64_t m,
+                                 size_t* bytes) {
+  if (!c || !bytes) return fail(MST_ERR_STATE, "NULL context or output");
+  if (!uses_chunked_block(c, m, m))
+    return fail(MST_ERR_CONFIG, "host-resident X / dX need the chunk-wise schedule (tuning chunked_block=1, fused_head=1)");
+  MST_TRY(mst_ctx_block_workspace(c, n, h, i, v, m, m, bytes));
+  *bytes += host_io_bytes(n, h, m);
+  return MST_OK;
+}
+
+int mst_block_step_host(mst_ctx* c, void* stream, const void* x_host, const int32_t* labels_host, const void* wg,
+                        const void* wu, const void* wd, const void* wout, int64_t n, int64_t h, int64_t i, int64_t v,
+                        int64_t m, int loss_mode, float grad_loss, float* stats, void* dx_host, float* dwg, float* dwu,
+                        float* dwd, float* dwout, int accumulate, void* ws, size_t ws_bytes) {
+  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  size_t need = 0, dev_need = 0;
+  MST_TRY(mst_ctx_block_host_workspace(c, n, h, i, v, m, &need));
+  MST_TRY(mst_ctx_block_workspace(c, n, h, i, v, m, m, &dev_need));
+  if (!ws || ws_bytes < need) return fail(MST_ERR_CONFIG, "workspace too small (%zu < %zu)", ws_bytes, need);
+  if (loss_mode != MST_LOSS_TOKEN_WEIGHTED && loss_mode != MST_LOSS_PAPER_MEAN)
+    return fail(MST_ERR_CONFIG, "unknown loss mode %d", loss_mode);
+  if (!x_host || !labels_host || !wg || !wu || !wd || !wout || !stats || !dx_host || !dwg || !dwu || !dwd || !dwout)
+    return fail(MST_ERR_CONFIG, "NULL tensor pointer");
+  MST_TRY(check_dims(n, h, i, m, "I"));
+  MST_TRY(check_dims(n, h, v, m, "V"));
+  if (!c->copy_stream) {
+    MST_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    for (cudaEvent_t& e : c->io_ev) MST_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* io_base = static_cast<char*>(ws) + align_up(dev_need, 1024);
+  const size_t xcb = align_up(size_t(max_chunk(n, m)) * h * 2, 256);
+  HostIO io{static_cast<const char*>(x_host), static_cast<char*>(dx_host),
+            {io_base, io_base + xcb}, {io_base + 2 * xcb, io_base + 3 * xcb}, c->copy_stream,
+            {c->io_ev[0], c->io_ev[1]}, {c->io_ev[2], c->io_ev[3]}, {c->io_ev[4], c->io_ev[5]},
+            {c->io_ev[6], c->io_ev[7]}, c->io_ev[8]};
+  int32_t* labels_dev = reinterpret_cast<int32_t*>(io_base + 4 * xcb);
+  MST_CUDA(cudaMemcpyAsync(labels_dev, labels_host, size_t(n) * 4, cudaMemcpyHostToDevice, st));
+  return block_step_chunked(c, st, nullptr, labels_dev, wg, wu, wd, wout, n, h, i, v, m, loss_mode, grad_loss, stats,
+                            nullptr, dwg, dwu, dwd, dwout, accumulate, ws, dev_need, nullptr, &io);
 }
 
 int mst_block_step(mst_ctx* c, void* stream, const void* x, const int32_t* labels, const void* wg, const void* wu,

@@ -110,6 +110,10 @@ _SIGS = {
     "mst_block_workspace": ([_I64, _I64, _I64, _I64, _I64, _I64, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
     "mst_ctx_block_workspace": ([_VP, _I64, _I64, _I64, _I64, _I64, _I64, ctypes.POINTER(ctypes.c_size_t)],
                                 ctypes.c_int),
+    "mst_ctx_block_host_workspace": ([_VP, _I64, _I64, _I64, _I64, _I64, ctypes.POINTER(ctypes.c_size_t)],
+                                     ctypes.c_int),
+    "mst_block_step_host": ([_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _I64, _I64, _I64, _I32,
+                             ctypes.c_float, _VP, _VP, _VP, _VP, _VP, _VP, _I32, _VP, ctypes.c_size_t], ctypes.c_int),
     "mst_mlp_forward": ([_VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _I64, _I64, _VP, ctypes.c_size_t,
                          ctypes.POINTER(_MlpSaved)], ctypes.c_int),
     "mst_mlp_backward": ([_VP, _VP, _VP, ctypes.POINTER(_MlpSaved), _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I32,
@@ -667,6 +671,48 @@ def block_step(X: torch.Tensor, L: torch.Tensor, mlp: MlpWeights, head: LmHeadWe
             raise DataError("all labels ignored: loss undefined (SPEC.md:219)")
         check_finite(loss=stats[2:3], dX=grads.dX, dW_gate=grads.W_gate, dW_up=grads.W_up, dW_down=grads.W_down,
                      dW_out=grads.W_out)
+    return stats, grads
+
+
+def block_step_host(X: torch.Tensor, L: torch.Tensor, mlp: MlpWeights, head: LmHeadWeights, M: int,
+                    dX: torch.Tensor, grads: Optional[BlockGrads] = None, stats: Optional[torch.Tensor] = None,
+                    mode: int = TOKEN_WEIGHTED, grad_loss: float = 1.0, accumulate: bool = False,
+                    workspace: Optional[torch.Tensor] = None):
+    """block_step with host-resident X, labels and dX (mst_block_step_host):
+    X / L are pinned CPU tensors, dX a pinned CPU bf16 output; the chunks are
+    streamed in and out on a copy stream while the GEMMs run.  Weights and
+    the fp32 weight gradients (grads.W_*) live on the device.  Returns
+    (stats, grads); dX is filled once the current stream is synchronised."""
+    dev = mlp.W_gate.device
+    ctx = Context.get(dev.index)
+    N, H = X.shape
+    I = mlp.W_gate.shape[1]
+    V = head.W_out.shape[1]
+    for t, name, dt, shape in ((X, "X", torch.bfloat16, (N, H)), (L, "L", torch.int32, (N,)),
+                               (dX, "dX", torch.bfloat16, (N, H))):
+        if not isinstance(t, torch.Tensor) or t.device.type != "cpu":
+            raise ConfigError(f"{name} must be a host (CPU) tensor, pinned for overlapped copies")
+        if t.dtype != dt:
+            raise DtypeError(f"{name} must be {dt}, got {t.dtype}")
+        if tuple(t.shape) != shape:
+            raise ShapeError(f"{name} must have shape {shape}, got {tuple(t.shape)}")
+        if not t.is_contiguous():
+            raise ConfigError(f"{name} must be contiguous")
+    if grads is None:
+        grads = BlockGrads(dX, *(torch.empty(*s, dtype=torch.float32, device=dev) for s in ((H, I), (H, I), (I, H),
+                                                                                          (H, V))))
+    nch = min(N, M)
+    if stats is None:
+        stats = torch.empty(stats_len(nch), dtype=torch.float32, device=dev)
+    nb = ctypes.c_size_t()
+    _check(ctx.lib.mst_ctx_block_host_workspace(ctx.handle, N, H, I, V, M, ctypes.byref(nb)))
+    ws = workspace if workspace is not None else ctx.workspace(nb.value)
+    _check(ctx.lib.mst_block_step_host(ctx.handle, _stream(mlp.W_gate), X.data_ptr(), L.data_ptr(),
+                                       mlp.W_gate.data_ptr(), mlp.W_up.data_ptr(), mlp.W_down.data_ptr(),
+                                       head.W_out.data_ptr(), N, H, I, V, M, mode, grad_loss, stats.data_ptr(),
+                                       dX.data_ptr(), grads.W_gate.data_ptr(), grads.W_up.data_ptr(),
+                                       grads.W_down.data_ptr(), grads.W_out.data_ptr(), int(accumulate),
+                                       ws.data_ptr(), ws.numel()))
     return stats, grads
 
 

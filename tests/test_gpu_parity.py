@@ -439,3 +439,28 @@ def test_tile_scheduler_back_to_back_launches():
         assert torch.equal(a, b)
     for (A, B, M, N, K), out in zip(data, outs[1]):
         assert rel(out, (A.double() @ B.double()).cpu().numpy()) <= 1e-5
+
+
+@pytest.mark.parametrize("shape", [(1024, 256, 688, 4096, 4), (777, 512, 136, 520, 3), (300, 64, 136, 520, 1),
+                                   (2048, 1024, 2816, 32000, 8)])
+def test_block_step_host_streams_bitwise_equal(shape):
+    """mst_block_step_host (X / labels / dX in pinned host memory, chunks
+    streamed on a copy stream) == mst_block_step on device tensors, bitwise,
+    including back-to-back calls that reuse the chunk buffers and events."""
+    N, H, I, V, M = shape
+    torch.manual_seed(3)
+    X = torch.randn(N, H, device="cuda").bfloat16()
+    W = [(0.05 * torch.randn(*s, device="cuda")).bfloat16() for s in ((H, I), (H, I), (I, H), (H, V))]
+    L = torch.randint(0, V, (N,), device="cuda", dtype=torch.int32)
+    L[::11] = -100
+    mlp, head = ms.MlpWeights(*W[:3]), ms.LmHeadWeights(W[3])
+    st, gr = ms.block_step(X, L, mlp, head, M, M)
+    Xh, Lh = X.cpu().pin_memory(), L.cpu().pin_memory()
+    for rep in range(2):
+        dXh = torch.full((N, H), float("nan"), dtype=torch.bfloat16).pin_memory()
+        sth, grh = ms.block_step_host(Xh, Lh, mlp, head, M, dXh)
+        torch.cuda.synchronize()
+        assert torch.equal(sth[:3], st[:3])
+        assert torch.equal(dXh, gr.dX.cpu())
+        for a, b in ((grh.W_gate, gr.W_gate), (grh.W_up, gr.W_up), (grh.W_down, gr.W_down), (grh.W_out, gr.W_out)):
+            assert torch.equal(a, b)
