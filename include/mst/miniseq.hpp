@@ -182,6 +182,44 @@ inline void miniseq_lmhead_backward(Context& ctx, void* stream, const mst_lmhead
                                accumulate ? 1 : 0, ws.data, ws.bytes));
 }
 
+// The MLP -> LM-Head block, forward + backward in one call (the unit the
+// paper times; cmd_sweep_m / cmd_max_seq SPEC.md:728-754).
+// Device tensors; `stats` receives the loss in [2].  M_mlp == M_head runs
+// the chunk-wise schedule (one O chunk, two dO chunks on the device).
+struct BlockGrads {
+  void* dX;  // [N, d] bf16
+  float *W_gate, *W_up, *W_down, *W_out;
+};
+inline size_t block_workspace_bytes(const Context& ctx, int64_t N, const MlpWeights& m, const LmHeadWeights& h,
+                                    int64_t M_mlp, int64_t M_head) {
+  size_t b = 0;
+  throw_on(mst_ctx_block_workspace(ctx.get(), N, m.d, m.I, h.V, M_mlp, M_head, &b));
+  return b;
+}
+inline void block_step(Context& ctx, void* stream, const void* X, const int32_t* L, int64_t N, const MlpWeights& m,
+                       const LmHeadWeights& h, int64_t M_mlp, int64_t M_head, LossMode mode, float grad_loss,
+                       float* stats, BlockGrads g, bool accumulate, Workspace ws) {
+  throw_on(mst_block_step(ctx.get(), stream, X, L, m.W_gate, m.W_up, m.W_down, h.W_out, N, m.d, m.I, h.V, M_mlp,
+                          M_head, static_cast<int>(mode), grad_loss, stats, g.dX, g.W_gate, g.W_up, g.W_down, g.W_out,
+                          accumulate ? 1 : 0, ws.data, ws.bytes));
+}
+// Same with X, L and dX in (pinned) host memory, streamed per chunk under the
+// GEMMs (mst_block_step_host): the sequence lives in host memory.
+inline size_t block_host_workspace_bytes(const Context& ctx, int64_t N, const MlpWeights& m, const LmHeadWeights& h,
+                                         int64_t M) {
+  size_t b = 0;
+  throw_on(mst_ctx_block_host_workspace(ctx.get(), N, m.d, m.I, h.V, M, &b));
+  return b;
+}
+inline void block_step_host(Context& ctx, void* stream, const void* X_host, const int32_t* L_host, int64_t N,
+                            const MlpWeights& m, const LmHeadWeights& h, int64_t M, LossMode mode, float grad_loss,
+                            float* stats, BlockGrads g_dX_host, bool accumulate, Workspace ws) {
+  throw_on(mst_block_step_host(ctx.get(), stream, X_host, L_host, m.W_gate, m.W_up, m.W_down, h.W_out, N, m.d, m.I,
+                               h.V, M, static_cast<int>(mode), grad_loss, stats, g_dX_host.dX, g_dX_host.W_gate,
+                               g_dX_host.W_up, g_dX_host.W_down, g_dX_host.W_out, accumulate ? 1 : 0, ws.data,
+                               ws.bytes));
+}
+
 // Op counters of the context (memtrack.hpp:19-35 conventions; mst.h "memtrack").
 inline mst_counters counters(const Context& ctx) {
   mst_counters c{};

@@ -43,6 +43,11 @@ int main() {
     threw = true;
   }
   expect(threw, "bad range -> BoundsError");
+  // the block-level wrappers bind to the ABI (compile-time: no device here)
+  (void)&mst::block_step;
+  (void)&mst::block_step_host;
+  (void)&mst::block_workspace_bytes;
+  (void)&mst::block_host_workspace_bytes;
 #ifdef MST_HAVE_MINITRAIN_MEMTRACK
   // hooks forwarding into minitrain::MemTracker::current() exist and have the ABI's types
   mst_mem_hook mh = &mst::detail::mem_to_minitrain;
