@@ -375,7 +375,11 @@ static void head_fwd_rows(const double* X, const int32_t* L, const double* Wout,
   tfree(Z, n * V, ORC_MEM_INTER_HEAD);
 }
 
-/* Per-chunk backward: dl = (exp(z - lse) - onehot) * scale. */
+/* Per-chunk backward: dl = (exp(z - lse) - onehot) * scale.
+ * round == 2 additionally replays the GPU single-pass head's rounding
+ * (mst_lmhead_fused / block_step): the softmax numerator
+ * exp(z - m_tile) relative to its 256-column vocabulary tile's maximum is
+ * stored in bf16 first; the label column is computed from the fp32 logit. */
 static void head_bwd_rows(const double* X, const int32_t* L, const double* Wout, int64_t n, int64_t H, int64_t V,
                           const double* lse, double scale, double* dX, double* cWout, int round) {
   double* Z = talloc(n * V, ORC_MEM_INTER_HEAD);
@@ -385,9 +389,18 @@ static void head_bwd_rows(const double* X, const int32_t* L, const double* Wout,
     double* z = Z + r * V;
     const int32_t lab = L[r];
     const int valid = lab >= 0 && lab < V;
-    for (int64_t v = 0; v < V; ++v) {
-      const double p = exp(z[v] - lse[r]);
-      z[v] = valid ? rb((p - (v == lab ? 1.0 : 0.0)) * scale, round) : 0.0;
+    for (int64_t t0 = 0; t0 < V; t0 += 256) {
+      const int64_t t1 = t0 + 256 < V ? t0 + 256 : V;
+      double mt = -INFINITY;
+      for (int64_t v = t0; v < t1; ++v) mt = z[v] > mt ? z[v] : mt;
+      for (int64_t v = t0; v < t1; ++v) {
+        double p;
+        if (round == 2 && v != lab)
+          p = rb(exp(z[v] - mt), 1) * exp(mt - lse[r]);
+        else
+          p = exp(z[v] - lse[r]);
+        z[v] = valid ? rb((p - (v == lab ? 1.0 : 0.0)) * scale, round) : 0.0;
+      }
     }
   }
   count_op(5ull * n * V, (uint64_t)(2 * n * V + 2 * n));

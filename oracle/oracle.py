@@ -295,12 +295,15 @@ def miniseq_lmhead_backward(X, L, Wout, M, mode=0, grad_loss=1.0, round_bf16=Fal
     return dX, dW
 
 
-def block(X, L, Wg, Wu, Wd, Wout, M_mlp, M_head, round_bf16=True, grad_loss=1.0):
+def block(X, L, Wg, Wu, Wd, Wout, M_mlp, M_head, round_bf16=True, grad_loss=1.0, single_pass=False):
     """MLP -> LM-Head block fwd+bwd in f64 (the GPU block_step's checker).
-    With round_bf16 the intermediates libmst stores in bf16 are rounded here too."""
+    With round_bf16 the intermediates libmst stores in bf16 are rounded here
+    too; single_pass additionally replays the single-pass head's bf16
+    softmax numerators (block_step's default head)."""
     O = miniseq_mlp_forward(X, Wg, Wu, Wd, M_mlp, round_bf16)
     loss, lse, _, _ = miniseq_lmhead_forward(O, L, Wout, M_head)
-    dO, dWout = miniseq_lmhead_backward(O, L, Wout, M_head, 0, grad_loss, round_bf16)
+    rnd = (2 if single_pass else 1) if round_bf16 else 0
+    dO, dWout = miniseq_lmhead_backward(O, L, Wout, M_head, 0, grad_loss, rnd)
     dX, dWg, dWu, dWd = miniseq_mlp_backward(dO, X, Wg, Wu, Wd, M_mlp, round_bf16)
     return dict(O=O, loss=loss, lse=lse, dO=dO, dWout=dWout, dX=dX, dWg=dWg, dWu=dWu, dWd=dWd)
 

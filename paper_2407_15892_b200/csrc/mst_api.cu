@@ -126,7 +126,7 @@ struct mst_ctx {
   int debug_nblk = 1;     // N blocks per tile of mst_debug_gemm
   // mst_block_step_host: copy stream and chunk events (created on first use)
   cudaStream_t copy_stream = nullptr;
-  cudaEvent_t io_ev[9] = {};
+  cudaEvent_t io_ev[10] = {};
   // memtrack side (mst.h): counters per memtrack.hpp:19-35, event hooks
   mst_counters ctr{};
   mst_mem_hook mem_fn = nullptr;
@@ -136,12 +136,43 @@ struct mst_ctx {
   const void* weights[4] = {nullptr, nullptr, nullptr, nullptr};  // weight tensors of the current call
   mst_grad_ready_hook ready_fn = nullptr;  // optimizer-in-backward hook (mst.h)
   void* ready_user = nullptr;
+  int tma3d = 1;  // MN-major operands as 3-D tensor maps (tuning "tma3d")
+  // Cross-stream ordering of the context's device scratch (tile counter,
+  // global-valid / count scratch): calls are serialised by `mu`, and a call
+  // on a different stream than the previous one waits for `tail_ev`, which
+  // every call records on its stream when it returns (mst.h "Threading").
+  std::recursive_mutex mu;
+  cudaStream_t last_stream = nullptr;
+  bool has_last = false;
+  cudaEvent_t tail_ev = nullptr;
 };
 
 namespace {
 
-// MN-major operands as 3-D tensor maps (one TMA per slab); tuning knob "tma3d".
-bool c3d_enabled = true;
+// One public call on a context: holds the context lock for the call and
+// orders the call after the previous call's work when the stream changes
+// (the scratch is per context, the stream per call).
+struct CtxCall {
+  mst_ctx* c;
+  cudaStream_t st;
+  std::lock_guard<std::recursive_mutex> lk;
+  int status = MST_OK;
+  CtxCall(mst_ctx* ctx, void* stream) : c(ctx), st(static_cast<cudaStream_t>(stream)), lk(ctx->mu) {
+    if (c->has_last && c->last_stream != st && c->tail_ev) {
+      if (cudaStreamWaitEvent(st, c->tail_ev, 0) != cudaSuccess) status = MST_ERR_CUDA;
+    }
+  }
+  ~CtxCall() {
+    if (!c->tail_ev) cudaEventCreateWithFlags(&c->tail_ev, cudaEventDisableTiming);
+    if (c->tail_ev) cudaEventRecord(c->tail_ev, st);
+    c->last_stream = st;
+    c->has_last = true;
+  }
+};
+#define MST_CALL(ctx, stream)                                                              \
+  if (!(ctx)) return fail(MST_ERR_STATE, "NULL context");                                 \
+  CtxCall call_guard_(ctx, stream);                                                        \
+  if (call_guard_.status != MST_OK) return fail(MST_ERR_CUDA, "cross-stream ordering failed")
 
 // ------------------------------------------------------------ memtrack side
 // count_matmul / count_op of memtrack.hpp:163-175 (conventions at :19-35).
@@ -258,15 +289,15 @@ struct Launch {
   Launch() { std::memset(&p, 0, sizeof(p)); }
 };
 
-bool use_3d(const Operand& o, int box_mn) {
-  return o.mn_major && c3d_enabled && o.mn % 64 == 0 && box_mn % 64 == 0 && (reinterpret_cast<uintptr_t>(o.base) & 127) == 0;
+bool use_3d(const mst_ctx* c, const Operand& o, int box_mn) {
+  return o.mn_major && c->tma3d && o.mn % 64 == 0 && box_mn % 64 == 0 && (reinterpret_cast<uintptr_t>(o.base) & 127) == 0;
 }
 
 int add_map(mst_ctx* c, Launch& L, const Operand& o, int box_mn) {
   if (L.nmaps >= mst::kMaxMaps) return fail(MST_ERR_INTERNAL, "too many tensor maps in one launch");
   CUtensorMap* m = &L.p.maps[L.nmaps];
   int s = !o.mn_major      ? tmap_2d(c, m, o.base, o.k, o.mn, o.ld, 64, box_mn)
-          : use_3d(o, box_mn) ? tmap_3d_mn(c, m, o.base, o.mn, o.k, o.ld, box_mn / 64)
+          : use_3d(c, o, box_mn) ? tmap_3d_mn(c, m, o.base, o.mn, o.k, o.ld, box_mn / 64)
                               : tmap_2d(c, m, o.base, o.mn, o.k, o.ld, 64, 64);
   if (s != MST_OK) return s;
   return -(L.nmaps++) - 100;  // encoded index (negative to distinguish from status)
@@ -316,8 +347,8 @@ int add_phase(mst_ctx* c, Launch& L, ProblemDesc& P, const PhaseSpec& s) {
   d.map_b1 = map_index(eb1);
   d.a_mn = s.a.mn_major ? 1 : 0;
   d.b_mn = s.b0.mn_major ? 1 : 0;
-  d.a_3d = use_3d(s.a, 128) ? 1 : 0;
-  d.b_3d = (use_3d(s.b0, nh) && use_3d(s.b1, nh)) ? 1 : 0;
+  d.a_3d = use_3d(c, s.a, 128) ? 1 : 0;
+  d.b_3d = (use_3d(c, s.b0, nh) && use_3d(c, s.b1, nh)) ? 1 : 0;
   d.umma_n = s.umma_n;
   d.tmem_col = s.tmem_col;
   d.k_start = s.k_start;
@@ -688,9 +719,14 @@ __global__ void sum_valid_kernel(float* stats, int m) {
 
 // In place: e (bf16 softmax numerator, tile max m_tile in part[].x) ->
 // dlogits = (e * 2^(m_tile - lse*log2e) - [v == label]) * scale, bf16.
+// The label column is recomputed from the fp32 target logit instead:
+// (exp(z_label - lse) - 1) * scale, so a confident row (p_label -> 1) keeps
+// the relative precision of 1 - p_label (e's bf16 rounding would leave an
+// absolute error of ~2^-9 on a value that can be far smaller).
 __global__ void normalize_dlogits_kernel(uint16_t* __restrict__ dl, int64_t ld, int rows, int cols,
                                          const float2* __restrict__ part, int nparts, const float* __restrict__ lse,
-                                         const int32_t* __restrict__ labels, const float* __restrict__ scale) {
+                                         const int32_t* __restrict__ labels, const float* __restrict__ scale,
+                                         const float* __restrict__ ztarget) {
   const int64_t per_row = cols / 8;
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t r = idx / per_row;
@@ -709,6 +745,12 @@ __global__ void normalize_dlogits_kernel(uint16_t* __restrict__ dl, int64_t ld, 
     const float d1 = (e1 * f - (c + 2 * k + 1 == lab ? 1.f : 0.f)) * sc;
     u[k] = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(d0)) |
            ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(d1)) << 16);
+  }
+  if (lab >= c && lab < c + 8) {
+    const float d = (exp2f((ztarget[r] - lse[r]) * 1.4426950408889634f) - 1.f) * sc;
+    const int k = lab - c;
+    const uint32_t b = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(d));
+    u[k >> 1] = (k & 1) ? ((u[k >> 1] & 0x0000ffffu) | (b << 16)) : ((u[k >> 1] & 0xffff0000u) | b);
   }
   *p = w;
 }
@@ -967,6 +1009,7 @@ void mst_ctx_destroy(mst_ctx* c) {
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   for (cudaEvent_t e : c->io_ev)
     if (e) cudaEventDestroy(e);
+  if (c->tail_ev) cudaEventDestroy(c->tail_ev);
   delete c;
 }
 
@@ -1043,7 +1086,7 @@ int mst_ctx_set_tuning(mst_ctx* c, const char* key, int value) {
     if (value < 1 || value > c->max_pairs) return fail(MST_ERR_CONFIG, "pairs must be 1..%d", c->max_pairs);
     c->num_pairs = value;
   } else if (std::strcmp(key, "tma3d") == 0) {
-    c3d_enabled = value != 0;
+    c->tma3d = value != 0;
   } else {
     return fail(MST_ERR_CONFIG, "unknown tuning key '%s'", key);
   }
@@ -1080,7 +1123,7 @@ int mst_ctx_set_grad_ready_hook(mst_ctx* c, mst_grad_ready_hook fn, void* user) 
 // ------------------------------------------------------------ optimizer (optim.cu)
 int mst_adamw_step(mst_ctx* c, void* stream, int64_t n, float* w, void* w_bf16, float* grad, float* m, float* v,
                    const mst_adamw_config* cfg, int64_t step, const float* grad_scale, int zero_grad) {
-  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  MST_CALL(c, stream);
   if (!cfg) return fail(MST_ERR_CONFIG, "NULL AdamW config");
   if (n < 0) return fail(MST_ERR_SHAPE, "negative parameter count");
   if (!w || !w_bf16 || !grad || !m || !v) return fail(MST_ERR_CONFIG, "NULL tensor pointer");
@@ -1102,7 +1145,7 @@ int mst_grad_sumsq_workspace(void) { return mst_optim::kSumsqBlocks; }
 
 int mst_grad_sumsq(mst_ctx* c, void* stream, const float* grad, int64_t n, double* partial_ws, double* sumsq,
                    int accumulate, float max_norm, float inv_steps, float* scale_out, float* norm_out) {
-  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  MST_CALL(c, stream);
   if (!grad || !partial_ws || !sumsq) return fail(MST_ERR_CONFIG, "NULL pointer");
   if (n < 0) return fail(MST_ERR_SHAPE, "negative element count");
   if (!mst_optim::aligned16(grad)) return fail(MST_ERR_CONFIG, "gradient must be 16-byte aligned");
@@ -1114,7 +1157,7 @@ int mst_grad_sumsq(mst_ctx* c, void* stream, const float* grad, int64_t n, doubl
 }
 
 int mst_grad_accumulate(mst_ctx* c, void* stream, float* into, const float* from, int64_t n) {
-  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  MST_CALL(c, stream);
   if (!into || !from) return fail(MST_ERR_CONFIG, "NULL pointer");
   if (n < 0) return fail(MST_ERR_SHAPE, "negative element count");
   if (!mst_optim::aligned16(into) || !mst_optim::aligned16(from))
@@ -1246,7 +1289,7 @@ static uint64_t head_fp(const mst_lmhead_saved* s) {
 
 int mst_mlp_forward(mst_ctx* c, void* stream, const void* x, const void* wg, const void* wu, const void* wd, void* out,
                     int64_t n, int64_t h, int64_t i, int64_t m, void* ws, size_t ws_bytes, mst_mlp_saved* saved) {
-  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  MST_CALL(c, stream);
   MST_TRY(check_dims(n, h, i, m, "I"));
   if (!x || !wg || !wu || !wd || !out) return fail(MST_ERR_CONFIG, "NULL tensor pointer");
   size_t need = 0;
@@ -1299,7 +1342,7 @@ int mst_mlp_forward(mst_ctx* c, void* stream, const void* x, const void* wg, con
 int mst_mlp_backward(mst_ctx* c, void* stream, const void* dout, const mst_mlp_saved* s, const void* wg, const void* wu,
                      const void* wd, void* dx, float* dwg, float* dwu, float* dwd, int accumulate, void* ws,
                      size_t ws_bytes) {
-  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  MST_CALL(c, stream);
   if (!s || s->fingerprint != mlp_fp(s)) return fail(MST_ERR_STATE, "stale or corrupted MLP saved state (SPEC.md:308)");
   if (s->w_gate != wg || s->w_up != wu || s->w_down != wd)
     return fail(MST_ERR_STATE, "MLP saved state was produced with different weights");
@@ -1390,7 +1433,7 @@ int mst_mlp_backward(mst_ctx* c, void* stream, const void* dout, const mst_mlp_s
 int mst_lmhead_forward(mst_ctx* c, void* stream, const void* x, const int32_t* labels, const void* wout, int64_t n,
                        int64_t h, int64_t v, int64_t m, int loss_mode, float* stats, float* lse, void* ws,
                        size_t ws_bytes, mst_lmhead_saved* saved) {
-  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  MST_CALL(c, stream);
   MST_TRY(check_dims(n, h, v, m, "V"));
   if (loss_mode != MST_LOSS_TOKEN_WEIGHTED && loss_mode != MST_LOSS_PAPER_MEAN)
     return fail(MST_ERR_CONFIG, "unknown loss mode %d", loss_mode);
@@ -1454,7 +1497,7 @@ int mst_lmhead_forward(mst_ctx* c, void* stream, const void* x, const int32_t* l
 int mst_lmhead_backward(mst_ctx* c, void* stream, const mst_lmhead_saved* s, const void* wout,
                         const float* global_stats, float grad_loss, void* dx, float* dwout, int accumulate, void* ws,
                         size_t ws_bytes) {
-  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  MST_CALL(c, stream);
   if (!s || s->fingerprint != head_fp(s)) return fail(MST_ERR_STATE, "stale or corrupted LM-Head saved state (SPEC.md:308)");
   if (s->w_out != wout) return fail(MST_ERR_STATE, "LM-Head saved state was produced with different weights");
   if (!dx || !dwout) return fail(MST_ERR_CONFIG, "NULL tensor pointer");
@@ -1511,7 +1554,7 @@ int mst_lmhead_backward(mst_ctx* c, void* stream, const mst_lmhead_saved* s, con
 int mst_lmhead_fused(mst_ctx* c, void* stream, const void* x, const int32_t* labels, const void* wout, int64_t n,
                      int64_t h, int64_t v, int64_t m, int loss_mode, float grad_loss, const float* global_valid,
                      float* stats, float* lse, void* dx, float* dwout, int accumulate, void* ws, size_t ws_bytes) {
-  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  MST_CALL(c, stream);
   MST_TRY(check_dims(n, h, v, m, "V"));
   if (loss_mode != MST_LOSS_TOKEN_WEIGHTED && loss_mode != MST_LOSS_PAPER_MEAN)
     return fail(MST_ERR_CONFIG, "unknown loss mode %d", loss_mode);
@@ -1571,7 +1614,7 @@ int mst_lmhead_fused(mst_ctx* c, void* stream, const void* x, const int32_t* lab
     chunk_reduce_kernel<<<1, 1024, 0, st>>>(lrow, labels + r0, (int)rows, (int)v, stats + 4 + j,
                                             stats + 4 + nch + j);
     normalize_dlogits_kernel<<<(unsigned)cdiv(rows * (v / 8), 256), 256, 0, st>>>(
-        static_cast<uint16_t*>(dl), v, (int)rows, (int)v, part, nparts, lse + r0, labels + r0, scales + j);
+        static_cast<uint16_t*>(dl), v, (int)rows, (int)v, part, nparts, lse + r0, labels + r0, scales + j, zt);
     c->launches += 3;
     {  // K5 (dX = dl W_out^T) + K6 (dW_out += X^T dl), grouped.
       Launch L;
@@ -1625,7 +1668,7 @@ __global__ void __launch_bounds__(256) nonfinite_count_kernel(const uint8_t* hea
 }
 
 int mst_count_nonfinite(mst_ctx* c, void* stream, const void* data, int64_t n, int dtype, unsigned int* count) {
-  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  MST_CALL(c, stream);
   if (!data || !count) return fail(MST_ERR_CONFIG, "NULL pointer");
   if (n < 0) return fail(MST_ERR_SHAPE, "negative element count");
   if (dtype != MST_DTYPE_BF16 && dtype != MST_DTYPE_F32) return fail(MST_ERR_DTYPE, "dtype must be bf16 or f32");
@@ -1647,7 +1690,7 @@ int mst_count_nonfinite(mst_ctx* c, void* stream, const void* data, int64_t n, i
 }
 
 int mst_count_valid(mst_ctx* c, void* stream, const int32_t* labels, int64_t n, int64_t v, float* out) {
-  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  MST_CALL(c, stream);
   if (!labels || !out) return fail(MST_ERR_CONFIG, "NULL pointer");
   if (n <= 0) return fail(MST_ERR_DATA, "N must be >= 1");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1845,7 +1888,7 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
                                                                      lse + r0, lrow, stats + 3);
     chunk_reduce_kernel<<<1, 1024, 0, st>>>(lrow, labels + r0, (int)rows, (int)v, stats + 4 + j, stats + 4 + nch + j);
     normalize_dlogits_kernel<<<(unsigned)cdiv(rows * (v / 8), 256), 256, 0, st>>>(
-        static_cast<uint16_t*>(dl), v, (int)rows, (int)v, part, nparts, lse + r0, labels + r0, scales + j);
+        static_cast<uint16_t*>(dl), v, (int)rows, (int)v, part, nparts, lse + r0, labels + r0, scales + j, zt);
     c->launches += 3;
     {  // K5 + K6
       Launch L;
@@ -1942,7 +1985,7 @@ int mst_block_step_host(mst_ctx* c, void* stream, const void* x_host, const int3
                         const void* wu, const void* wd, const void* wout, int64_t n, int64_t h, int64_t i, int64_t v,
                         int64_t m, int loss_mode, float grad_loss, float* stats, void* dx_host, float* dwg, float* dwu,
                         float* dwd, float* dwout, int accumulate, void* ws, size_t ws_bytes) {
-  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  MST_CALL(c, stream);
   size_t need = 0, dev_need = 0;
   MST_TRY(mst_ctx_block_host_workspace(c, n, h, i, v, m, &need));
   MST_TRY(mst_ctx_block_workspace(c, n, h, i, v, m, m, &dev_need));
@@ -1965,6 +2008,11 @@ int mst_block_step_host(mst_ctx* c, void* stream, const void* x_host, const int3
             {c->io_ev[0], c->io_ev[1]}, {c->io_ev[2], c->io_ev[3]}, {c->io_ev[4], c->io_ev[5]},
             {c->io_ev[6], c->io_ev[7]}, c->io_ev[8]};
   int32_t* labels_dev = reinterpret_cast<int32_t*>(io_base + 4 * xcb);
+  // The copy stream writes into workspace chunk buffers: it first waits for
+  // everything already queued on the compute stream (an earlier op that used
+  // the same workspace region, or a recycled allocator block).
+  MST_CUDA(cudaEventRecord(c->io_ev[9], st));
+  MST_CUDA(cudaStreamWaitEvent(c->copy_stream, c->io_ev[9], 0));
   MST_CUDA(cudaMemcpyAsync(labels_dev, labels_host, size_t(n) * 4, cudaMemcpyHostToDevice, st));
   return block_step_chunked(c, st, nullptr, labels_dev, wg, wu, wd, wout, n, h, i, v, m, loss_mode, grad_loss, stats,
                             nullptr, dwg, dwu, dwd, dwout, accumulate, ws, dev_need, nullptr, &io);
@@ -1982,7 +2030,7 @@ int mst_block_step_sp(mst_ctx* c, void* stream, const void* x, const int32_t* la
                       const void* wd, const void* wout, int64_t n, int64_t h, int64_t i, int64_t v, int64_t m_mlp,
                       int64_t m_head, int loss_mode, float grad_loss, float* stats, void* dx, float* dwg, float* dwu,
                       float* dwd, float* dwout, int accumulate, void* ws, size_t ws_bytes, const float* global_valid) {
-  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  MST_CALL(c, stream);
   size_t need = 0;
   MST_TRY(mst_ctx_block_workspace(c, n, h, i, v, m_mlp, m_head, &need));
   if (!ws || ws_bytes < need) return fail(MST_ERR_CONFIG, "workspace too small (%zu < %zu)", ws_bytes, need);
@@ -2037,7 +2085,7 @@ static int check_rows(int64_t n, int64_t d) {
 
 int mst_rmsnorm_forward(mst_ctx* c, void* stream, const void* x, const void* residual, const float* gain, void* y,
                         void* sum_out, float* rstd, int64_t n, int64_t d, float eps) {
-  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  MST_CALL(c, stream);
   MST_TRY(check_rows(n, d));
   if (!x || !gain || !y || !rstd || (residual && !sum_out)) return fail(MST_ERR_CONFIG, "NULL tensor pointer");
   if (!(eps > 0.f)) return fail(MST_ERR_CONFIG, "eps must be > 0");
@@ -2059,7 +2107,7 @@ int mst_rmsnorm_workspace(const mst_ctx* c, int64_t n, int64_t d, size_t* bytes)
 int mst_rmsnorm_backward(mst_ctx* c, void* stream, const void* s, const float* gain, const float* rstd, const void* dy,
                          const void* dres, void* dx, float* dgain, int accumulate, int64_t n, int64_t d, void* ws,
                          size_t ws_bytes) {
-  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  MST_CALL(c, stream);
   MST_TRY(check_rows(n, d));
   if (!s || !gain || !rstd || !dy || !dx || !dgain) return fail(MST_ERR_CONFIG, "NULL tensor pointer");
   if (d > 6144) return fail(MST_ERR_BOUNDS, "rmsnorm backward supports d <= 6144 (per-warp dgain rows in smem)");
@@ -2075,7 +2123,7 @@ int mst_rmsnorm_backward(mst_ctx* c, void* stream, const void* s, const float* g
 
 int mst_embedding_forward(mst_ctx* c, void* stream, const void* table, const int32_t* tokens, void* out, int64_t n,
                           int64_t d, int64_t vocab, int* bad_count) {
-  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  MST_CALL(c, stream);
   MST_TRY(check_rows(n, d));
   if (vocab <= 0) return fail(MST_ERR_SHAPE, "vocabulary must be >= 1");
   if (!table || !tokens || !out || !bad_count) return fail(MST_ERR_CONFIG, "NULL pointer");
@@ -2089,7 +2137,7 @@ int mst_embedding_forward(mst_ctx* c, void* stream, const void* table, const int
 
 int mst_embedding_backward(mst_ctx* c, void* stream, const int32_t* order, const int32_t* seg, const int32_t* uniq,
                            int64_t nseg, const void* dx, float* dtable, int64_t d, int64_t vocab, int accumulate) {
-  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  MST_CALL(c, stream);
   if (d <= 0 || d % 8 || vocab <= 0 || nseg < 0) return fail(MST_ERR_SHAPE, "bad embedding extents");
   if (nseg > 0 && (!order || !seg || !uniq || !dx)) return fail(MST_ERR_CONFIG, "NULL pointer");
   if (!dtable) return fail(MST_ERR_CONFIG, "NULL gradient table");
@@ -2102,7 +2150,7 @@ int mst_embedding_backward(mst_ctx* c, void* stream, const int32_t* order, const
 
 int mst_debug_gemm(mst_ctx* c, void* stream, const void* a, const void* b, void* out, int64_t m, int64_t n, int64_t k,
                    int a_mn, int b_mn, int out_f32, int beta) {
-  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  MST_CALL(c, stream);
   if (m <= 0 || n <= 0 || k <= 0) return fail(MST_ERR_SHAPE, "extents must be positive");
   if (m % 8 || n % 8 || k % 8) return fail(MST_ERR_SHAPE, "extents must be multiples of 8");
   if (beta && !out_f32) return fail(MST_ERR_CONFIG, "accumulation (beta = 1) needs the fp32 output");

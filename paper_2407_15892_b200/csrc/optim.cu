@@ -111,8 +111,9 @@ __global__ void __launch_bounds__(kThreads) sumsq_kernel(const float* __restrict
 }
 
 // Fixed-order sum of the partials into *sumsq (accumulate != 0 adds to it),
-// then the clip factor: scale = max_norm / ||g|| if the
-// norm exceeds max_norm, else 1; times 1 / accumulation steps.  A
+// then the clip factor of the averaged gradient g/steps:
+// scale = max_norm / ||g/steps|| if that norm exceeds max_norm, else 1;
+// times 1 / accumulation steps (the average itself).  A
 // non-finite norm propagates NaN into the scale (the host raises
 // NonFiniteError when it checks).
 __global__ void sumsq_finish_kernel(const double* __restrict__ partial, int nparts, double* sumsq, int accumulate,
@@ -122,7 +123,9 @@ __global__ void sumsq_finish_kernel(const double* __restrict__ partial, int npar
   for (int i = 0; i < nparts; ++i) s += partial[i];
   *sumsq = s;
   if (scale_out) {
-    const double norm = sqrt(s);
+    // SPEC.md:500-506 then 486-491: the accumulated sum is divided by the
+    // step count first, and the clip applies to the norm of that average.
+    const double norm = sqrt(s) * (double)inv_steps;
     if (norm_out) *norm_out = (float)norm;
     double sc = (max_norm > 0.f && norm > (double)max_norm) ? (double)max_norm / norm : 1.0;
     if (!isfinite(norm)) sc = NAN;

@@ -180,9 +180,12 @@ def accumulate(into: Dict[str, torch.Tensor], from_: Dict[str, torch.Tensor]) ->
 
 class GradAccumulator:
     """accumulate(grads-into, grads-from, steps) (SPEC.md:500-506): sums
-    micro-batch gradients; flush() returns the averaged set (the 1/steps is
-    applied on the fly by the AdamW kernel through AdamW.step's grad scale,
-    or explicitly with scale=True).  Flushing before any add is an error."""
+    micro-batch gradients.  One contract: flush() returns the SUM and the
+    division by `steps` happens in AdamW.step (OptimConfig.accumulation_steps
+    = steps folds 1/steps into the AdamW kernel's gradient scale and clips the
+    norm of the averaged set, so no extra pass over the gradients);
+    flush(scale=True) returns the averaged set for any other consumer.
+    Flushing before any add is an error."""
 
     def __init__(self, steps: int):
         if steps < 1:
@@ -198,7 +201,7 @@ class GradAccumulator:
             accumulate(self.sum, grads)
         self.count += 1
 
-    def flush(self, scale: bool = True) -> Dict[str, torch.Tensor]:
+    def flush(self, scale: bool = False) -> Dict[str, torch.Tensor]:
         if self.sum is None:
             raise ms.StateError("flush before any accumulation (SPEC.md:503)")
         out = self.sum
@@ -296,9 +299,16 @@ def _train_step_in_backward(X, L, opt, M_mlp, M_head, grads, gmap, mlp, head, ct
     lib = _lib()
     opt.begin_backward()
 
+    errors = []
+
     def ready(_user, which, _stream):  # the library records the grad.* release
-        name = _NAMES[which]
-        opt.step_in_backward(name, gmap[name])
+        # ctypes prints and drops exceptions raised in a callback: keep the
+        # first one and re-raise it once block_step has returned.
+        try:
+            name = _NAMES[which]
+            opt.step_in_backward(name, gmap[name])
+        except BaseException as exc:  # noqa: BLE001
+            errors.append(exc)
 
     hook = _GRAD_READY(ready)
     ms._check(lib.mst_ctx_set_grad_ready_hook(ctx.handle, ctypes.cast(hook, ctypes.c_void_p), None))
@@ -306,6 +316,8 @@ def _train_step_in_backward(X, L, opt, M_mlp, M_head, grads, gmap, mlp, head, ct
         stats, grads = ms.block_step(X, L, mlp, head, M_mlp, M_head, grads=grads)
     finally:
         ms._check(lib.mst_ctx_set_grad_ready_hook(ctx.handle, None, None))
+    if errors:
+        raise errors[0]
     missing = [k for k, p in P.items() if not p.stepped]
     if missing:
         raise ms.StateError(f"parameters not stepped in backward: {missing}")

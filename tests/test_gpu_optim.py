@@ -97,7 +97,7 @@ def test_accumulation_matches_oracle_and_errors():
         acc.flush()
     for gm in micro:
         acc.add(gm)
-    out = acc.flush()["w"]
+    out = acc.flush(scale=True)["w"]
     ref = O.accumulate([[gm["w"].double().cpu().numpy()] for gm in micro], k)[0]
     assert rel(out.cpu(), ref) <= REL
     # g and -g cancel exactly
@@ -106,6 +106,47 @@ def test_accumulation_matches_oracle_and_errors():
     acc.add({"w": g})
     acc.add({"w": -g})
     assert torch.count_nonzero(acc.flush()["w"]) == 0
+
+
+@pytest.mark.parametrize("max_norm", [0.05, 1e9])
+def test_accumulation_with_active_clip_matches_oracle(max_norm):
+    """GradAccumulator.flush() (the sum) -> AdamW.step with
+    accumulation_steps = k: sum, divide by k, clip the norm of the AVERAGED
+    gradients (SPEC.md:500-506 then 486-491), Adam step.  max_norm 0.05
+    clips (||avg|| ~ 0.5), 1e9 does not."""
+    k, n = 3, 20_000
+    w = _param(n, 8).bfloat16()
+    opt = optim.AdamW({"w": w}, optim.OptimConfig(clip_norm=max_norm, accumulation_steps=k))
+    micro = [torch.randn(n, device="cuda") * 0.01 for _ in range(k)]
+    acc = optim.GradAccumulator(k)
+    for g in micro:
+        acc.add({"w": g})
+    w0 = opt.state.params["w"].master.double().cpu().numpy()
+    norm = opt.step(acc.flush(), check_finite=True)
+    avg = O.accumulate([[g.double().cpu().numpy()] for g in micro], k)
+    (gc,), ref_norm = O.clip_global_norm(avg, max_norm)
+    assert abs(norm - ref_norm) / ref_norm < 1e-6  # the norm of the average, not of the sum
+    assert (ref_norm > max_norm) == (max_norm < 1)
+    wr, _, _ = O.adamw_step(w0, gc, np.zeros(n), np.zeros(n), 1)
+    assert rel(opt.state.params["w"].master.cpu(), wr) <= REL
+
+
+def test_in_backward_hook_errors_are_raised():
+    """An exception inside the gradient-ready callback (here: a parameter
+    stepped twice) surfaces from train_step instead of being dropped by
+    ctypes."""
+    X, L, W = _block(3)
+    opt = optim.AdamW(W, optim.OptimConfig(in_backward=True))
+    orig = opt.step_in_backward
+
+    def twice(name, grad):
+        orig(name, grad)
+        if name == "W_out":
+            orig(name, grad)
+
+    opt.step_in_backward = twice
+    with pytest.raises(ms.StateError):
+        optim.train_step(X, L, opt, 2, 2)
 
 
 def _block(seed=0, N=512, H=128, I=256, V=1024):
