@@ -172,31 +172,31 @@ def cpu_block(tokens: int, m: int, nthreads: int, seed: int = 0):
     return oracle.CpuBlock(X, L, Wg, Wu, Wd, Wo, min(m, tokens), min(m, tokens), nthreads), np
 
 
-def cpu_baseline(m: int, budget_s: float = 20.0) -> dict:
+# One bounded CPU sample for BOTH CPU legs (this arm's cpu_baseline and the
+# --impl reference arm): 256 tokens at Llama3-8B widths, M=8 -> 32-row chunks.
+CPU_SAMPLE_TOKENS = 256
+CPU_SAMPLE_M = 8
+
+
+def cpu_baseline(m: int = CPU_SAMPLE_M) -> dict:
     """The reference path (CPU port of SPEC.md:271-361, f32, sequential-K
     matmuls, OpenMP over output rows) on all host threads, on a bounded sample
-    of the same workload (Llama3-8B widths, fewer tokens; cost per token is
-    independent of S)."""
+    of the same workload (Llama3-8B widths, CPU_SAMPLE_TOKENS tokens; cost per
+    token is independent of S).  One untimed warm-up step, then one timed step
+    -- the same sample and code the --impl reference arm times."""
     from oracle import oracle
 
     nth = oracle.host_threads()
-    probe_tokens = 16
-    blk, _ = cpu_block(probe_tokens, m, nth)
-    blk.step()  # warm (page-in)
-    t0 = time.perf_counter()
-    blk.step()
-    t_probe = time.perf_counter() - t0
-    tokens = int(max(16, min(256, probe_tokens * budget_s / max(t_probe, 1e-3))))
-    tokens = (tokens // 8) * 8
-    del blk
+    tokens = CPU_SAMPLE_TOKENS
     blk, _ = cpu_block(tokens, m, nth)
+    blk.step()  # warm (page-in, thread pool)
     t0 = time.perf_counter()
     loss = blk.step()
     dt = time.perf_counter() - t0
     return {"value": tokens / dt, "unit": UNIT, "cores": nth, "kind": "port",
-            "sample": f"{tokens} tokens (H=4096 I=14336 V=128256, M={min(m, tokens)}) fwd+bwd in {dt:.1f} s, f32, "
-                      f"oracle/mst_oracle.c orc_block_step_f32 (loss {loss:.4f})",
-            "tflops": tokens * flops_per_token() / dt / 1e12}
+            "sample": f"{tokens} tokens (H=4096 I=14336 V=128256, M={min(m, tokens)}: {tokens // min(m, tokens)}-row "
+                      f"chunks) fwd+bwd in {dt:.1f} s, f32, oracle/mst_oracle.c orc_block_step_f32 (loss {loss:.4f})",
+            "executed_tflops": tokens * model_flops_per_token() / dt / 1e12}
 
 
 def run_reference(args) -> None:
@@ -206,16 +206,9 @@ def run_reference(args) -> None:
     from oracle import oracle
 
     nth = oracle.host_threads()
-    # size one step so the whole --steps K --warmup W run takes ~2-3 minutes
-    per_step_budget = max(3.0, min(15.0, 150.0 / max(1, args.steps + args.warmup)))
-    probe, _ = cpu_block(16, args.m_mlp, nth)
-    probe.step()
-    t0 = time.perf_counter()
-    probe.step()
-    t_probe = time.perf_counter() - t0
-    del probe
-    tokens = int(max(16, min(512, 16 * per_step_budget / max(t_probe, 1e-3)))) // 8 * 8
-    blk, _ = cpu_block(tokens, args.m_mlp, nth)
+    tokens = CPU_SAMPLE_TOKENS  # the same sample as this arm's cpu_baseline leg
+    m = CPU_SAMPLE_M
+    blk, _ = cpu_block(tokens, m, nth)
     for _ in range(args.warmup):
         blk.step()
     t0 = time.perf_counter()
@@ -223,15 +216,72 @@ def run_reference(args) -> None:
         blk.step()
     dt = (time.perf_counter() - t0) / args.steps
     value = tokens / dt
-    sample = (f"{tokens} tokens per step at Llama3-8B widths (H=4096 I=14336 V=128256), M={min(args.m_mlp, tokens)}, "
-              f"f32 CPU port of the reference path (oracle/mst_oracle.c), {nth} threads")
+    sample = (f"{tokens} tokens per step at Llama3-8B widths (H=4096 I=14336 V=128256), M={m} ({tokens // m}-row "
+              f"chunks), f32 CPU port of the reference path (oracle/mst_oracle.c), {nth} threads")
     emit({"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
           "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
           "vs_baseline": None, "dtype": "f32", "data": "synthetic",
           "config": {"workload": "config 2 (Llama3-8B MLP+LM-Head widths), bounded CPU sample", "tokens_per_step": tokens,
-                     "M_mlp": args.m_mlp, "M_head": args.m_head, "parallelism": "cpu"},
+                     "M_mlp": m, "M_head": m, "parallelism": "cpu"},
           "cpu_baseline": {"value": value, "unit": UNIT, "cores": nth, "kind": "port", "sample": sample},
           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+
+
+def max_seq_probe(dev, chunk: int = 8192) -> dict:
+    """cmd_max_seq on this GPU: the largest S (multiple of
+    the chunk length) whose block step fits, from the workspace bound -- per
+    token the step keeps X and dX (bf16) plus a label and an fp32 LSE, i.e.
+    4H + 8 bytes; weights, fp32 dW and the chunk buffers are S-independent --
+    then ONE real step at that S (device-resident X / labels / dX, M = S/chunk)
+    that must produce a finite loss.  On an allocation failure S shrinks by 3%."""
+    import torch
+
+    from paper_2407_15892_b200 import miniseq as ms
+
+    ctx = ms.Context.get(dev.index)
+    torch.cuda.empty_cache()
+    free, total = torch.cuda.mem_get_info(dev)
+    per_token = 4 * H + 8
+    fixed = 6 * (3 * H * I + H * V) + (ms.block_workspace_bytes(chunk, H, I, V, 1, 1, ctx) - 4 * chunk)
+    margin = 3 << 30  # allocator rounding, CUDA context growth
+    S = int((free - fixed - margin) // per_token) // chunk * chunk
+    for attempt in range(3):
+        M = S // chunk
+        try:
+            g = torch.Generator(device=dev).manual_seed(7)
+            X = torch.randn(S, H, device=dev, generator=g, dtype=torch.bfloat16)
+            W = [(0.02 * torch.randn(*sh, device=dev, generator=g)).bfloat16() for sh in ((H, I), (H, I), (I, H),
+                                                                                       (H, V))]
+            L = torch.randint(0, V, (S,), device=dev, generator=g, dtype=torch.int32)
+            grads = ms.alloc_block_grads(S, H, I, V, dev)
+            stats = torch.empty(ms.stats_len(M), device=dev)
+            ws = torch.empty(ms.block_workspace_bytes(S, H, I, V, M, M, ctx), dtype=torch.uint8, device=dev)
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            ms.block_step(X, L, ms.MlpWeights(*W[:3]), ms.LmHeadWeights(W[3]), M, M, grads=grads, stats=stats,
+                          workspace=ws)
+            e1.record()
+            torch.cuda.synchronize(dev)
+            loss = float(stats[2])
+            step_ms = e0.elapsed_time(e1)
+            peak = torch.cuda.max_memory_allocated(dev)
+            del X, W, L, grads, stats, ws
+            torch.cuda.empty_cache()
+            if not math.isfinite(loss):
+                return {"max_seq_tokens": None, "error": f"non-finite loss at S={S}"}
+            return {"max_seq_tokens": S, "chunk_tokens": chunk, "M": M, "step_ms": step_ms,
+                    "tokens_per_s": S / step_ms * 1e3, "loss": loss, "device_total_gb": total / 1e9,
+                    "device_peak_allocated_gb": peak / 1e9, "bytes_per_token": per_token,
+                    "how": "S from the workspace bound (4H+8 B/token beside S-independent weights, fp32 dW and chunk "
+                           "buffers), then one verified fwd+bwd step at that S"}
+        except (torch.OutOfMemoryError, ms.Error) as exc:
+            for name in ("X", "W", "L", "grads", "stats", "ws"):
+                locals().pop(name, None)
+            torch.cuda.empty_cache()
+            last = str(exc)[:120]
+            S = int(S * 0.97) // chunk * chunk
+    return {"max_seq_tokens": None, "error": last}
 
 
 def _tracked_peak(S: int, M: int) -> int:
@@ -255,6 +305,7 @@ def main() -> None:
     ap.add_argument("--m-head", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-max-seq", action="store_true", help="skip the max-sequence probe (one ~40 s step)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -437,7 +488,7 @@ def main() -> None:
     peaks = load_peaks()
     achieved = gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
     traffic = ncu_traffic_per_launch()
-    executed_fpt = gemm_flops / args.steps / S if gemm_flops else flops_per_token()
+    executed_fpt = gemm_flops / args.steps / S if gemm_flops else model_flops_per_token()
     tflops_step = tokens_step / world * executed_fpt / (ms_step / 1e3) / 1e12
     ws_m1 = ms.block_workspace_bytes(S, H, I, V, 1, 1, ctx)
 
@@ -463,8 +514,6 @@ def main() -> None:
                    "l2": "no flush: every step streams 1.4 GB of bf16 weights and 2.8 GB of fp32 dW (>> 126 MB L2)"},
         "tflops_per_gpu": tflops_step,
         "executed_flops_per_token": executed_fpt,
-        "canonical_flops_per_token": flops_per_token(),
-        "canonical_tflops_per_gpu": tokens_step / world * flops_per_token() / (ms_step / 1e3) / 1e12,
         "mfu_model_flops": tokens_step / world * model_flops_per_token() / (ms_step / 1e3) / 1e12 / peaks["tflops"],
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peaks["tflops_sustained"], "unit": "TFLOP/s",
                      "frac": achieved / peaks["tflops_sustained"] if achieved else None, "traffic": traffic,
@@ -487,6 +536,12 @@ def main() -> None:
     }
     if e2e is None:
         out["e2e"] = None
+    if world == 1 and not args.no_max_seq:
+        # free this run's buffers first: the probe needs the whole device
+        X = L = grads = ws = Wg = Wu = Wd = Wo = mlp = head = None  # noqa: F841
+        Xb = Lb = hws = None  # noqa: F841
+        out["max_seq"] = max_seq_probe(dev)
+        out["max_seq_tokens"] = out["max_seq"].get("max_seq_tokens")
     if world == 1 and not args.no_cpu_baseline:
         try:
             out["cpu_baseline"] = cpu_baseline(Mm)

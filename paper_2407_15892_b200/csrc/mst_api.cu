@@ -1255,19 +1255,36 @@ static size_t chunked_extra_bytes(int64_t n, int64_t i, int64_t m) {
   return 2 * align_up(size_t(max_chunk(n, m)) * i * 4, 256) + 512;
 }
 
+// The head plan refines the MLP plan: every MLP chunk boundary is also a
+// head chunk boundary, so each MLP chunk holds whole head chunks (always
+// true for M_mlp == M_head; for the paper's M_mlp=4 / M_head=16 when 16 | S,
+// and in general when the balanced plans happen to nest).
+static bool plans_nest(int64_t n, int64_t m_mlp, int64_t m_head) {
+  if (n <= 0 || m_mlp <= 0 || m_head <= 0) return false;
+  if (m_mlp == m_head) return true;
+  const std::vector<int64_t> bm = plan_bounds(n, m_mlp), bh = plan_bounds(n, m_head);
+  size_t k = 0;
+  for (int64_t x : bm) {
+    while (k < bh.size() && bh[k] < x) ++k;
+    if (k == bh.size() || bh[k] != x) return false;
+  }
+  return true;
+}
+
 int mst_block_workspace(int64_t n, int64_t h, int64_t i, int64_t v, int64_t m_mlp, int64_t m_head, size_t* bytes) {
   size_t a = 0, b = 0;
   MST_TRY(mst_mlp_workspace(n, h, i, m_mlp, &a));
   MST_TRY(mst_lmhead_workspace(n, h, v, m_head, &b));
   const size_t two_pass = block_fixed_bytes(n, h) + 256 + std::max(a, b);
-  const size_t chunked =
-      m_mlp == m_head ? chunked_fixed_bytes(n, h, m_mlp) + 256 + a + b + chunked_extra_bytes(n, i, m_mlp) : 0;
+  const size_t chunked = plans_nest(n, m_mlp, m_head)
+                             ? chunked_fixed_bytes(n, h, m_mlp) + 256 + a + b + chunked_extra_bytes(n, i, m_mlp)
+                             : 0;
   *bytes = std::max(two_pass, chunked);
   return MST_OK;
 }
 
-static bool uses_chunked_block(const mst_ctx* c, int64_t m_mlp, int64_t m_head) {
-  return c->chunked_block && c->fused_head && m_mlp == m_head;
+static bool uses_chunked_block(const mst_ctx* c, int64_t n, int64_t m_mlp, int64_t m_head) {
+  return c->chunked_block && c->fused_head && plans_nest(n, m_mlp, m_head);
 }
 
 int mst_ctx_block_workspace(const mst_ctx* c, int64_t n, int64_t h, int64_t i, int64_t v, int64_t m_mlp,
@@ -1276,7 +1293,7 @@ int mst_ctx_block_workspace(const mst_ctx* c, int64_t n, int64_t h, int64_t i, i
   size_t a = 0, b = 0;
   MST_TRY(mst_mlp_workspace(n, h, i, m_mlp, &a));
   MST_TRY(mst_lmhead_workspace(n, h, v, m_head, &b));
-  *bytes = uses_chunked_block(c, m_mlp, m_head)
+  *bytes = uses_chunked_block(c, n, m_mlp, m_head)
                ? chunked_fixed_bytes(n, h, m_mlp) + 256 + a + b + chunked_extra_bytes(n, i, m_mlp)
                : block_fixed_bytes(n, h) + 256 + std::max(a, b);
   return MST_OK;
@@ -1732,7 +1749,7 @@ static size_t host_io_bytes(int64_t n, int64_t h, int64_t m) {  // 2 X + 2 dX ch
 
 static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const int32_t* labels, const void* wg,
                               const void* wu, const void* wd, const void* wout, int64_t n, int64_t h, int64_t i,
-                              int64_t v, int64_t m, int loss_mode, float grad_loss, float* stats, void* dx, float* dwg,
+                              int64_t v, int64_t m, int64_t mh, int loss_mode, float grad_loss, float* stats, void* dx, float* dwg,
                               float* dwu, float* dwd, float* dwout, int accumulate, void* ws, size_t ws_bytes,
                               const float* global_valid, const HostIO* io = nullptr) {
   char* base = static_cast<char*>(ws);
@@ -1747,23 +1764,33 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
   float *dhb, *zt, *lrow, *scales;
   float2* part;
   carve_mlp(cv, n, h, i, m, &hb, &dg, &du, &dhb, &xt, &ht);
-  carve_head(cv, n, h, v, m, &part, &zt, &lrow, &dl, &scales, &ot);
+  carve_head(cv, n, h, v, mh, &part, &zt, &lrow, &dl, &scales, &ot);
   float* g32 = static_cast<float*>(cv.take(size_t(max_chunk(n, m)) * i * 4));
   float* u32 = static_cast<float*>(cv.take(size_t(max_chunk(n, m)) * i * 4));
-  const int64_t ldt = ld_t(n, m);
+  const int64_t ldt = ld_t(n, m), ldt_h = ld_t(n, mh);
   const std::vector<int64_t> b = plan_bounds(n, m);
   const int nch = (int)b.size() - 1;
+  // Head plan: refines the MLP plan (plans_nest), head chunks hc0[j] ..
+  // hc0[j+1]-1 lie inside MLP chunk j.
+  const std::vector<int64_t> bh = plan_bounds(n, mh);
+  const int nch_h = (int)bh.size() - 1;
+  std::vector<int> hc0(nch + 1, 0);
+  for (int j = 0, k = 0; j <= nch; ++j) {
+    while (k < nch_h && bh[k] < b[j]) ++k;
+    hc0[j] = k;
+  }
+  hc0[nch] = nch_h;
   const int nparts = (int)cdiv(v, 256);
   // dlogits scales depend only on the labels: compute them up front.
-  MST_CUDA(cudaMemsetAsync(stats, 0, sizeof(float) * MST_STATS_LEN(nch), st));
-  chunk_valid_kernel<<<nch, 256, 0, st>>>(labels, n, nch, (int)v, stats);
-  sum_valid_kernel<<<1, 32, 0, st>>>(stats, nch);
+  MST_CUDA(cudaMemsetAsync(stats, 0, sizeof(float) * MST_STATS_LEN(nch_h), st));
+  chunk_valid_kernel<<<nch_h, 256, 0, st>>>(labels, n, nch_h, (int)v, stats);
+  sum_valid_kernel<<<1, 32, 0, st>>>(stats, nch_h);
   float* gstats = stats;
   if (global_valid) {  // sequence-parallel caller: dlogits scaled by the all-reduced token count
     gstats = c->scratch_dev + 64;
     MST_CUDA(cudaMemcpyAsync(gstats + 1, global_valid, sizeof(float), cudaMemcpyDeviceToDevice, st));
   }
-  grad_scale_kernel<<<(nch + 255) / 256, 256, 0, st>>>(gstats, stats, nch, loss_mode, grad_loss, scales);
+  grad_scale_kernel<<<(nch_h + 255) / 256, 256, 0, st>>>(gstats, stats, nch_h, loss_mode, grad_loss, scales);
   c->launches += 3;
   WeightScope ws_(c, wg, wu, wd, wout);
   const uint64_t act_bytes = (uint64_t)max_chunk(n, m) * h * 2;  // one chunk of O, two of dO
@@ -1853,7 +1880,6 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
   }
   for (int j = 0; j < nch; ++j) {
     const int64_t r0 = b[j], rows = rows_of(j);
-    const int beta = (j > 0 || accumulate) ? 1 : 0;
     void* oj = o;
     void* doj = dO[j & 1];
     {  // K2(j) + the weight/input gradients of chunk j-1
@@ -1865,43 +1891,50 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
       if (j > 0) grads_live(j - 1, false);
       if (io && j > 0) MST_TRY(d2h(j - 1));
     }
-    const uint64_t part_bytes = (uint64_t)rows * nparts * 8 + (uint64_t)rows * 8;
     if (j == 0) grad_alloc(c, 3, (uint64_t)h * v * 4);
-    mem_alloc(c, (uint64_t)rows * h * 2, "act.oT");
-    mem_alloc(c, part_bytes, "inter.head.partials");
-    mem_alloc(c, (uint64_t)rows * v * 2, "inter.head.dlogits");
-    cnt_op(c, 5ull * rows * v, (uint64_t)(rows * v + 2 * rows));      // cross-entropy forward
-    cnt_op(c, 5ull * rows * v, (uint64_t)(2 * rows * v + 2 * rows));  // cross-entropy backward
-    MST_TRY(transpose_bf16(c, st, oj, h, ot, ldt, rows, h));
-    {  // K3': logits GEMM, partials + softmax numerators
-      Launch L;
-      MST_TRY(build_plain(c, L, Operand{oj, rows, h, h, false}, Operand{wout, v, h, v, true}, dl, v,
-                          mst::kEpiCeFwdNum, 0, (c->wide_mask & 1) ? 2 : 1));
-      ProblemDesc& P = L.p.prob[0];
-      P.labels = labels + r0;
-      P.part = part;
-      P.ztarget = zt;
-      P.nparts = nparts;
-      MST_TRY(launch(c, st, L));
+    for (int k = hc0[j]; k < hc0[j + 1]; ++k) {  // the head chunks of MLP chunk j
+      const int64_t hr0 = bh[k], hrows = bh[k + 1] - bh[k];
+      const int hbeta = (k > 0 || accumulate) ? 1 : 0;
+      void* ok = const_cast<char*>(bptr(oj, (hr0 - r0) * h));
+      void* dok = const_cast<char*>(bptr(doj, (hr0 - r0) * h));
+      const uint64_t part_bytes = (uint64_t)hrows * nparts * 8 + (uint64_t)hrows * 8;
+      mem_alloc(c, (uint64_t)hrows * h * 2, "act.oT");
+      mem_alloc(c, part_bytes, "inter.head.partials");
+      mem_alloc(c, (uint64_t)hrows * v * 2, "inter.head.dlogits");
+      cnt_op(c, 5ull * hrows * v, (uint64_t)(hrows * v + 2 * hrows));      // cross-entropy forward
+      cnt_op(c, 5ull * hrows * v, (uint64_t)(2 * hrows * v + 2 * hrows));  // cross-entropy backward
+      MST_TRY(transpose_bf16(c, st, ok, h, ot, ldt_h, hrows, h));
+      {  // K3': logits GEMM, partials + softmax numerators
+        Launch L;
+        MST_TRY(build_plain(c, L, Operand{ok, hrows, h, h, false}, Operand{wout, v, h, v, true}, dl, v,
+                            mst::kEpiCeFwdNum, 0, (c->wide_mask & 1) ? 2 : 1));
+        ProblemDesc& P = L.p.prob[0];
+        P.labels = labels + hr0;
+        P.part = part;
+        P.ztarget = zt;
+        P.nparts = nparts;
+        MST_TRY(launch(c, st, L));
+      }
+      ce_combine_kernel<<<(unsigned)cdiv(hrows * 32, 256), 256, 0, st>>>(part, nparts, zt, labels + hr0, (int)hrows,
+                                                                        (int)v, lse + hr0, lrow, stats + 3);
+      chunk_reduce_kernel<<<1, 1024, 0, st>>>(lrow, labels + hr0, (int)hrows, (int)v, stats + 4 + k,
+                                              stats + 4 + nch_h + k);
+      normalize_dlogits_kernel<<<(unsigned)cdiv(hrows * (v / 8), 256), 256, 0, st>>>(
+          static_cast<uint16_t*>(dl), v, (int)hrows, (int)v, part, nparts, lse + hr0, labels + hr0, scales + k, zt);
+      c->launches += 3;
+      {  // K5 + K6
+        Launch L;
+        MST_TRY(build_plain(c, L, Operand{dl, hrows, v, v, false}, Operand{wout, h, v, v, false}, dok, h,
+                            mst::kEpiStoreBf16, 0, (c->wide_mask & 2) ? 2 : 1));
+        MST_TRY(build_plain(c, L, Operand{ot, h, hrows, ldt_h, false}, Operand{dl, v, hrows, v, true}, dwout, v,
+                            mst::kEpiAccF32, hbeta));
+        MST_TRY(launch(c, st, L));
+      }
+      if (k == nch_h - 1) grad_ready(c, 3, st, (uint64_t)h * v * 4);  // dW_out complete
+      mem_free(c, (uint64_t)hrows * v * 2, "inter.head.dlogits");
+      mem_free(c, part_bytes, "inter.head.partials");
+      mem_free(c, (uint64_t)hrows * h * 2, "act.oT");
     }
-    ce_combine_kernel<<<(unsigned)cdiv(rows * 32, 256), 256, 0, st>>>(part, nparts, zt, labels + r0, (int)rows, (int)v,
-                                                                     lse + r0, lrow, stats + 3);
-    chunk_reduce_kernel<<<1, 1024, 0, st>>>(lrow, labels + r0, (int)rows, (int)v, stats + 4 + j, stats + 4 + nch + j);
-    normalize_dlogits_kernel<<<(unsigned)cdiv(rows * (v / 8), 256), 256, 0, st>>>(
-        static_cast<uint16_t*>(dl), v, (int)rows, (int)v, part, nparts, lse + r0, labels + r0, scales + j, zt);
-    c->launches += 3;
-    {  // K5 + K6
-      Launch L;
-      MST_TRY(build_plain(c, L, Operand{dl, rows, v, v, false}, Operand{wout, h, v, v, false}, doj, h,
-                          mst::kEpiStoreBf16, 0, (c->wide_mask & 2) ? 2 : 1));
-      MST_TRY(build_plain(c, L, Operand{ot, h, rows, ldt, false}, Operand{dl, v, rows, v, true}, dwout, v,
-                          mst::kEpiAccF32, beta));
-      MST_TRY(launch(c, st, L));
-    }
-    if (j == nch - 1) grad_ready(c, 3, st, (uint64_t)h * v * 4);  // dW_out complete
-    mem_free(c, (uint64_t)rows * v * 2, "inter.head.dlogits");
-    mem_free(c, part_bytes, "inter.head.partials");
-    mem_free(c, (uint64_t)rows * h * 2, "act.oT");
     if (c->fuse_swiglu_bwd) {
       // K7a with the SwiGLU backward in its epilogue: dh = dO_j W_d^T stays in
       // TMEM; dG, dU come out directly (no dh round trip through HBM).
@@ -1965,7 +1998,7 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
   mem_free(c, (uint64_t)n * 4, "act.lse");
   mem_free(c, 2 * act_bytes, "act.dO");
   mem_free(c, act_bytes, "act.O");
-  finalize_loss_kernel<<<1, 32, 0, st>>>(stats, nch, loss_mode);
+  finalize_loss_kernel<<<1, 32, 0, st>>>(stats, nch_h, loss_mode);
   c->launches += 1;
   MST_CUDA(cudaGetLastError());
   return MST_OK;
@@ -1974,7 +2007,7 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
 int mst_ctx_block_host_workspace(const mst_ctx* c, int64_t n, int64_t h, int64_t i, int64_t v, int64_t m,
                                  size_t* bytes) {
   if (!c || !bytes) return fail(MST_ERR_STATE, "NULL context or output");
-  if (!uses_chunked_block(c, m, m))
+  if (!uses_chunked_block(c, n, m, m))
     return fail(MST_ERR_CONFIG, "host-resident X / dX need the chunk-wise schedule (tuning chunked_block=1, fused_head=1)");
   MST_TRY(mst_ctx_block_workspace(c, n, h, i, v, m, m, bytes));
   *bytes += host_io_bytes(n, h, m);
@@ -2014,7 +2047,7 @@ int mst_block_step_host(mst_ctx* c, void* stream, const void* x_host, const int3
   MST_CUDA(cudaEventRecord(c->io_ev[9], st));
   MST_CUDA(cudaStreamWaitEvent(c->copy_stream, c->io_ev[9], 0));
   MST_CUDA(cudaMemcpyAsync(labels_dev, labels_host, size_t(n) * 4, cudaMemcpyHostToDevice, st));
-  return block_step_chunked(c, st, nullptr, labels_dev, wg, wu, wd, wout, n, h, i, v, m, loss_mode, grad_loss, stats,
+  return block_step_chunked(c, st, nullptr, labels_dev, wg, wu, wd, wout, n, h, i, v, m, m, loss_mode, grad_loss, stats,
                             nullptr, dwg, dwu, dwd, dwout, accumulate, ws, dev_need, nullptr, &io);
 }
 
@@ -2038,9 +2071,9 @@ int mst_block_step_sp(mst_ctx* c, void* stream, const void* x, const int32_t* la
     return fail(MST_ERR_CONFIG, "unknown loss mode %d", loss_mode);
   if (!x || !labels || !wg || !wu || !wd || !wout || !stats || !dx || !dwg || !dwu || !dwd || !dwout)
     return fail(MST_ERR_CONFIG, "NULL tensor pointer");
-  if (uses_chunked_block(c, m_mlp, m_head))
+  if (uses_chunked_block(c, n, m_mlp, m_head))
     return block_step_chunked(c, static_cast<cudaStream_t>(stream), x, labels, wg, wu, wd, wout, n, h, i, v, m_mlp,
-                              loss_mode, grad_loss, stats, dx, dwg, dwu, dwd, dwout, accumulate, ws, ws_bytes,
+                              m_head, loss_mode, grad_loss, stats, dx, dwg, dwu, dwd, dwout, accumulate, ws, ws_bytes,
                               global_valid);
   char* base = static_cast<char*>(ws);
   const size_t ob = align_up(size_t(n) * h * 2, 256);

@@ -43,17 +43,19 @@ def _chunk(N: int, M: int) -> int:
     return -(-N // c)  # the longest chunk of the balanced plan (App. A-1)
 
 
-def predict_block_peak(N: int, H: int, I: int, V: int, M: int) -> Dict[str, int]:
+def predict_block_peak(N: int, H: int, I: int, V: int, M: int, M_head: int | None = None) -> Dict[str, int]:
     """Peak live bytes per label class of one chunk-wise block step
-    (mst_block_step, M_mlp = M_head = M), as the library's memtrack events
-    report them: the MLP chunk buffers h (bf16), G and U (fp32, kept for the
-    backward), dh (fp32), dG, dU, h^T (bf16) -> 20 n I bytes at their common
-    peak; the LM-Head chunk's softmax numerators / dlogits (bf16) plus the
-    per-256-column CE partials and two fp32 row scalars; the activations:
-    one O chunk and two dO chunks (bf16; dO_j is read by chunk j+1's dW_down
-    GEMM) and the sequence-wide lse (fp32)."""
+    (mst_block_step; M_mlp = M, M_head = M unless given, head chunks nested in
+    the MLP chunks), as the library's memtrack events report them: the MLP
+    chunk buffers h (bf16), G and U (fp32, kept for the backward), dh (fp32),
+    dG, dU, h^T (bf16) -> 20 n I bytes at their common peak; one LM-Head
+    chunk's softmax numerators / dlogits (bf16) plus the per-256-column CE
+    partials and two fp32 row scalars; the activations: one O chunk and two
+    dO chunks of the MLP chunk length (bf16; dO_j is read by chunk j+1's
+    dW_down GEMM) and the sequence-wide lse (fp32)."""
     n = _chunk(N, M)
-    head = n * V * 2 + n * (-(-V // 256)) * 8 + n * 8
+    nh = _chunk(N, M if M_head is None else M_head)
+    head = nh * V * 2 + nh * (-(-V // 256)) * 8 + nh * 8
     mlp = 20 * n * I
     # the head's chunk buffers coexist with the forward MLP buffers of the same chunk (h, G, U = 10 n I)
     inter = max(mlp, 10 * n * I + head)

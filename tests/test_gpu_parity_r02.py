@@ -40,14 +40,25 @@ def _peaked_inputs(orc, seed, N, H, V, z_label=14.0, pair_every=4):
     for r in range(N):
         d = X[r] / np.dot(X[r], X[r]) * z_label
         W[:, labels[r]] = d
-        if r % pair_every == 0:
-            W[:, labels[r] ^ 1] = d * (1.0 - 1e-3)  # near-equal twin in the same tile
+        if r % pair_every == 0:  # near-equal twin logit in the same tile, different direction
+            W[:, labels[r] ^ 1] = _twin(d, X[r], 1e-3, rng)
             twins.append(r)
     c["Wout"] = torch.from_numpy(W).float().bfloat16().float().numpy()
     L = labels.astype(np.int32)
     L[::13] = -100
     c["L"] = L
     return c, twins
+
+
+def _twin(d, x, eps, rng):
+    """A column whose logit against x is (1 - eps) that of d but whose
+    direction differs (random part orthogonal to x with the norm of d): the
+    two near-equal logits then contribute independent directions to dX_r
+    instead of cancelling (nearly parallel columns would make dX_r a
+    difference of two bf16-rounded dlogits, beyond any bf16 dlogits path)."""
+    q = rng.standard_normal(len(d))
+    q -= np.dot(q, x) / np.dot(x, x) * x
+    return d * (1.0 - eps) + q / np.linalg.norm(q) * np.linalg.norm(d)
 
 
 def _softmax_label_prob(c):
@@ -113,7 +124,7 @@ def test_confident_softmax_block_step(orc):
         d = O[r] / (np.linalg.norm(O[r]) ** 2) * 12.0  # z_label ~ 12 for every row
         W[:, labels[r]] = d
         if r % 5 == 0:
-            W[:, labels[r] ^ 1] = d * (1 - 2e-3)
+            W[:, labels[r] ^ 1] = _twin(d, O[r], 2e-3, rng)
     c["Wout"] = torch.from_numpy(W).float().bfloat16().float().numpy()
     L = labels.astype(np.int32)
     L[::11] = -100
@@ -274,3 +285,41 @@ def test_config4_full_size_m16():
     torch.cuda.empty_cache()
     ref = _torch_ref_rowblocks(X, L, Wg, Wu, Wd, Wo, rows=4096)
     _check_full(res[16], ref, "config4 M=16")
+
+
+@pytest.mark.parametrize("shape", [(1024, 256, 688, 4096, 4, 16), (777, 64, 136, 520, 3, 9), (1000, 128, 256, 1000, 2, 10),
+                                   (600, 64, 128, 512, 3, 4)])
+def test_nested_chunkwise_schedule_matches_op_by_op(shape):
+    """M_head a refinement of M_mlp (every MLP chunk boundary is a head chunk
+    boundary): block_step runs the chunk-wise schedule with the head chunks
+    nested in each MLP chunk (no [S, H] O / dO, no G,U recompute GEMM) and
+    agrees with the op-by-op schedule to fp32 rounding.  (777, 3 / 9) and
+    (600, 3 / 4) do not nest (balanced plans) and keep the op-by-op schedule."""
+    N, H, I, V, Mm, Mh = shape
+    torch.manual_seed(17)
+    X = torch.randn(N, H, device="cuda").bfloat16()
+    W = [(0.05 * torch.randn(*s, device="cuda")).bfloat16() for s in ((H, I), (H, I), (I, H), (H, V))]
+    L = torch.randint(0, V, (N,), device="cuda", dtype=torch.int32)
+    L[::7] = -100
+    mlp, head = ms.MlpWeights(*W[:3]), ms.LmHeadWeights(W[3])
+    ctx = ms.Context.get(0)
+    out = {}
+    try:
+        for chunked in (1, 0):
+            ctx.set_tuning("chunked_block", chunked)
+            ws = ms.block_workspace_bytes(N, H, I, V, Mm, Mh, ctx)
+            st, gr = ms.block_step(X, L, mlp, head, Mm, Mh)
+            torch.cuda.synchronize()
+            out[chunked] = (ws, st.clone(), {k: getattr(gr, k).clone() for k in ("dX", "W_gate", "W_up", "W_down",
+                                                                                    "W_out")})
+    finally:
+        ctx.set_tuning("chunked_block", 1)
+    bm = {r[0] for r in ms.make_chunk_plan(N, Mm).ranges}
+    bh = {r[0] for r in ms.make_chunk_plan(N, Mh).ranges}
+    if bm <= bh:  # nested: chunk-sized O / dO instead of [S, H]
+        assert out[1][0] < out[0][0]
+    else:  # not nested: the op-by-op schedule either way
+        assert out[1][0] == out[0][0]
+    assert abs(float(out[1][1][2]) - float(out[0][1][2])) <= 1e-6 * abs(float(out[0][1][2]))
+    for k in ("dX", "W_gate", "W_up", "W_down", "W_out"):
+        assert rel(out[1][2][k], out[0][2][k].double().cpu().numpy()) <= 1e-5, k

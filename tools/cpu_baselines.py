@@ -30,4 +30,4 @@ for nth, tokens in ((1, 32), (oracle.host_threads(), 256)):
     dt = time.perf_counter() - t0
     print(json.dumps({"mode": f"({'ii' if nth == 1 else 'iii'}) f32 port at Llama3-8B widths, {nth} thread(s)",
                       "tokens": tokens, "seconds": dt, "tokens_per_s": tokens / dt,
-                      "tflops": tokens * bench.flops_per_token() / dt / 1e12, "loss": loss}), flush=True)
+                      "executed_tflops": tokens * bench.model_flops_per_token() / dt / 1e12, "loss": loss}), flush=True)

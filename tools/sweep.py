@@ -26,7 +26,10 @@ from paper_2407_15892_b200 import miniseq as ms  # noqa: E402
 
 
 def flops_per_token(H, I, V):
-    return 22.0 * H * I + 8.0 * H * V
+    """FLOPs the block step executes per token (18HI + 6HV: no recompute GEMM
+    is left in the chunk-wise schedule with the single-pass head), so the
+    reported rate can be compared with the hardware peak."""
+    return 18.0 * H * I + 6.0 * H * V
 
 
 def make(S, H, I, V, dev, seed=0):
@@ -76,7 +79,7 @@ def sweep_m():
         peak = torch.cuda.max_memory_allocated()
         print(json.dumps({"config": "3 (Llama2-7B widths H=4096 I=11008 V=32000, S=16384)", "M": M,
                           "ms_per_step": ms_step, "tokens_per_s": S / ms_step * 1e3,
-                          "tflops": S * flops_per_token(H, I, V) / ms_step / 1e9,
+                          "executed_tflops": S * flops_per_token(H, I, V) / ms_step / 1e9,
                           "peak_intermediate_gb": intermediate_bytes(S, I, V, M, M) / 1e9,
                           "workspace_gb": ms.block_workspace_bytes(S, H, I, V, M, M, ms.Context.get(0)) / 1e9,
                           "device_peak_allocated_gb": peak / 1e9, "loss": loss}), flush=True)
@@ -92,7 +95,7 @@ def sweep_m2():
         ms_step, loss = timed_steps(X, L, W, M, M)
         print(json.dumps({"config": "2 (Llama3-8B widths, S=8192)", "M": M, "ms_per_step": ms_step,
                           "tokens_per_s": S / ms_step * 1e3,
-                          "tflops": S * flops_per_token(H, I, V) / ms_step / 1e9,
+                          "executed_tflops": S * flops_per_token(H, I, V) / ms_step / 1e9,
                           "peak_intermediate_gb": intermediate_bytes(S, I, V, M, M) / 1e9,
                           "workspace_gb": ms.block_workspace_bytes(S, H, I, V, M, M, ms.Context.get(0)) / 1e9,
                           "device_peak_allocated_gb": torch.cuda.max_memory_allocated() / 1e9, "loss": loss}),
@@ -124,7 +127,7 @@ def long_context():
     torch.cuda.reset_peak_memory_stats()
     ms_step, loss = timed_steps(X, L, W, M, M, steps=2, warmup=1)
     print(json.dumps({"config": "4 (Llama3-8B widths, S=65536, M=16)", "ms_per_step": ms_step,
-                      "tokens_per_s": S / ms_step * 1e3, "tflops": S * flops_per_token(H, I, V) / ms_step / 1e9,
+                      "tokens_per_s": S / ms_step * 1e3, "executed_tflops": S * flops_per_token(H, I, V) / ms_step / 1e9,
                       "peak_intermediate_gb": intermediate_bytes(S, I, V, M, M) / 1e9,
                       "peak_intermediate_gb_at_M1": intermediate_bytes(S, I, V, 1, 1) / 1e9,
                       "device_peak_allocated_gb": torch.cuda.max_memory_allocated() / 1e9, "loss": loss}),
