@@ -349,29 +349,28 @@ def main() -> None:
     grads = ms.alloc_block_grads(S, H, I, V, dev)
     nch = min(S, Mh)
     stats = torch.empty(ms.stats_len(nch), dtype=torch.float32, device=dev)
-    if world > 1:  # the op-by-op schedule overlaps the dW all-reduce (see below)
-        ctx.set_tuning("chunked_block", 1 if os.environ.get("MST_SP_CHUNKED") == "1" else 0)
+    slabs = int(os.environ.get("MST_SP_SLABS", "4"))
     ws = torch.empty(ms.block_workspace_bytes(S, H, I, V, Mm, Mh, ctx), dtype=torch.uint8, device=dev)
 
     if world == 1:
         def run_step(Xs, Ls):
             ms.block_step(Xs, Ls, mlp, head, Mm, Mh, grads=grads, stats=stats, workspace=ws)
-            return stats[2:3]
+            return stats[2:3], grads.dX
     else:
         ops = GpuOps()
-        # N>1: the op-by-op block schedule finishes dW_out after the LM-Head, so
-        # its 2.1 GB all-reduce (issued from the gradient-ready hook) overlaps
-        # the whole MLP backward; the chunk-wise schedule (N=1 default) would
-        # expose most of it.  MST_SP_CHUNKED=1 selects the chunk-wise one.
-        sp_chunked = os.environ.get("MST_SP_CHUNKED") == "1"
-        ctx.set_tuning("chunked_block", 1 if sp_chunked else 0)
+        # N>1: the same chunk-wise schedule as N=1; the last chunk's launches
+        # that finalise dW_out and dW_gate / dW_up are cut into `slabs` row
+        # slabs and each slab's SUM all-reduce is issued from the library's
+        # gradient-slab hook as soon as it is enqueued (NCCL's stream waits on
+        # it), overlapping the remaining launches (parallel.sp_block_step_fused).
 
-        def run_step(Xs, Ls):  # global valid count -> fused block (global scale) -> hook-driven dW all-reduces -> loss
-            return sp_block_step_fused(ops, Xs, Ls, (Wg, Wu, Wd), Wo, Mm, Mh, grads, workspace=ws,
-                                       stats=stats).loss.reshape(1)
+        def run_step(Xs, Ls):  # global valid count -> fused block (global scale) -> slab all-reduces -> loss
+            r = sp_block_step_fused(ops, Xs, Ls, (Wg, Wu, Wd), Wo, Mm, Mh, grads, workspace=ws, stats=stats,
+                                    slabs=slabs)
+            return r.loss.reshape(1), r.dX
 
     def step():
-        return run_step(X, L)
+        return run_step(X, L)[0]
 
     def barrier():
         if world > 1:
@@ -435,11 +434,11 @@ def main() -> None:
                 ready[k].record(cstream)
 
         host_abi = world == 1 and Mm == Mh
+        dXh = torch.empty(S, H, dtype=torch.bfloat16).pin_memory()
         if host_abi:
             # Through the C ABI with host buffers: mst_block_step_host copies
             # X_j in and dX_j out chunk by chunk on its copy stream while the
             # GEMMs run; the loss is read back every step.
-            dXh = torch.empty(S, H, dtype=torch.bfloat16).pin_memory()
             nb = ctypes.c_size_t()
             ms._check(ctx.lib.mst_ctx_block_host_workspace(ctx.handle, S, H, I, V, Mm, ctypes.byref(nb)))
             hws = torch.empty(nb.value, dtype=torch.uint8, device=dev)
@@ -456,7 +455,9 @@ def main() -> None:
                     stream.wait_event(ready[k])
                     if it + 1 < n:
                         prefetch(1 - k)
-                    loss_h.copy_(run_step(Xb[k], Lb[k]), non_blocking=True)
+                    loss_d, dX_d = run_step(Xb[k], Lb[k])
+                    loss_h.copy_(loss_d, non_blocking=True)
+                    dXh.copy_(dX_d, non_blocking=True)  # the step's input gradient back to the host
                     free[k].record(stream)
 
         run_e2e(2)
@@ -472,12 +473,12 @@ def main() -> None:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t)
         e2e = {"value": tokens_step / dt, "unit": UNIT, "h2d_bytes_per_step": Xh.numel() * 2 + Lh.numel() * 4,
-               "d2h_bytes_per_step": 4 + (S * H * 2 if host_abi else 0), "ms_per_step": dt * 1e3,
+               "d2h_bytes_per_step": 4 + S * H * 2, "ms_per_step": dt * 1e3,
                "path": ("C ABI mst_block_step_host with pinned host X / labels / dX: X_j H2D and dX_j D2H per chunk "
                         "on a copy stream overlapping the GEMMs, loss D2H every step; wall clock with synchronize"
                         if host_abi else
                         "pinned host X/labels -> H2D (double-buffered, copy stream overlapping the previous step), "
-                        "block_step / sp_block_step_fused (mst_block_step[_sp] + NCCL for N>1), loss D2H; "
+                        "block_step / sp_block_step_fused (mst_block_step[_sp] + NCCL for N>1), loss and dX D2H; "
                         "wall clock with synchronize")}
 
     if rank != 0:
@@ -494,10 +495,8 @@ def main() -> None:
 
     def act_fixed(mm, mh):
         """O / dO / lse part of the block workspace: one O and two dO chunks
-        plus lse (chunk-wise schedule), or full [S, H] O and dO (op-by-op)."""
-        if (world == 1 or os.environ.get("MST_SP_CHUNKED") == "1") and mm == mh:
-            return 3 * -(-S // min(S, mm)) * H * 2 + S * 4
-        return 2 * S * H * 2 + S * 4
+        plus lse (chunk-wise schedule: the bench's M_head refines M_mlp)."""
+        return 3 * -(-S // min(S, mm)) * H * 2 + S * 4
 
     inter = lambda mm, mh: ms.block_workspace_bytes(S, H, I, V, mm, mh, ctx) - act_fixed(mm, mh)  # noqa: E731
     out = {
@@ -508,9 +507,9 @@ def main() -> None:
                                f"S={S} tokens/GPU, M_mlp={Mm} M_head={Mh}",
                    "H": H, "I": I, "V": V, "seq_len": S, "global_tokens": tokens_step, "M_mlp": Mm, "M_head": Mh,
                    "parallelism": f"sp{world}" if world > 1 else "single",
-                   "schedule": "chunk-wise (MLP fwd -> head -> MLP bwd per chunk)" if world == 1 or
-                               os.environ.get("MST_SP_CHUNKED") == "1" else
-                               "op-by-op (MLP fwd, head fwd+bwd, MLP bwd; dW_out all-reduce overlaps the MLP backward)",
+                   "schedule": "chunk-wise (MLP fwd -> head -> MLP bwd per chunk)" + (
+                       "" if world == 1 else f"; dW all-reduce per row slab ({slabs} slabs) as the last chunk's "
+                                             "launches finalise them"),
                    "l2": "no flush: every step streams 1.4 GB of bf16 weights and 2.8 GB of fp32 dW (>> 126 MB L2)"},
         "tflops_per_gpu": tflops_step,
         "executed_flops_per_token": executed_fpt,

@@ -212,6 +212,21 @@ MST_API int mst_grad_accumulate(mst_ctx* ctx, void* stream, float* into, const f
 typedef void (*mst_grad_ready_hook)(void* user, int which, void* stream);
 MST_API int mst_ctx_set_grad_ready_hook(mst_ctx* ctx, mst_grad_ready_hook fn, void* user);
 
+/* Gradient-slab hook (sequence-parallel overlap): during
+ * mst_block_step[_sp|_host] the library calls fn(user, which, row0, row1,
+ * stream) at enqueue time right after the launch that makes rows
+ * [row0, row1) of weight gradient `which` (numbering as above; rows of the
+ * row-major fp32 gradient, so every slab is one contiguous buffer) final in
+ * stream order.  Every row of every gradient is reported exactly once per
+ * call.  With `slabs` > 1 the chunk-wise schedule cuts the launches that
+ * finalise dW_out (the last head chunk's dW_out GEMM) and dW_gate / dW_up
+ * (the last MLP chunk's dW GEMM) into `slabs` row slabs of H, one launch
+ * each, so a caller that all-reduces each slab as it is reported overlaps
+ * most of the communication with the remaining launches (dW_down is one
+ * slab).  slabs = 1: one report per gradient.  NULL disables. */
+typedef void (*mst_grad_slab_hook)(void* user, int which, int64_t row0, int64_t row1, void* stream);
+MST_API int mst_ctx_set_grad_slab_hook(mst_ctx* ctx, mst_grad_slab_hook fn, void* user, int slabs);
+
 /* make_chunk_plan(N, M) — SPEC.md:286-294.  Writes min(M,N)+1 row bounds
  * into `bounds` (capacity >= min(M,N)+1): chunk c is [bounds[c], bounds[c+1]).
  * Balanced rule: the first N mod M chunks hold ceil(N/M) rows. */

@@ -121,9 +121,6 @@ struct ProblemDesc {
   int32_t map_out0, map_out1, map_out2;  // output tensor maps (TMA store boxes)
   int32_t _pad;
   int64_t ld_aux;
-  void* out0;          // kEpiAccF32 with red.global: output base pointers (halves g = 0, 1)
-  void* out1;
-  int64_t ld0, ld1;
   const float* aux;    // kEpiSwigluBwd: dh [rows, ld_aux] fp32; kEpiDhSwigluBwd: G
   const float* aux2;   // kEpiDhSwigluBwd: U [rows, ld_aux] fp32
   const int32_t* labels;

@@ -136,6 +136,9 @@ struct mst_ctx {
   const void* weights[4] = {nullptr, nullptr, nullptr, nullptr};  // weight tensors of the current call
   mst_grad_ready_hook ready_fn = nullptr;  // optimizer-in-backward hook (mst.h)
   void* ready_user = nullptr;
+  mst_grad_slab_hook slab_fn = nullptr;    // sequence-parallel gradient slabs (mst.h)
+  void* slab_user = nullptr;
+  int slabs = 1;
   int tma3d = 1;  // MN-major operands as 3-D tensor maps (tuning "tma3d")
   // Cross-stream ordering of the context's device scratch (tile counter,
   // global-valid / count scratch): calls are serialised by `mu`, and a call
@@ -221,6 +224,12 @@ struct WeightScope {
 // otherwise the caller frees it after its optimizer step.
 const char* const kGradLabel[4] = {"grad.W_gate", "grad.W_up", "grad.W_down", "grad.W_out"};
 void grad_alloc(mst_ctx* c, int which, uint64_t bytes) { mem_alloc(c, bytes, kGradLabel[which]); }
+
+// Rows [r0, r1) of a weight gradient are final in stream order
+// (mst_ctx_set_grad_slab_hook).
+void grad_slab(mst_ctx* c, int which, int64_t r0, int64_t r1, cudaStream_t st) {
+  if (c->slab_fn && r1 > r0) c->slab_fn(c->slab_user, which, r0, r1, st);
+}
 
 // A weight gradient is final in stream order (mst_ctx_set_grad_ready_hook).
 void grad_ready(mst_ctx* c, int which, cudaStream_t st, uint64_t bytes) {
@@ -379,6 +388,9 @@ double tile_cost(const ProblemDesc& P) {
     case mst::kEpiSwigluBwd: bytes = 3 * 256.0 * 128 * 2 + 256.0 * 128 * 4; break;
     case mst::kEpiCeFwd: bytes = 256.0 * 16; break;
     case mst::kEpiCeBwd: bytes = 256.0 * 256 * 2; break;
+    case mst::kEpiCeFwdNum: bytes = 256.0 * 256 * 2 + 256.0 * 12; break;
+    case mst::kEpiSwigluSave: bytes = 256.0 * 128 * (2 + 4 + 4); break;
+    case mst::kEpiDhSwigluBwd: bytes = 256.0 * 256 * (4 + 4 + 2 + 2); break;
   }
   const double epi = bytes * P.nblk / 46.0;
   return std::max(mma, epi) + 800.0;
@@ -857,8 +869,6 @@ int build_plain(mst_ctx* c, Launch& L, const Operand& a, const Operand& b, void*
     MST_TRY(add_out_map(c, L, out, b.mn, a.mn, ld_out, epi == mst::kEpiAccF32, &P.map_out0));
     P.map_out1 = P.map_out0;
   }
-  P.out0 = P.out1 = out;
-  P.ld0 = P.ld1 = ld_out;
   P.col_off0 = 0;
   P.col_off1 = 128;
   L.flops += 2.0 * a.mn * b.mn * a.k;
@@ -870,10 +880,15 @@ int build_plain(mst_ctx* c, Launch& L, const Operand& a, const Operand& b, void*
 // K9 (dX_j = dG W_g^T + dU W_u^T), K8 (dW_d += h^T dO_j) and K10
 // ([dW_g | dW_u] += X_j^T [dG | dU]) of one chunk: mutually independent,
 // added to one grouped launch (Alg. 3 lines 5-7).
+// parts: bit 1 K9, bit 2 K8, bit 4 K10 restricted to the dW rows [k10_r0, k10_r1)
+// of H (row slabs of the final chunk, mst_ctx_set_grad_slab_hook).
+enum { kGradK9 = 1, kGradK8 = 2, kGradK10 = 4, kGradAll = 7 };
 int add_mlp_grads(mst_ctx* c, Launch& L, const void* dg, const void* du, const void* ht, const void* xt,
                   const void* doj, const void* wg, const void* wu, void* dxj, float* dwg, float* dwu, float* dwd,
-                  int64_t rows, int64_t h, int64_t i, int64_t ldt, int beta) {
-  {  // K9: one accumulator over both phases (B K-major)
+                  int64_t rows, int64_t h, int64_t i, int64_t ldt, int beta, int parts = kGradAll,
+                  int64_t k10_r0 = 0, int64_t k10_r1 = -1) {
+  if (k10_r1 < 0) k10_r1 = h;
+  if (parts & kGradK9) {  // K9: one accumulator over both phases (B K-major)
     ProblemDesc& P = L.p.prob[L.p.num_problems++];
     P.nblk = (c->wide_mask & 8) ? 2 : 1;
     PhaseSpec q0{};
@@ -903,34 +918,36 @@ int add_mlp_grads(mst_ctx* c, Launch& L, const void* dg, const void* du, const v
     cnt_mm(c, rows, i, h, (uint64_t)(h * i));  // dG W_g^T
     cnt_mm(c, rows, i, h, (uint64_t)(h * i));  // dU W_u^T
   }
-  cnt_op(c, (uint64_t)(rows * h), 3ull * rows * h);  // dX' + dX'' (fused: one K = 2I accumulation)
+  if (parts & kGradK9) cnt_op(c, (uint64_t)(rows * h), 3ull * rows * h);  // dX' + dX'' (fused: one K = 2I accumulation)
   // K8: dW_d[I,H] += h^T dO_j (A = h^T, K-major)
-  MST_TRY(build_plain(c, L, Operand{ht, i, rows, ldt, false}, Operand{doj, h, rows, h, true}, dwd, h, mst::kEpiAccF32,
-                      beta));
-  {  // K10: [dW_g | dW_u][H, I] += X_j^T [dG | dU]  (A = X_j^T, K-major)
+  if (parts & kGradK8)
+    MST_TRY(build_plain(c, L, Operand{ht, i, rows, ldt, false}, Operand{doj, h, rows, h, true}, dwd, h,
+                        mst::kEpiAccF32, beta));
+  if ((parts & kGradK10) && k10_r1 > k10_r0) {  // K10: [dW_g | dW_u][H, I] += X_j^T [dG | dU]  (A = X_j^T, K-major)
+    const int64_t hs = k10_r1 - k10_r0;
+    xt = bptr(xt, k10_r0 * ldt);
+    dwg += k10_r0 * i;
+    dwu += k10_r0 * i;
     ProblemDesc& P = L.p.prob[L.p.num_problems++];
     PhaseSpec q{};
-    q.a = {xt, h, rows, ldt, false};
+    q.a = {xt, hs, rows, ldt, false};
     q.b0 = {dg, i, rows, i, true};
     q.b1 = {du, i, rows, i, true};
     q.umma_n = 256;
     MST_TRY(add_phase(c, L, P, q));
-    P.m_tiles = (int)cdiv(h, 256);
+    P.m_tiles = (int)cdiv(hs, 256);
     P.tile_n = 128;
     P.n_tiles = (int)cdiv(i, 128);
-    P.rows = (int)h;
+    P.rows = (int)hs;
     P.cols = (int)i;
     P.epi = mst::kEpiAccF32;
     P.beta = beta;
-    MST_TRY(add_out_map(c, L, dwg, i, h, i, true, &P.map_out0));
-    MST_TRY(add_out_map(c, L, dwu, i, h, i, true, &P.map_out1));
-    P.out0 = dwg;
-    P.out1 = dwu;
-    P.ld0 = P.ld1 = i;
+    MST_TRY(add_out_map(c, L, dwg, i, hs, i, true, &P.map_out0));
+    MST_TRY(add_out_map(c, L, dwu, i, hs, i, true, &P.map_out1));
     P.col_off0 = P.col_off1 = 0;
-    L.flops += 2.0 * h * (2.0 * i) * rows;
-    cnt_mm(c, h, rows, i, 0);  // dW_g += X^T dG
-    cnt_mm(c, h, rows, i, 0);  // dW_u += X^T dU
+    L.flops += 2.0 * hs * (2.0 * i) * rows;
+    cnt_mm(c, hs, rows, i, 0);  // dW_g += X^T dG
+    cnt_mm(c, hs, rows, i, 0);  // dW_u += X^T dU
   }
   return MST_OK;
 }
@@ -1113,6 +1130,15 @@ int mst_ctx_set_mem_hook(mst_ctx* c, mst_mem_hook fn, void* user) {
   c->mem_user = user;
   return MST_OK;
 }
+int mst_ctx_set_grad_slab_hook(mst_ctx* c, mst_grad_slab_hook fn, void* user, int slabs) {
+  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  if (slabs < 1 || slabs > 64) return fail(MST_ERR_CONFIG, "slabs must be 1..64, got %d", slabs);
+  c->slab_fn = fn;
+  c->slab_user = user;
+  c->slabs = fn ? slabs : 1;
+  return MST_OK;
+}
+
 int mst_ctx_set_grad_ready_hook(mst_ctx* c, mst_grad_ready_hook fn, void* user) {
   if (!c) return fail(MST_ERR_STATE, "NULL context");
   c->ready_fn = fn;
@@ -1864,14 +1890,14 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
     L.flops += 2.0 * rows * (2.0 * i) * h;
     return MST_OK;
   };
-  auto add_grads = [&](Launch& L, int j) -> int {
+  auto add_grads = [&](Launch& L, int j, int parts = kGradAll, int64_t k10_r0 = 0, int64_t k10_r1 = -1) -> int {
     const int64_t rows = rows_of(j);
-    if (j == 0)
+    if (j == 0 && (parts & kGradK9))
       for (int wi = 0; wi < 3; ++wi) grad_alloc(c, wi, (uint64_t)h * i * 4);
     const int beta = (j > 0 || accumulate) ? 1 : 0;
-    if (io) MST_CUDA(cudaStreamWaitEvent(st, io->dx_free[j & 1], 0));  // dX of chunk j-2 copied out
+    if (io && (parts & kGradK9)) MST_CUDA(cudaStreamWaitEvent(st, io->dx_free[j & 1], 0));  // dX of chunk j-2 out
     return add_mlp_grads(c, L, dg, du, ht, xt, dO[j & 1], wg, wu, dxdev(j),
-                         dwg, dwu, dwd, rows, h, i, ldt, beta);
+                         dwg, dwu, dwd, rows, h, i, ldt, beta, parts, k10_r0, k10_r1);
   };
   {
     Launch L;
@@ -1922,15 +1948,23 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
       normalize_dlogits_kernel<<<(unsigned)cdiv(hrows * (v / 8), 256), 256, 0, st>>>(
           static_cast<uint16_t*>(dl), v, (int)hrows, (int)v, part, nparts, lse + hr0, labels + hr0, scales + k, zt);
       c->launches += 3;
-      {  // K5 + K6
+      // K5 + K6.  The last head chunk's K6 finalises dW_out: with a slab hook
+      // it is cut into row slabs of H, one launch each (K5 rides in the
+      // first), and each slab is handed to the hook as soon as it is enqueued.
+      const bool last_head = k == nch_h - 1;
+      const int64_t per = (last_head && c->slab_fn && c->slabs > 1) ? cdiv(cdiv(h, 256), c->slabs) * 256 : h;
+      for (int64_t s0 = 0; s0 < h; s0 += per) {
+        const int64_t s1 = std::min(h, s0 + per);
         Launch L;
-        MST_TRY(build_plain(c, L, Operand{dl, hrows, v, v, false}, Operand{wout, h, v, v, false}, dok, h,
-                            mst::kEpiStoreBf16, 0, (c->wide_mask & 2) ? 2 : 1));
-        MST_TRY(build_plain(c, L, Operand{ot, h, hrows, ldt_h, false}, Operand{dl, v, hrows, v, true}, dwout, v,
-                            mst::kEpiAccF32, hbeta));
+        if (s0 == 0)
+          MST_TRY(build_plain(c, L, Operand{dl, hrows, v, v, false}, Operand{wout, h, v, v, false}, dok, h,
+                              mst::kEpiStoreBf16, 0, (c->wide_mask & 2) ? 2 : 1));
+        MST_TRY(build_plain(c, L, Operand{bptr(ot, s0 * ldt_h), s1 - s0, hrows, ldt_h, false},
+                            Operand{dl, v, hrows, v, true}, dwout + s0 * v, v, mst::kEpiAccF32, hbeta));
         MST_TRY(launch(c, st, L));
+        if (last_head) grad_slab(c, 3, s0, s1, st);
       }
-      if (k == nch_h - 1) grad_ready(c, 3, st, (uint64_t)h * v * 4);  // dW_out complete
+      if (last_head) grad_ready(c, 3, st, (uint64_t)h * v * 4);  // dW_out complete
       mem_free(c, (uint64_t)hrows * v * 2, "inter.head.dlogits");
       mem_free(c, part_bytes, "inter.head.partials");
       mem_free(c, (uint64_t)hrows * h * 2, "act.oT");
@@ -1983,13 +2017,23 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
       MST_TRY(launch(c, st, L));
     }
   }
-  {
-    Launch L;
-    MST_TRY(add_grads(L, nch - 1));
-    MST_TRY(launch(c, st, L));
+  {  // the last chunk's K9 / K8 / K10 finalise dX and dW_{down,gate,up}; with a
+     // slab hook K10 is cut into row slabs of H (K9 and K8 ride in the first)
+    const int64_t per = (c->slab_fn && c->slabs > 1) ? cdiv(cdiv(h, 256), c->slabs) * 256 : h;
+    for (int64_t s0 = 0; s0 < h; s0 += per) {
+      const int64_t s1 = std::min(h, s0 + per);
+      Launch L;
+      MST_TRY(add_grads(L, nch - 1, s0 == 0 ? kGradAll : kGradK10, s0, s1));
+      MST_TRY(launch(c, st, L));
+      if (s0 == 0) {
+        grad_slab(c, 2, 0, i, st);
+        if (io) MST_TRY(d2h(nch - 1));  // the last dX chunk out
+      }
+      grad_slab(c, 0, s0, s1, st);
+      grad_slab(c, 1, s0, s1, st);
+    }
     grads_live(nch - 1, false);
-    if (io) {  // the last dX chunk out, and the compute stream joins the copies
-      MST_TRY(d2h(nch - 1));
+    if (io) {  // the compute stream joins the copies
       MST_CUDA(cudaEventRecord(io->done, io->cs));
       MST_CUDA(cudaStreamWaitEvent(st, io->done, 0));
     }
@@ -2096,9 +2140,13 @@ int mst_block_step_sp(mst_ctx* c, void* stream, const void* x, const int32_t* la
                                &hs));
     MST_TRY(mst_lmhead_backward(c, stream, &hs, wout, stats, grad_loss, dO, dwout, accumulate, rest, rest_bytes));
   }
+  grad_slab(c, 3, 0, h, static_cast<cudaStream_t>(stream));
   grad_ready(c, 3, static_cast<cudaStream_t>(stream), (uint64_t)h * v * 4);
   for (int wi = 0; wi < 3; ++wi) grad_alloc(c, wi, (uint64_t)h * i * 4);
   MST_TRY(mst_mlp_backward(c, stream, dO, &ms, wg, wu, wd, dx, dwg, dwu, dwd, accumulate, rest, rest_bytes));
+  grad_slab(c, 2, 0, i, static_cast<cudaStream_t>(stream));
+  grad_slab(c, 0, 0, h, static_cast<cudaStream_t>(stream));
+  grad_slab(c, 1, 0, h, static_cast<cudaStream_t>(stream));
   for (int wi = 0; wi < 3; ++wi) grad_ready(c, wi, static_cast<cudaStream_t>(stream), (uint64_t)h * i * 4);
   return MST_OK;
 }

@@ -169,6 +169,9 @@ _SIGS.update({  # decoder-layer plumbing (model module), used b
 })
 
 _GRAD_READY_HOOK = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p)
+# mst_grad_slab_hook(user, which, row0, row1, stream)
+_GRAD_SLAB_HOOK = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p)
+_SIGS["mst_ctx_set_grad_slab_hook"] = ([_VP, _VP, _VP, _I32], ctypes.c_int)
 
 
 class _Counters(ctypes.Structure):
@@ -617,7 +620,7 @@ def block_step(X: torch.Tensor, L: torch.Tensor, mlp: MlpWeights, head: LmHeadWe
                mode: int = TOKEN_WEIGHTED, grad_loss: float = 1.0, grads: Optional[BlockGrads] = None,
                stats: Optional[torch.Tensor] = None, accumulate: bool = False,
                workspace: Optional[torch.Tensor] = None, check: bool = False,
-               global_valid: Optional[torch.Tensor] = None, grad_ready=None):
+               global_valid: Optional[torch.Tensor] = None, grad_ready=None, grad_slab=None, slabs: int = 1):
     """One MLP -> LM-Head block, forward + backward (the unit the paper times,
     PAPER.md:475).  Returns (stats, grads); stats[2] is the loss.
     check=True surfaces the SPEC's errors synchronously: NonFiniteError for
@@ -627,7 +630,11 @@ def block_step(X: torch.Tensor, L: torch.Tensor, mlp: MlpWeights, head: LmHeadWe
     sequence-parallel group (mst_block_step_sp).  grad_ready(which): called
     while the step is enqueued, right after the launch that makes gradient
     `which` (0 W_gate, 1 W_up, 2 W_down, 3 W_out) final in stream order
-    (mst_ctx_set_grad_ready_hook)."""
+    (mst_ctx_set_grad_ready_hook).  grad_slab(which, row0, row1): called
+    as rows [row0, row1) of gradient `which` become final; `slabs` > 1 cuts
+    the finalising launches into that many row slabs (mst_ctx_set_grad_slab_hook:
+    the sequence-parallel all-reduce overlap).  Exceptions raised inside either
+    callback are re-raised after the step is enqueued."""
     if check:
         check_finite(X=X, W_gate=mlp.W_gate, W_up=mlp.W_up, W_down=mlp.W_down, W_out=head.W_out)
     ctx = Context.get(X.device.index)
@@ -649,10 +656,22 @@ def block_step(X: torch.Tensor, L: torch.Tensor, mlp: MlpWeights, head: LmHeadWe
     ws = workspace if workspace is not None else ctx.workspace(need)
     if global_valid is not None:
         _req(global_valid, "global_valid", torch.float32, (1,))
-    hook = None
+    hook = slab_hook = None
+    errors = []
+
+    def guarded(fn, *a):  # ctypes prints and drops callback exceptions: keep them
+        try:
+            fn(*a)
+        except BaseException as exc:  # noqa: BLE001
+            errors.append(exc)
+
     if grad_ready is not None:
-        hook = _GRAD_READY_HOOK(lambda _u, which, _s: grad_ready(int(which)))
+        hook = _GRAD_READY_HOOK(lambda _u, which, _s: guarded(grad_ready, int(which)))
         _check(ctx.lib.mst_ctx_set_grad_ready_hook(ctx.handle, ctypes.cast(hook, ctypes.c_void_p), None))
+    if grad_slab is not None:
+        slab_hook = _GRAD_SLAB_HOOK(lambda _u, which, r0, r1, _s: guarded(grad_slab, int(which), int(r0), int(r1)))
+        _check(ctx.lib.mst_ctx_set_grad_slab_hook(ctx.handle, ctypes.cast(slab_hook, ctypes.c_void_p), None,
+                                                  int(slabs)))
     try:
         _check(ctx.lib.mst_block_step_sp(ctx.handle, _stream(X), X.data_ptr(), L.data_ptr(), mlp.W_gate.data_ptr(),
                                          mlp.W_up.data_ptr(), mlp.W_down.data_ptr(), head.W_out.data_ptr(), N, H, I,
@@ -663,6 +682,10 @@ def block_step(X: torch.Tensor, L: torch.Tensor, mlp: MlpWeights, head: LmHeadWe
     finally:
         if hook is not None:
             _check(ctx.lib.mst_ctx_set_grad_ready_hook(ctx.handle, None, None))
+        if slab_hook is not None:
+            _check(ctx.lib.mst_ctx_set_grad_slab_hook(ctx.handle, None, None, 1))
+    if errors:
+        raise errors[0]
     if check:
         s = stats[:4].tolist()
         if s[3] > 0:

@@ -8,9 +8,12 @@ mini-sequence pipeline on it.  The only cross-rank traffic is:
      so every rank scales its dlogits by the GLOBAL count (token-weighted
      loss) — the per-rank gradients then already sum to the
      P=1 gradient; then the (loss sum, valid) pair for the reported loss;
-  2. the weight gradients: all-reduce SUM.  dW_out is final after the head
-     and is reduced asynchronously while the MLP backward runs;
-     dW_{gate,up,down} are reduced at the end.
+  2. the weight gradients: all-reduce SUM.  On the fused chunk-wise block
+     (sp_block_step_fused) each row slab is reduced asynchronously as soon
+     as the library reports it final (mst_ctx_set_grad_slab_hook), so the
+     reduction overlaps the last chunks' launches; sp_block_step (the SPEC
+     op sequence) reduces dW_out while the MLP backward runs and
+     dW_{gate,up,down} at the end.
 
 The collective backend is whatever torch.distributed was initialised with:
 NCCL over NVLink on B200 boxes, gloo in the CPU tests.  The compute is an
@@ -76,40 +79,55 @@ class GpuOps:
         g = self.ms.MlpGrads(*grads)
         return self.ms.miniseq_mlp_backward(dO, saved, self.ms.MlpWeights(*w), saved.plan, grads=g)[0]
 
-    def block_step(self, X, L, w, Wout, M_mlp, M_head, grads, global_valid, grad_ready, workspace=None, stats=None):
+    def block_step(self, X, L, w, Wout, M_mlp, M_head, grads, global_valid, grad_slab, slabs=1, workspace=None,
+                   stats=None):
         """The whole fused block (mst_block_step_sp, chunk-wise schedule) with the
-        global valid count; grad_ready(which) fires as each dW becomes final."""
+        global valid count; grad_slab(which, r0, r1) fires as rows of each dW
+        become final (`slabs` row slabs for dW_out / dW_gate / dW_up)."""
         ms = self.ms
         N, H = X.shape
         bg = ms.BlockGrads(dX=torch.empty(N, H, device=X.device, dtype=torch.bfloat16), W_gate=grads[0],
                            W_up=grads[1], W_down=grads[2], W_out=grads[3]) if not isinstance(grads, ms.BlockGrads) \
             else grads
         stats, bg = ms.block_step(X, L, ms.MlpWeights(*w), ms.LmHeadWeights(Wout), M_mlp, M_head, grads=bg,
-                                  stats=stats, workspace=workspace, global_valid=global_valid, grad_ready=grad_ready)
+                                  stats=stats, workspace=workspace, global_valid=global_valid, grad_slab=grad_slab,
+                                  slabs=slabs)
         return stats, bg.dX
 
 
 def sp_block_step_fused(ops, X: torch.Tensor, L: torch.Tensor, w: tuple, Wout: torch.Tensor, M_mlp: int,
-                        M_head: int, grads: tuple, group=None, overlap: bool = True, **kw) -> StepResult:
+                        M_head: int, grads: tuple, group=None, overlap: bool = True, slabs: int = 4,
+                        **kw) -> StepResult:
     """Sequence-parallel step on the fused chunk-wise block (the fast path):
     one all-reduce of the valid count before the step, the block itself with
-    the global count (mst_block_step_sp), each weight gradient's SUM
-    all-reduce issued from the library's gradient-ready hook the moment it is
-    final (dW_out after the LM-Head backward of the last chunk, overlapping
-    that chunk's MLP backward; the MLP gradients at the end), then the loss
-    pair.  Same results as sp_block_step (tests/test_dist_gloo.py)."""
+    the global count (mst_block_step_sp), then each weight gradient's SUM
+    all-reduce issued per row slab from the library's gradient-slab hook the
+    moment the slab is final: dW_out's slabs during the last head chunk's
+    launches (overlapping them and the last chunk's MLP backward), dW_down
+    and the dW_gate / dW_up slabs during the last MLP chunk's launches; only
+    the last slab's reduction is exposed.  Then the loss pair.  Same results
+    as sp_block_step (tests/test_dist_gloo.py)."""
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     valid = ops.count_valid(L, Wout.shape[1])
     if world > 1:
-        dist.all_reduce(valid, op=dist.ReduceOp.SUM, group=group)
+        # fp32 counts are exact integers per rank (< 2^24 tokens); the sum is
+        # formed in fp64 and rounded once
+        v64 = valid.double()
+        dist.all_reduce(v64, op=dist.ReduceOp.SUM, group=group)
+        valid.copy_(v64)
     works = []
+    reported = {}
     gl = (grads.W_gate, grads.W_up, grads.W_down, grads.W_out) if hasattr(grads, "W_out") else tuple(grads)
 
-    def ready(which: int) -> None:
+    def slab(which: int, r0: int, r1: int) -> None:
+        reported[which] = reported.get(which, 0) + (r1 - r0)
         if world > 1:
-            works.append(dist.all_reduce(gl[which], op=dist.ReduceOp.SUM, group=group, async_op=overlap))
+            works.append(dist.all_reduce(gl[which][r0:r1], op=dist.ReduceOp.SUM, group=group, async_op=overlap))
 
-    stats, dX = ops.block_step(X, L, w, Wout, M_mlp, M_head, grads, valid, ready, **kw)
+    stats, dX = ops.block_step(X, L, w, Wout, M_mlp, M_head, grads, valid, slab, slabs, **kw)
+    for k, t in enumerate(gl):  # every gradient row reduced exactly once
+        if reported.get(k) != t.shape[0]:
+            raise RuntimeError(f"gradient {k}: {reported.get(k)} of {t.shape[0]} rows reported final")
     gstats = stats.clone()
     if world > 1:
         head = gstats[:2].contiguous()

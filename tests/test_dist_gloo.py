@@ -55,15 +55,21 @@ class OracleOps:
             g.copy_(torch.from_numpy(v))
         return torch.from_numpy(dX)
 
-    def block_step(self, X, L, w, Wout, M_mlp, M_head, grads, global_valid, grad_ready):
-        """Stand-in for GpuOps.block_step (mst_block_step_sp): same call order
-        of the gradient-ready hook (W_out after the head, MLP weights at the end)."""
+    def block_step(self, X, L, w, Wout, M_mlp, M_head, grads, global_valid, grad_slab, slabs=1):
+        """Stand-in for GpuOps.block_step (mst_block_step_sp): same order of the
+        gradient-slab reports (dW_out's row slabs after the head, then dW_down
+        whole and the dW_gate / dW_up slabs), slabs of ceil(rows / slabs)."""
         O, ms = self.mlp_forward(X, w, M_mlp)
         stats, dO = self.lmhead_fused(O, L, Wout, M_head, global_valid, grads[3])
-        grad_ready(3)
+        H = X.shape[1]
+        per = -(-H // slabs)
+        for r0 in range(0, H, per):
+            grad_slab(3, r0, min(H, r0 + per))
         dX = self.mlp_backward(dO, ms, w, grads[:3])
-        for k in range(3):
-            grad_ready(k)
+        grad_slab(2, 0, grads[2].shape[0])
+        for r0 in range(0, H, per):
+            grad_slab(0, r0, min(H, r0 + per))
+            grad_slab(1, r0, min(H, r0 + per))
         return stats, dX
 
 
@@ -87,7 +93,7 @@ def _worker(rank, world, port, ret, mode):
         w = (f(c["Wg"]), f(c["Wu"]), f(c["Wd"]))
         grads = tuple(torch.zeros_like(t) for t in (*w, f(c["Wout"])))
         if mode == "block":  # the bench's fast path: whole fused block + hook-driven gradient all-reduces
-            r = sp_block_step_fused(OracleOps(orc), X, L, w, f(c["Wout"]), M_MLP, M_HEAD, grads)
+            r = sp_block_step_fused(OracleOps(orc), X, L, w, f(c["Wout"]), M_MLP, M_HEAD, grads, slabs=3)
         else:
             r = sp_block_step(OracleOps(orc), X, L, w, f(c["Wout"]), M_MLP, M_HEAD, grads, fused=mode == "fused")
         ref = orc.block(c["X"], c["L"], c["Wg"], c["Wu"], c["Wd"], c["Wout"], M_MLP, M_HEAD, round_bf16=False)
