@@ -64,6 +64,33 @@ def build_lib(force: bool = False, verbose: bool = False, out: Path | None = Non
     return target
 
 
+CPP_BIN = ROOT / "tests" / "cpp" / "_bin"
+
+
+def build_cpp_device(ref_include: Path | None = None, out: Path | None = None) -> Path:
+    """Compile tests/cpp/device_run.cpp (the C++ binding run on the GPU,
+    tests/test_cpp_device.py) against libmst.so; with the reference's headers
+    on the include path it forwards the library's memory events into the
+    reference's own minitrain::MemTracker.  Host compile only (g++ + the
+    CUDA runtime), so it builds here and travels to the GPU box prebuilt."""
+    lib = build_lib()
+    target = out or (CPP_BIN / "device_run")
+    target.parent.mkdir(parents=True, exist_ok=True)
+    cuda = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
+    cxx = "/usr/bin/g++" if Path("/usr/bin/g++").exists() else (shutil.which("g++") or "g++")
+    cmd = [cxx, "-std=c++20", "-O2", "-Wall", "-Wextra", "-I", str(ROOT / "include"), "-I", str(cuda / "include")]
+    if ref_include is not None:
+        cmd += ["-I", str(ref_include)]
+    else:
+        cmd += ["-DMST_STANDALONE_ERRORS"]
+    cmd += [str(ROOT / "tests" / "cpp" / "device_run.cpp"), str(lib), f"-Wl,-rpath,{lib.parent}",
+            "-L", str(cuda / "lib64"), "-lcudart", f"-Wl,-rpath,{cuda / 'lib64'}", "-o", str(target)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"g++ failed ({res.returncode}):\n{' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
+    return target
+
+
 if __name__ == "__main__":
     import sys
 
