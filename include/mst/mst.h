@@ -94,9 +94,23 @@ typedef struct mst_lmhead_saved {
 MST_API int mst_abi_version(void);
 MST_API const char* mst_last_error(void);
 
-/* Context: one per host thread per device (SPEC.md:99 threading contract). */
+/* Context: one per host thread per device (SPEC.md:99 threading contract).
+ * Calls on one context are serialised by a context lock, and a call on a
+ * different stream than the previous call first waits (device-side event)
+ * for the previous call's work: the context's device scratch (tile counter,
+ * valid-count scratch) is shared by its calls, the stream is per call.  For
+ * concurrent work on several streams use one context per stream.
+ *
+ * Deferred errors: data errors that only the device can see -- every label
+ * ignored (DataError), labels outside [0, V) other than -100
+ * (DataError), a non-finite loss (NonFiniteError) -- are raised
+ * into the context's sticky error word by the kernel that computes the loss.
+ * The first call that starts after that kernel has completed returns the
+ * error (and clears it) without doing any work; mst_ctx_check synchronises
+ * `stream` and returns it at once. */
 MST_API int mst_ctx_create(int device, mst_ctx** out);
 MST_API void mst_ctx_destroy(mst_ctx* ctx);
+MST_API int mst_ctx_check(mst_ctx* ctx, void* stream);
 /* Number of CTA pairs a grouped launch uses (diagnostics / tests). */
 MST_API int mst_ctx_num_pairs(const mst_ctx* ctx);
 /* Kernel launches issued by this context since creation (bench evidence). */

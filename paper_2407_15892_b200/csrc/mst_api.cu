@@ -140,6 +140,9 @@ struct mst_ctx {
   void* slab_user = nullptr;
   int slabs = 1;
   int tma3d = 1;  // MN-major operands as 3-D tensor maps (tuning "tma3d")
+  // Deferred (sticky) data errors raised by the device (mst.h): host-mapped word
+  unsigned int* err_host = nullptr;
+  unsigned int* err_dev = nullptr;
   // Cross-stream ordering of the context's device scratch (tile counter,
   // global-valid / count scratch): calls are serialised by `mu`, and a call
   // on a different stream than the previous one waits for `tail_ev`, which
@@ -151,6 +154,17 @@ struct mst_ctx {
 };
 
 namespace {
+
+// Deferred data errors (mst.h): a kernel of an earlier call flagged the
+// context's host-mapped error word; the next call reports and clears it.
+int take_sticky(mst_ctx* c) {
+  if (!c->err_host) return MST_OK;
+  const unsigned int f = __atomic_exchange_n(c->err_host, 0u, __ATOMIC_ACQ_REL);
+  if (f & 1u) return fail(MST_ERR_DATA, "deferred error from an earlier call: all labels ignored, loss undefined (SPEC.md:219)");
+  if (f & 2u) return fail(MST_ERR_DATA, "deferred error from an earlier call: labels outside [0, V) and != -100");
+  if (f & 4u) return fail(MST_ERR_NONFINITE, "deferred error from an earlier call: non-finite loss (SPEC.md:26)");
+  return MST_OK;
+}
 
 // One public call on a context: holds the context lock for the call and
 // orders the call after the previous call's work when the stream changes
@@ -164,6 +178,7 @@ struct CtxCall {
     if (c->has_last && c->last_stream != st && c->tail_ev) {
       if (cudaStreamWaitEvent(st, c->tail_ev, 0) != cudaSuccess) status = MST_ERR_CUDA;
     }
+    if (status == MST_OK) status = take_sticky(c);
   }
   ~CtxCall() {
     if (!c->tail_ev) cudaEventCreateWithFlags(&c->tail_ev, cudaEventDisableTiming);
@@ -573,8 +588,11 @@ __global__ void chunk_reduce_kernel(const float* __restrict__ loss_row, const in
   }
 }
 
-// stats[0..3] from the per-chunk entries (SPEC.md:316-317 loss modes).
-__global__ void finalize_loss_kernel(float* stats, int m, int mode) {
+// stats[0..3] from the per-chunk entries (SPEC.md:316-317 loss modes).  The
+// SPEC's data errors are also raised into the context's sticky error word
+// (host-mapped; mst.h "Deferred errors"): 1 = every label ignored
+// (SPEC.md:219), 2 = labels outside [0, V) other than -100, 4 = non-finite loss.
+__global__ void finalize_loss_kernel(float* stats, int m, int mode, unsigned int* err, const float* gvalid) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double s = 0, v = 0, pm = 0;
   int nonempty = 0;
@@ -590,6 +608,16 @@ __global__ void finalize_loss_kernel(float* stats, int m, int mode) {
   stats[0] = (float)s;
   stats[1] = (float)v;
   stats[2] = mode == MST_LOSS_PAPER_MEAN ? (float)(pm / m) : (float)(s / v);
+  if (err) {
+    // a sequence shard with no valid label is fine when the global count is not 0
+    const double vall = gvalid ? (double)*gvalid : v;
+    const unsigned int f =
+        (vall == 0 ? 1u : 0u) | (stats[3] > 0.f ? 2u : 0u) | ((v > 0 && !isfinite(stats[2])) ? 4u : 0u);
+    if (f) {
+      atomicOr_system(err, f);
+      __threadfence_system();
+    }
+  }
 }
 
 // Per-chunk dlogits scale: grad_loss / valid_global (token-weighted) or
@@ -1010,6 +1038,11 @@ int mst_ctx_create(int device, mst_ctx** out) {
   c->max_pairs = c->num_pairs;
   e = cudaMalloc(&c->scratch_dev, 4096);
   if (e == cudaSuccess) e = cudaMemset(c->scratch_dev, 0, 4096);
+  if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void**>(&c->err_host), 64, cudaHostAllocMapped);
+  if (e == cudaSuccess) {
+    *c->err_host = 0;
+    e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->err_dev), c->err_host, 0);
+  }
   if (e != cudaSuccess) {
     delete c;
     return fail(MST_ERR_CUDA, "cudaMalloc: %s", cudaGetErrorString(e));
@@ -1027,6 +1060,7 @@ void mst_ctx_destroy(mst_ctx* c) {
   for (cudaEvent_t e : c->io_ev)
     if (e) cudaEventDestroy(e);
   if (c->tail_ev) cudaEventDestroy(c->tail_ev);
+  if (c->err_host) cudaFreeHost(c->err_host);
   delete c;
 }
 
@@ -1130,6 +1164,13 @@ int mst_ctx_set_mem_hook(mst_ctx* c, mst_mem_hook fn, void* user) {
   c->mem_user = user;
   return MST_OK;
 }
+int mst_ctx_check(mst_ctx* c, void* stream) {
+  if (!c) return fail(MST_ERR_STATE, "NULL context");
+  std::lock_guard<std::recursive_mutex> lk(c->mu);
+  MST_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  return take_sticky(c);
+}
+
 int mst_ctx_set_grad_slab_hook(mst_ctx* c, mst_grad_slab_hook fn, void* user, int slabs) {
   if (!c) return fail(MST_ERR_STATE, "NULL context");
   if (slabs < 1 || slabs > 64) return fail(MST_ERR_CONFIG, "slabs must be 1..64, got %d", slabs);
@@ -1517,7 +1558,7 @@ int mst_lmhead_forward(mst_ctx* c, void* stream, const void* x, const int32_t* l
     c->launches += 2;
     mem_free(c, part_bytes, "inter.head.partials");
   }
-  finalize_loss_kernel<<<1, 32, 0, st>>>(stats, nch, loss_mode);
+  finalize_loss_kernel<<<1, 32, 0, st>>>(stats, nch, loss_mode, c->err_dev, nullptr);
   c->launches += 1;
   MST_CUDA(cudaGetLastError());
   if (saved) {
@@ -1671,7 +1712,7 @@ int mst_lmhead_fused(mst_ctx* c, void* stream, const void* x, const int32_t* lab
     mem_free(c, part_bytes, "inter.head.partials");
     mem_free(c, (uint64_t)rows * h * 2, "act.xT");
   }
-  finalize_loss_kernel<<<1, 32, 0, st>>>(stats, nch, loss_mode);
+  finalize_loss_kernel<<<1, 32, 0, st>>>(stats, nch, loss_mode, c->err_dev, global_valid);
   c->launches += 1;
   MST_CUDA(cudaGetLastError());
   return MST_OK;
@@ -2042,7 +2083,7 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
   mem_free(c, (uint64_t)n * 4, "act.lse");
   mem_free(c, 2 * act_bytes, "act.dO");
   mem_free(c, act_bytes, "act.O");
-  finalize_loss_kernel<<<1, 32, 0, st>>>(stats, nch_h, loss_mode);
+  finalize_loss_kernel<<<1, 32, 0, st>>>(stats, nch_h, loss_mode, c->err_dev, global_valid);
   c->launches += 1;
   MST_CUDA(cudaGetLastError());
   return MST_OK;

@@ -172,6 +172,7 @@ _GRAD_READY_HOOK = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int, ctypes.
 # mst_grad_slab_hook(user, which, row0, row1, stream)
 _GRAD_SLAB_HOOK = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p)
 _SIGS["mst_ctx_set_grad_slab_hook"] = ([_VP, _VP, _VP, _I32], ctypes.c_int)
+_SIGS["mst_ctx_check"] = ([_VP, _VP], ctypes.c_int)
 
 
 class _Counters(ctypes.Structure):
@@ -270,6 +271,15 @@ class Context:
         self._hooks = (_MEM_HOOK(mem), _COUNT_HOOK(cnt))  # keep the trampolines alive
         _check(self.lib.mst_ctx_set_mem_hook(self.handle, ctypes.cast(self._hooks[0], ctypes.c_void_p), None))
         _check(self.lib.mst_ctx_set_count_hook(self.handle, ctypes.cast(self._hooks[1], ctypes.c_void_p), None))
+
+    def check(self, stream: Optional[int] = None) -> None:
+        """Synchronise `stream` (default: the current stream) and raise the
+        context's deferred device-side error, if any (mst_ctx_check: all
+        labels ignored / invalid labels -> DataError, non-finite loss ->
+        NonFiniteError); clears it."""
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+        _check(self.lib.mst_ctx_check(self.handle, stream))
 
     def set_tuning(self, key: str, value: int) -> None:
         """Engine tuning / diagnostic knobs (mst_ctx_set_tuning in mst.h)."""
@@ -488,6 +498,7 @@ def check_lmhead_stats(saved: LmHeadSaved) -> None:
     """Host-side checks the asynchronous C ABI defers (forces a sync):
     invalid label ids (DataError) and all-ignored input."""
     s = saved.stats[:4].tolist()
+    Context.get(saved.stats.device.index).check()  # consumes the deferred flag this forward raised
     if s[3] > 0:
         raise DataError(f"{int(s[3])} labels outside [0, V) and != -100")
     if s[1] == 0:
@@ -688,6 +699,7 @@ def block_step(X: torch.Tensor, L: torch.Tensor, mlp: MlpWeights, head: LmHeadWe
         raise errors[0]
     if check:
         s = stats[:4].tolist()
+        ctx.check()  # the deferred device-side error of this step, if any
         if s[3] > 0:
             raise DataError(f"{int(s[3])} labels outside [0, V) and != -100")
         if s[1] == 0:
