@@ -176,7 +176,8 @@ struct CtxCall {
   int status = MST_OK;
   CtxCall(mst_ctx* ctx, void* stream) : c(ctx), st(static_cast<cudaStream_t>(stream)), lk(ctx->mu) {
     if (c->has_last && c->last_stream != st && c->tail_ev) {
-      if (cudaStreamWaitEvent(st, c->tail_ev, 0) != cudaSuccess) status = MST_ERR_CUDA;
+      if (cudaStreamWaitEvent(st, c->tail_ev, 0) != cudaSuccess)
+        status = fail(MST_ERR_CUDA, "cross-stream ordering: cudaStreamWaitEvent failed");
     }
     if (status == MST_OK) status = take_sticky(c);
   }
@@ -190,7 +191,7 @@ struct CtxCall {
 #define MST_CALL(ctx, stream)                                                              \
   if (!(ctx)) return fail(MST_ERR_STATE, "NULL context");                                 \
   CtxCall call_guard_(ctx, stream);                                                        \
-  if (call_guard_.status != MST_OK) return fail(MST_ERR_CUDA, "cross-stream ordering failed")
+  if (call_guard_.status != MST_OK) return call_guard_.status
 
 // ------------------------------------------------------------ memtrack side
 // count_matmul / count_op of memtrack.hpp:163-175 (conventions at :19-35).
