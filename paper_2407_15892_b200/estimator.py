@@ -10,12 +10,20 @@ module restricted to what this repository builds.
                                       the cross-check of predict_peak against
                                       tracked device allocations
 
-Not reproduced: predict_peak's whole-model Appendix D rows (weights /
-gradients / optimizer / activation for Llama3-8B, Tables 4-7) — those need
-the full model's activation inventory under the paper's PyTorch allocator.
+  predict_peak(cfg, S, B, M_mlp, M_head, recompute, in_backward, convention)
+                                      SPEC.md:590-596 -> MemBreakdown (SPEC.md:546-549):
+                                      "paper"  the Appendix D convention (PAPER.md:665-777:
+                                               bf16 weights / gradients / Adam moments, the
+                                               HF-Llama saved-tensor inventory);
+                                      "repo"   this repository's model.py + optim.AdamW
+                                               (bf16 weights, fp32 gradients, fp32 master +
+                                               moments, model.py's saved set, libmst's
+                                               chunk workspace) -- cross-checked against
+                                               tracked device allocations (tests/test_gpu_estimator.py)
 """
 from __future__ import annotations
 
+from dataclasses import dataclass, field
 from fractions import Fraction
 from typing import Dict
 
@@ -61,3 +69,130 @@ def predict_block_peak(N: int, H: int, I: int, V: int, M: int, M_head: int | Non
     inter = max(mlp, 10 * n * I + head)
     return {"inter.mlp.": mlp, "inter.head.": head, "inter.": inter, "act.O": n * H * 2, "act.dO": 2 * n * H * 2,
             "act.lse": N * 4}
+
+
+# ------------------------------------------------------------------ predict_peak
+@dataclass
+class MemBreakdown:
+    """bytes per component at the predicted peak; formulas
+    recorded as strings for the report.  total == sum of the components."""
+    weights: int
+    gradients: int
+    optimizer: int
+    activation: int
+    peak_intermediate: int
+    phase: str = ""
+    formulas: Dict[str, str] = field(default_factory=dict)
+
+    def __post_init__(self):
+        for k in ("weights", "gradients", "optimizer", "activation", "peak_intermediate"):
+            if getattr(self, k) < 0:
+                raise ValueError(f"{k} < 0")
+
+    @property
+    def total(self) -> int:
+        return self.weights + self.gradients + self.optimizer + self.activation + self.peak_intermediate
+
+    def rows(self, unit: float = 2 ** 30) -> Dict[str, float]:
+        """The `estimate` report rows: weights, gradients,
+        optimizer, activation, peak-intermediate, total (GiB by default, the
+        unit of Appendix D's "GB")."""
+        return {k: getattr(self, k) / unit for k in ("weights", "gradients", "optimizer", "activation",
+                                                     "peak_intermediate", "total")}
+
+
+def param_counts(d: int, I: int, V: int, heads: int, G: int, layers: int) -> Dict[str, int]:
+    """Parameters of the Llama-style decoder: untied
+    embedding and W_out, per layer W_qkv [d, d + 2d/G], W_o, three MLP
+    matrices, two RMSNorm gains; the final gain."""
+    kv = d // G
+    mats = V * d + layers * (d * (d + 2 * kv) + d * d + 3 * d * I) + d * V
+    gains = layers * 2 * d + d
+    return {"matrices": mats, "gains": gains, "total": mats + gains}
+
+
+def _paper_activation(d, I, V, G, L, N, M_mlp, M_head, recompute) -> Dict[str, int]:
+    """Appendix D's activation (bf16, HF Llama with FlashAttention2): per layer
+    the saved tensors 11 N d (two fp32 RMSNorm inputs counted double, their
+    outputs, q/k/v incl. the pre-rotary copies, attention output) + 4 N I
+    (the MLP input products G, silu(G), U, h) elements; the head keeps bf16
+    logits, their fp32 copy and the fp32 log-softmax: N V (2 + 4 + 4) bytes.
+    Recompute keeps one N d layer input per layer and rebuilds one layer at a
+    time; MsT divides the MLP and head intermediates by M_mlp / M_head."""
+    layer_d, layer_i = 11 * N * d * 2, 4 * N * I * 2
+    head = N * V * 10
+    if not recompute:
+        return {"saved": L * (layer_d + layer_i), "inter": head}
+    return {"saved": L * N * d * 2, "inter": layer_d + layer_i // M_mlp + head // M_head}
+
+
+def _repo_activation(d, I, V, G, L, N, M_mlp, M_head, recompute) -> Dict[str, int]:
+    """model.py's saved set (bf16 unless noted): per layer the residual sum xs,
+    and unless per-layer recompute: a = rmsnorm(xs), qkv [N, d + 2d/G], the
+    attention output o, x2, b = rmsnorm(x2) and two fp32 rstd rows; then the
+    final norm's input / rstd, the head-input gradient dF, the LM-Head lse and
+    the int32 tokens / labels.  Intermediates: libmst's persistent context
+    workspace (the largest of the MLP and LM-Head chunk workspaces) plus one
+    layer's transient backward buffers (dqkv, da, do, db, dx, the attention
+    gradients) -- and with recompute the rebuilt layer's saved set."""
+    from . import miniseq as ms
+
+    kv = d // G
+    per_layer_full = N * (6 * d + 2 * kv) * 2 + 8 * N
+    saved = L * (N * d * 2 if recompute else per_layer_full) + N * d * 2 * 3 + 4 * N * 2 + 8 * N
+    lib = ms.load_library()
+    import ctypes
+
+    a, b = ctypes.c_size_t(), ctypes.c_size_t()
+    ms._check(lib.mst_mlp_workspace(N, d, I, M_mlp, ctypes.byref(a)))
+    ms._check(lib.mst_lmhead_workspace(N, d, V, M_head, ctypes.byref(b)))
+    ws = max(a.value, b.value)
+    transient = N * (d + 2 * kv) * 2 * 2 + N * d * 2 * 4
+    return {"saved": saved, "inter": ws + transient + (per_layer_full if recompute else 0)}
+
+
+def predict_peak(d: int, I: int, V: int, heads: int, G: int, layers: int, S: int, B: int = 1, M_mlp: int = 1,
+                 M_head: int = 1, recompute: bool = False, in_backward: bool = False,
+                 convention: str = "paper") -> MemBreakdown:
+    """predict_peak: the larger of two phases --
+    (A) the end of the forward / the backward: weights + optimizer state +
+        activations + the peak intermediate (+ the fp32 gradients already
+        produced, "repo" convention: model.py keeps every gradient until the
+        optimizer step);
+    (B) the optimizer step (absent with optimizer-in-backward): weights +
+        gradients + optimizer state + the optimizer's intermediate.
+    "paper": Appendix D: bf16 weights (2 B/param),
+    gradients (2 B), Adam moments (2 x 2 B) plus a weight-sized optimizer
+    intermediate; Llama3-8B / S=4096 gives 75 (vanilla), 74 (in-backward),
+    52 (recompute) GiB.  "repo": bf16 weights + fp32 gains, fp32 gradients,
+    AdamW fp32 master + moments (12 B/param, no intermediate: the update is
+    one fused kernel)."""
+    if convention not in ("paper", "repo"):
+        raise ValueError("convention is 'paper' or 'repo'")
+    N = S * B
+    P = param_counts(d, I, V, heads, G, layers)
+    act_fn = _paper_activation if convention == "paper" else _repo_activation
+    act = act_fn(d, I, V, G, layers, N, M_mlp, M_head, recompute)
+    if convention == "paper":
+        w = 2 * P["total"]
+        g = 2 * P["total"]
+        opt_state, opt_inter = 4 * P["total"], 2 * P["total"]
+        grads_in_a = 0
+        f = {"weights": "2 B x params", "gradients": "2 B x params (0 with optimizer-in-backward)",
+             "optimizer": "Adam moments 2 x 2 B x params (+ 2 B x params intermediate at the step)",
+             "activation": "per layer 11 N d + 4 N I bf16 elements; recompute: N d per layer",
+             "peak_intermediate": "head N V (2+4+4) B / M_head; recompute: one layer's set, MLP part / M_mlp"}
+    else:
+        w = 2 * P["matrices"] + 4 * P["gains"]
+        g = 4 * P["total"]
+        opt_state, opt_inter = 12 * P["matrices"] + 8 * P["gains"], 0
+        grads_in_a = 0 if in_backward else g
+        f = {"weights": "2 B x matrix params + 4 B x gains", "gradients": "4 B x params (fp32)",
+             "optimizer": "AdamW fp32 master + m + v (12 B / matrix param, 8 B / gain)",
+             "activation": "model.py saved set: per layer N(6d + 2d/G) bf16 + 8N; recompute: N d per layer",
+             "peak_intermediate": "libmst chunk workspace max(MLP, head) + one layer's backward buffers"}
+    phase_a = w + opt_state + act["saved"] + act["inter"] + grads_in_a
+    phase_b = -1 if in_backward else w + g + opt_state + opt_inter
+    if phase_b > phase_a:
+        return MemBreakdown(w, g, opt_state + opt_inter, 0, 0, "optimizer step", f)
+    return MemBreakdown(w, grads_in_a, opt_state, act["saved"], act["inter"], "forward/backward", f)
