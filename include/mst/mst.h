@@ -387,6 +387,28 @@ MST_API int mst_embedding_backward(mst_ctx* ctx, void* stream, const int32_t* or
                                    const int32_t* uniq, int64_t nseg, const void* dx, float* dtable, int64_t d,
                                    int64_t vocab, int accumulate);
 
+/* Causal grouped-query attention (attn_forward / attn_backward, SPEC.md:233-241;
+ * the decoder's attention around the MsT blocks) on tcgen05 kernels: exact
+ * softmax attention tile by tile, the [S, S] scores never reach HBM.
+ * Token-major bf16 tensors: q element (b, t, head h, e) at
+ * q[(b*seq + t)*ldq + h*head_dim + e]; k, v with kv_heads heads (query head h
+ * reads kv head h / (heads / kv_heads)); o, dq, dk, dv the same way (the
+ * decoder passes column slices of its fused [N, d + 2d/G] qkv buffer).
+ * head_dim a multiple of 8 up to 128; scale 1/sqrt(head_dim); causal = 1.
+ * lse: device fp32 [batch, heads, seq] log-sum-exp of the scaled scores
+ * (natural log), written by the forward, read by the backward.  The
+ * backward's workspace (mst_attention_workspace) holds rowsum(dO * O).
+ * Deterministic: no atomics; dq, dk, dv are overwritten. */
+MST_API int mst_attention_forward(mst_ctx* ctx, void* stream, const void* q, int64_t ldq, const void* k, int64_t ldk,
+                                  const void* v, int64_t ldv, void* o, int64_t ldo, float* lse, int64_t batch,
+                                  int64_t seq, int64_t heads, int64_t kv_heads, int64_t head_dim, int causal);
+MST_API int mst_attention_workspace(int64_t batch, int64_t seq, int64_t heads, size_t* bytes);
+MST_API int mst_attention_backward(mst_ctx* ctx, void* stream, const void* q, int64_t ldq, const void* k, int64_t ldk,
+                                   const void* v, int64_t ldv, const void* o, int64_t ldo, const void* dout,
+                                   int64_t lddo, const float* lse, void* dq, int64_t lddq, void* dk, int64_t lddk,
+                                   void* dv, int64_t lddv, int64_t batch, int64_t seq, int64_t heads, int64_t kv_heads,
+                                   int64_t head_dim, int causal, void* workspace, size_t workspace_bytes);
+
 /* Diagnostic single GEMM through the same engine: C[M,N] = A[M,K] B[K,N].
  * a_mn=0: A row-major [M,K]; a_mn=1: A given as row-major [K,M] (A^T).
  * b_mn=1: B row-major [K,N]; b_mn=0: B given as row-major [N,K] (B^T).

@@ -1,0 +1,701 @@
+// Causal grouped-query attention, forward and backward, on tcgen05 (sm_100a)
+// -- the attention of the Llama-style decoder around the MsT blocks
+// (reference: SPEC.md:233-241 attn_forward / attn_backward, PAPER.md:128
+// "FlashAttention2").  Exact softmax attention computed
+// tile by tile (FlashAttention-style online softmax): the [S, S] scores never
+// reach HBM, the forward saves one fp32 log-sum-exp per (row, head).
+//
+// Layout: token-major, q element (b, t, head h, e) at q[(b*S + t)*ldq + h*hd + e]
+// (k, v likewise with kv_heads heads; o, dq, dk, dv likewise), so the
+// decoder's fused [N, d + 2d/G] qkv buffer and the Ulysses head-sharded
+// tensors are both read in place.  Each operand is a 3-D tensor map
+// {hd, heads, rows} with a {64, 1, 128} box: one 128-token x 64-feature
+// SWIZZLE_128B tile per load; head dims below 64 are zero-padded by the TMA
+// (out-of-bounds fill), 64 < hd <= 128 takes two loads.
+//
+// Kernels (one CTA per 128-row tile, single-CTA UMMA M=128, fp32 TMEM
+// accumulators, warp roles: w0 TMA, w1 MMA, w2 TMEM allocator, w4-w7 softmax /
+// gradient math with one row per thread):
+//   attn_fwd_kernel   per (q tile, head): S = Q K^T -> online softmax -> O += P V
+//   attn_dkv_kernel   per (kv tile, kv head): over the q heads of its group and the
+//                     q tiles at or after it: S^T = K Q^T, dP^T = V dO^T,
+//                     dV += P^T dO, dK += dS^T Q
+//   attn_dq_kernel    per (q tile, head): over the kv tiles at or before it:
+//                     S, dP, dQ += dS K
+//   attn_delta_kernel D = rowsum(dO * O) per (row, head)
+// No atomics anywhere: dQ, dK, dV are each produced by exactly one CTA, so
+// results are bitwise reproducible.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+
+#include "attention.cuh"
+#include "ptx.cuh"
+
+namespace mst_attn {
+
+using namespace mst;
+
+constexpr int kBM = 128;           // rows per tile (q or kv tokens)
+constexpr int kTile = 16384;       // one 128 x 64 bf16 SW128 tile
+constexpr int kThreads = 256;
+constexpr float kLog2e = 1.4426950408889634f;
+
+struct Maps {
+  CUtensorMap q, k, v, o, dout;
+};
+
+struct Args {
+  Maps m;
+  uint16_t* o;         // forward output (bf16)
+  float* lse;          // [B, heads, S] natural-log units
+  const float* delta;  // [B, heads, S] rowsum(dO * O)
+  uint16_t *dq, *dk, *dv;
+  int64_t ldo, lddq, lddk, lddv;
+  int B, S, heads, kvh, hd;
+  float scale2;        // softmax scale * log2(e)
+  float scale;         // softmax scale
+  int nqb;             // q (= kv) tiles per sequence
+};
+
+__device__ __forceinline__ uint64_t kdesc(uint32_t saddr) { return ptx::sdesc_sw128(saddr, 16, 1024); }
+// MN-major operand: 64-wide N blocks one 16 KB tile apart.
+__device__ __forceinline__ uint64_t mdesc(uint32_t saddr) { return ptx::sdesc_sw128(saddr, kTile, 1024); }
+
+// One 128 x (64 * nblk) operand tile: nblk loads of a 128-row x 64-feature box.
+template <int NB>
+__device__ __forceinline__ void load_tile(const CUtensorMap* m, uint32_t dst, uint32_t bar, int head, int row) {
+#pragma unroll
+  for (int c = 0; c < NB; ++c) ptx::tma_load_3d(m, dst + c * kTile, bar, c * 64, head, row);
+}
+
+// D[128 x N] (+)= A[128 x K] B: A K-major in 64-deep sub-tiles (kTile apart),
+// B K-major (b_mn = 0: 64-deep sub-tiles kTile apart) or MN-major (b_mn = 1:
+// K rows of 128 B, 64-wide N blocks kTile apart); K = 64 * ksub.
+__device__ __forceinline__ void mma_tile(uint32_t d, uint32_t a, uint32_t b, int ksub, int n, bool b_mn,
+                                         bool accumulate) {
+  const uint32_t idesc = ptx::idesc_bf16(128, n, 0, b_mn ? 1 : 0);
+  for (int c = 0; c < ksub; ++c) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t ad = kdesc(a + c * kTile + k * 32);
+      const uint64_t bd = b_mn ? mdesc(b + c * 8192 + k * 2048) : kdesc(b + c * kTile + k * 32);
+      ptx::umma_bf16_cg1(d, ad, bd, idesc, (accumulate || c || k) ? 1u : 0u);
+    }
+  }
+}
+
+// This thread's 128-value row r of a K-major [128 x 128] bf16 operand made of
+// two 64-column SW128 sub-tiles; v[c] for column c.
+__device__ __forceinline__ void store_row_bf16(uint8_t* base, int r, const float* v) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int sub = j >> 3, ch = j & 7;
+    const uint4 w = make_uint4(ptx::pack_bf16(v[8 * j], v[8 * j + 1]), ptx::pack_bf16(v[8 * j + 2], v[8 * j + 3]),
+                               ptx::pack_bf16(v[8 * j + 4], v[8 * j + 5]), ptx::pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+    *reinterpret_cast<uint4*>(base + sub * kTile + r * 128 + ((ch ^ (r & 7)) << 4)) = w;
+  }
+}
+
+__device__ __forceinline__ void load_row(uint32_t taddr, float (&v)[128]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint32_t r[32];
+    ptx::tmem_ld_32x32b_x32(taddr + 32 * c, r);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[32 * c + j] = __uint_as_float(r[j]);
+  }
+  ptx::tmem_ld_wait();
+}
+
+// Writes columns [0, hd) of this thread's accumulator row (TMEM, nsub * 64
+// columns) times `mul` as bf16 to dst (16-byte stores; hd % 8 == 0).
+__device__ __forceinline__ void store_acc_row(uint32_t taddr, int nsub, float mul, uint16_t* dst, int hd, bool ok) {
+  for (int c = 0; c < nsub * 2; ++c) {
+    uint32_t r[32];
+    ptx::tmem_ld_32x32b_x32(taddr + 32 * c, r);
+    ptx::tmem_ld_wait();
+    if (!ok) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int e = 32 * c + 8 * j;
+      if (e < hd) {
+        const uint4 w = make_uint4(ptx::pack_bf16(__uint_as_float(r[8 * j]) * mul, __uint_as_float(r[8 * j + 1]) * mul),
+                                   ptx::pack_bf16(__uint_as_float(r[8 * j + 2]) * mul, __uint_as_float(r[8 * j + 3]) * mul),
+                                   ptx::pack_bf16(__uint_as_float(r[8 * j + 4]) * mul, __uint_as_float(r[8 * j + 5]) * mul),
+                                   ptx::pack_bf16(__uint_as_float(r[8 * j + 6]) * mul, __uint_as_float(r[8 * j + 7]) * mul));
+        *reinterpret_cast<uint4*>(dst + e) = w;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ forward
+template <int NSUB>  // head-dim tiles of 64 (hd <= 64 * NSUB)
+__global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_constant__ Args a) {
+  constexpr int kST = NSUB == 1 ? 3 : 2;  // K/V stages
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* q_s = sm;
+  uint8_t* k_s = q_s + NSUB * kTile;              // [kST] K tiles
+  uint8_t* v_s = k_s + kST * NSUB * kTile;        // [kST] V tiles
+  uint8_t* p_s = v_s + kST * NSUB * kTile;        // P: 2 sub-tiles
+  uint64_t* bars = reinterpret_cast<uint64_t*>(p_s + 2 * kTile);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;
+  uint64_t* v_full = k_full + kST;
+  uint64_t* kv_empty = v_full + kST;
+  uint64_t* s_full = kv_empty + kST;  // [2]
+  uint64_t* p_full = s_full + 2;
+  uint64_t* pv_done = p_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int hb = a.heads * a.B;
+  const int qblk = a.nqb - 1 - static_cast<int>(blockIdx.x) / hb;  // longest (last) q tiles first
+  const int h = static_cast<int>(blockIdx.x) % a.heads;
+  const int b = (static_cast<int>(blockIdx.x) % hb) / a.heads;
+  const int g = h / (a.heads / a.kvh);
+  const int q0 = qblk * kBM;
+  const int nblk = qblk + 1;  // causal: kv tiles 0 .. qblk
+  const int row0 = b * a.S;
+
+  if (warp == 1 && lane == 0) {
+    ptx::mbar_init(ptx::smem_u32(q_full), 1);
+    for (int s = 0; s < kST; ++s) {
+      ptx::mbar_init(ptx::smem_u32(&k_full[s]), 1);
+      ptx::mbar_init(ptx::smem_u32(&v_full[s]), 1);
+      ptx::mbar_init(ptx::smem_u32(&kv_empty[s]), 1);
+    }
+    ptx::mbar_init(ptx::smem_u32(&s_full[0]), 1);
+    ptx::mbar_init(ptx::smem_u32(&s_full[1]), 1);
+    ptx::mbar_init(ptx::smem_u32(p_full), 4);
+    ptx::mbar_init(ptx::smem_u32(pv_done), 1);
+    ptx::fence_mbarrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc_cg1(ptx::smem_u32(tmem_slot), 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS[2] = {tmem, tmem + 128};
+  const uint32_t tO = tmem + 256;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer
+      ptx::prefetch_tmap(&a.m.q);
+      ptx::prefetch_tmap(&a.m.k);
+      ptx::prefetch_tmap(&a.m.v);
+      ptx::mbar_arrive_expect_tx(ptx::smem_u32(q_full), NSUB * kTile);
+      load_tile<NSUB>(&a.m.q, ptx::smem_u32(q_s), ptx::smem_u32(q_full), h, row0 + q0);
+      for (int j = 0; j < nblk; ++j) {
+        const int s = j % kST;
+        ptx::mbar_wait(ptx::smem_u32(&kv_empty[s]), ((j / kST) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(ptx::smem_u32(&k_full[s]), NSUB * kTile);
+        load_tile<NSUB>(&a.m.k, ptx::smem_u32(k_s + s * NSUB * kTile), ptx::smem_u32(&k_full[s]), g, row0 + j * kBM);
+        ptx::mbar_arrive_expect_tx(ptx::smem_u32(&v_full[s]), NSUB * kTile);
+        load_tile<NSUB>(&a.m.v, ptx::smem_u32(v_s + s * NSUB * kTile), ptx::smem_u32(&v_full[s]), g, row0 + j * kBM);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      auto pv = [&](int i) {
+        const int s = i % kST;
+        ptx::mbar_wait(ptx::smem_u32(p_full), i & 1);
+        ptx::mbar_wait(ptx::smem_u32(&v_full[s]), (i / kST) & 1);
+        ptx::tc_fence_after();
+        // O[128 x 64*NSUB] (+)= P[128 x 128] V[128 x 64*NSUB]  (V MN-major)
+        mma_tile(tO, ptx::smem_u32(p_s), ptx::smem_u32(v_s + s * NSUB * kTile), 2, 64 * NSUB, true, i > 0);
+        ptx::umma_commit_cg1(ptx::smem_u32(pv_done));
+        ptx::umma_commit_cg1(ptx::smem_u32(&kv_empty[s]));
+      };
+      ptx::mbar_wait(ptx::smem_u32(q_full), 0);
+      for (int j = 0; j < nblk; ++j) {
+        const int s = j % kST;
+        ptx::mbar_wait(ptx::smem_u32(&k_full[s]), (j / kST) & 1);
+        ptx::tc_fence_after();
+        mma_tile(tS[j & 1], ptx::smem_u32(q_s), ptx::smem_u32(k_s + s * NSUB * kTile), NSUB, 128, false, false);
+        ptx::umma_commit_cg1(ptx::smem_u32(&s_full[j & 1]));
+        if (j >= 1) pv(j - 1);
+      }
+      pv(nblk - 1);
+    }
+  } else if (warp >= 4) {  // ---- online softmax, one q row per thread
+    const int r = (warp - 4) * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const int q = q0 + r;
+    float m2 = -INFINITY, l = 0.f;
+    float v[128];
+    for (int j = 0; j < nblk; ++j) {
+      ptx::mbar_wait(ptx::smem_u32(&s_full[j & 1]), (j >> 1) & 1);
+      ptx::tc_fence_after();
+      load_row(tS[j & 1] + lane_off, v);
+      const int kv0 = j * kBM;
+      float mx = -INFINITY;
+      if (kv0 + kBM - 1 > q0) {  // the diagonal tile: mask kv > q
+#pragma unroll
+        for (int c = 0; c < 128; ++c) {
+          v[c] = (kv0 + c <= q) ? v[c] * a.scale2 : -INFINITY;
+          mx = fmaxf(mx, v[c]);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 128; ++c) {
+          v[c] *= a.scale2;
+          mx = fmaxf(mx, v[c]);
+        }
+      }
+      const float mn = fmaxf(m2, mx);
+      float rs = 0.f;
+#pragma unroll
+      for (int c = 0; c < 128; ++c) {
+        v[c] = ptx::ex2(v[c] - mn);
+        rs += v[c];
+      }
+      const float alpha = ptx::ex2(m2 - mn);  // 0 on the first tile
+      if (j >= 1) {
+        ptx::mbar_wait(ptx::smem_u32(pv_done), (j - 1) & 1);  // PV_{j-1} done: O current, P buffer free
+        ptx::tc_fence_after();
+        if (!__all_sync(0xffffffffu, alpha == 1.f)) {
+          for (int c = 0; c < 2 * NSUB; ++c) {
+            uint32_t o[32];
+            ptx::tmem_ld_32x32b_x32(tO + lane_off + 32 * c, o);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            ptx::tmem_st_32x32b_x32(tO + lane_off + 32 * c, o);
+          }
+          ptx::tmem_st_wait();
+        }
+      }
+      l = l * alpha + rs;
+      m2 = mn;
+      store_row_bf16(p_s, r, v);
+      ptx::fence_proxy_async_smem();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_local(ptx::smem_u32(p_full));
+    }
+    ptx::mbar_wait(ptx::smem_u32(pv_done), (nblk - 1) & 1);
+    ptx::tc_fence_after();
+    const bool ok = q < a.S;
+    store_acc_row(tO + lane_off, NSUB, 1.f / l, a.o + (static_cast<int64_t>(row0) + q) * a.ldo + h * a.hd, a.hd, ok);
+    if (ok) a.lse[(static_cast<int64_t>(b) * a.heads + h) * a.S + q] = (m2 + __log2f(l)) * 0.69314718055994531f;
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_cg1(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------------------ D = rowsum(dO * O)
+__global__ void attn_delta_kernel(const uint16_t* __restrict__ o, int64_t ldo, const uint16_t* __restrict__ dout,
+                                  int64_t lddo, float* __restrict__ delta, int B, int S, int heads, int hd) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // (b, h, t)
+  if (idx >= static_cast<int64_t>(B) * heads * S) return;
+  const int t = static_cast<int>(idx % S);
+  const int h = static_cast<int>((idx / S) % heads);
+  const int b = static_cast<int>(idx / (static_cast<int64_t>(S) * heads));
+  const int64_t row = static_cast<int64_t>(b) * S + t;
+  const uint16_t* po = o + row * ldo + h * hd;
+  const uint16_t* pd = dout + row * lddo + h * hd;
+  float acc = 0.f;
+  for (int e = 0; e < hd; e += 8) {
+    const uint4 x = *reinterpret_cast<const uint4*>(po + e);
+    const uint4 y = *reinterpret_cast<const uint4*>(pd + e);
+    const uint32_t xa[4] = {x.x, x.y, x.z, x.w}, ya[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      acc += __uint_as_float(xa[k] << 16) * __uint_as_float(ya[k] << 16);
+      acc += __uint_as_float(xa[k] & 0xffff0000u) * __uint_as_float(ya[k] & 0xffff0000u);
+    }
+  }
+  delta[idx] = acc;
+}
+
+// ------------------------------------------------------------------ dK, dV
+template <int NSUB>
+__global__ void __launch_bounds__(kThreads, 1) attn_dkv_kernel(const __grid_constant__ Args a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* k_s = sm;
+  uint8_t* v_s = k_s + NSUB * kTile;
+  uint8_t* q_s = v_s + NSUB * kTile;
+  uint8_t* do_s = q_s + NSUB * kTile;
+  uint8_t* pt_s = do_s + NSUB * kTile;  // P^T  [kv][q], 2 sub-tiles
+  uint8_t* dst_s = pt_s + 2 * kTile;    // dS^T [kv][q]
+  float* vec = reinterpret_cast<float*>(dst_s + 2 * kTile);  // [2][2][128]: lse2, delta per buffer
+  uint64_t* bars = reinterpret_cast<uint64_t*>(vec + 512);
+  uint64_t* kv_full = bars;
+  uint64_t* qdo_full = bars + 1;
+  uint64_t* qdo_empty = bars + 2;
+  uint64_t* s_full = bars + 3;
+  uint64_t* dp_full = bars + 4;
+  uint64_t* ps_full = bars + 5;
+  uint64_t* ps_free = bars + 6;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 7);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gb = a.kvh * a.B;
+  const int kblk = static_cast<int>(blockIdx.x) / gb;  // the first kv tiles have the most q tiles: first
+  const int g = static_cast<int>(blockIdx.x) % a.kvh;
+  const int b = (static_cast<int>(blockIdx.x) % gb) / a.kvh;
+  const int grp = a.heads / a.kvh;
+  const int k0 = kblk * kBM;
+  const int nq = a.nqb - kblk;  // q tiles kblk .. nqb-1
+  const int iters = grp * nq;
+  const int row0 = b * a.S;
+
+  if (warp == 1 && lane == 0) {
+    for (int i = 0; i < 7; ++i) ptx::mbar_init(ptx::smem_u32(&bars[i]), i == 5 ? 4 : 1);
+    ptx::fence_mbarrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc_cg1(ptx::smem_u32(tmem_slot), 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tDP = tmem + 128, tDV = tmem + 256, tDK = tmem + 384;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      ptx::mbar_arrive_expect_tx(ptx::smem_u32(kv_full), 2 * NSUB * kTile);
+      load_tile<NSUB>(&a.m.k, ptx::smem_u32(k_s), ptx::smem_u32(kv_full), g, row0 + k0);
+      load_tile<NSUB>(&a.m.v, ptx::smem_u32(v_s), ptx::smem_u32(kv_full), g, row0 + k0);
+      for (int t = 0; t < iters; ++t) {
+        const int hq = g * grp + t / nq, i = kblk + t % nq;
+        ptx::mbar_wait(ptx::smem_u32(qdo_empty), (t & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(ptx::smem_u32(qdo_full), 2 * NSUB * kTile);
+        load_tile<NSUB>(&a.m.q, ptx::smem_u32(q_s), ptx::smem_u32(qdo_full), hq, row0 + i * kBM);
+        load_tile<NSUB>(&a.m.dout, ptx::smem_u32(do_s), ptx::smem_u32(qdo_full), hq, row0 + i * kBM);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      ptx::mbar_wait(ptx::smem_u32(kv_full), 0);
+      for (int t = 0; t < iters; ++t) {
+        ptx::mbar_wait(ptx::smem_u32(qdo_full), t & 1);
+        ptx::tc_fence_after();
+        mma_tile(tS, ptx::smem_u32(k_s), ptx::smem_u32(q_s), NSUB, 128, false, false);    // S^T = K Q^T
+        ptx::umma_commit_cg1(ptx::smem_u32(s_full));
+        mma_tile(tDP, ptx::smem_u32(v_s), ptx::smem_u32(do_s), NSUB, 128, false, false);  // dP^T = V dO^T
+        ptx::umma_commit_cg1(ptx::smem_u32(dp_full));
+        ptx::mbar_wait(ptx::smem_u32(ps_full), t & 1);
+        ptx::tc_fence_after();
+        mma_tile(tDV, ptx::smem_u32(pt_s), ptx::smem_u32(do_s), 2, 64 * NSUB, true, t > 0);   // dV += P^T dO
+        mma_tile(tDK, ptx::smem_u32(dst_s), ptx::smem_u32(q_s), 2, 64 * NSUB, true, t > 0);   // dK += dS^T Q
+        ptx::umma_commit_cg1(ptx::smem_u32(qdo_empty));
+        ptx::umma_commit_cg1(ptx::smem_u32(ps_free));
+      }
+    }
+  } else if (warp >= 4) {  // one kv row per thread
+    const int r = (warp - 4) * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const int kv = k0 + r;
+    float p[128], ds[128];
+    for (int t = 0; t < iters; ++t) {
+      const int hq = g * grp + t / nq, i = kblk + t % nq;
+      const int q0 = i * kBM;
+      float* lse2 = vec + (t & 1) * 256;
+      float* dl = lse2 + 128;
+      {  // this q tile's lse (log2 units) and D into shared memory
+        const int q = q0 + r;
+        const int64_t o = (static_cast<int64_t>(b) * a.heads + hq) * a.S + q;
+        lse2[r] = q < a.S ? a.lse[o] * kLog2e : INFINITY;  // rows past the sequence: P = 0
+        dl[r] = q < a.S ? a.delta[o] : 0.f;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+      ptx::mbar_wait(ptx::smem_u32(s_full), t & 1);
+      ptx::tc_fence_after();
+      load_row(tS + lane_off, p);
+      const bool diag = q0 == k0;  // the diagonal tile holds the q < kv entries
+#pragma unroll
+      for (int c = 0; c < 128; ++c) {
+        const float x = ptx::ex2(p[c] * a.scale2 - lse2[c]);
+        p[c] = (diag && q0 + c < kv) ? 0.f : x;
+      }
+      ptx::mbar_wait(ptx::smem_u32(dp_full), t & 1);
+      ptx::tc_fence_after();
+      load_row(tDP + lane_off, ds);
+#pragma unroll
+      for (int c = 0; c < 128; ++c) ds[c] = p[c] * (ds[c] - dl[c]);
+      if (t >= 1) ptx::mbar_wait(ptx::smem_u32(ps_free), (t - 1) & 1);
+      store_row_bf16(pt_s, r, p);
+      store_row_bf16(dst_s, r, ds);
+      ptx::fence_proxy_async_smem();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_local(ptx::smem_u32(ps_full));
+    }
+    ptx::mbar_wait(ptx::smem_u32(ps_free), (iters - 1) & 1);
+    ptx::tc_fence_after();
+    const bool ok = kv < a.S;
+    const int64_t row = static_cast<int64_t>(row0) + kv;
+    store_acc_row(tDV + lane_off, NSUB, 1.f, a.dv + row * a.lddv + g * a.hd, a.hd, ok);
+    store_acc_row(tDK + lane_off, NSUB, a.scale, a.dk + row * a.lddk + g * a.hd, a.hd, ok);
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_cg1(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------------------ dQ
+template <int NSUB>
+__global__ void __launch_bounds__(kThreads, 1) attn_dq_kernel(const __grid_constant__ Args a) {
+  constexpr int kST = 2;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* q_s = sm;
+  uint8_t* do_s = q_s + NSUB * kTile;
+  uint8_t* k_s = do_s + NSUB * kTile;        // [kST]
+  uint8_t* v_s = k_s + kST * NSUB * kTile;   // [kST]
+  uint8_t* ds_s = v_s + kST * NSUB * kTile;  // dS [q][kv], 2 sub-tiles
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ds_s + 2 * kTile);
+  uint64_t* qdo_full = bars;
+  uint64_t* kv_full = bars + 1;        // [kST]
+  uint64_t* kv_empty = kv_full + kST;  // [kST]
+  uint64_t* s_full = kv_empty + kST;
+  uint64_t* dp_full = s_full + 1;
+  uint64_t* ds_full = dp_full + 1;
+  uint64_t* ds_free = ds_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ds_free + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int hb = a.heads * a.B;
+  const int qblk = a.nqb - 1 - static_cast<int>(blockIdx.x) / hb;
+  const int h = static_cast<int>(blockIdx.x) % a.heads;
+  const int b = (static_cast<int>(blockIdx.x) % hb) / a.heads;
+  const int g = h / (a.heads / a.kvh);
+  const int q0 = qblk * kBM;
+  const int nblk = qblk + 1;
+  const int row0 = b * a.S;
+
+  if (warp == 1 && lane == 0) {
+    ptx::mbar_init(ptx::smem_u32(qdo_full), 1);
+    for (int s = 0; s < kST; ++s) {
+      ptx::mbar_init(ptx::smem_u32(&kv_full[s]), 1);
+      ptx::mbar_init(ptx::smem_u32(&kv_empty[s]), 1);
+    }
+    ptx::mbar_init(ptx::smem_u32(s_full), 1);
+    ptx::mbar_init(ptx::smem_u32(dp_full), 1);
+    ptx::mbar_init(ptx::smem_u32(ds_full), 4);
+    ptx::mbar_init(ptx::smem_u32(ds_free), 1);
+    ptx::fence_mbarrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc_cg1(ptx::smem_u32(tmem_slot), 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tDP = tmem + 128, tDQ = tmem + 256;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      ptx::mbar_arrive_expect_tx(ptx::smem_u32(qdo_full), 2 * NSUB * kTile);
+      load_tile<NSUB>(&a.m.q, ptx::smem_u32(q_s), ptx::smem_u32(qdo_full), h, row0 + q0);
+      load_tile<NSUB>(&a.m.dout, ptx::smem_u32(do_s), ptx::smem_u32(qdo_full), h, row0 + q0);
+      for (int j = 0; j < nblk; ++j) {
+        const int s = j % kST;
+        ptx::mbar_wait(ptx::smem_u32(&kv_empty[s]), ((j / kST) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(ptx::smem_u32(&kv_full[s]), 2 * NSUB * kTile);
+        load_tile<NSUB>(&a.m.k, ptx::smem_u32(k_s + s * NSUB * kTile), ptx::smem_u32(&kv_full[s]), g, row0 + j * kBM);
+        load_tile<NSUB>(&a.m.v, ptx::smem_u32(v_s + s * NSUB * kTile), ptx::smem_u32(&kv_full[s]), g, row0 + j * kBM);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      ptx::mbar_wait(ptx::smem_u32(qdo_full), 0);
+      for (int j = 0; j < nblk; ++j) {
+        const int s = j % kST;
+        ptx::mbar_wait(ptx::smem_u32(&kv_full[s]), (j / kST) & 1);
+        ptx::tc_fence_after();
+        mma_tile(tS, ptx::smem_u32(q_s), ptx::smem_u32(k_s + s * NSUB * kTile), NSUB, 128, false, false);   // S
+        ptx::umma_commit_cg1(ptx::smem_u32(s_full));
+        mma_tile(tDP, ptx::smem_u32(do_s), ptx::smem_u32(v_s + s * NSUB * kTile), NSUB, 128, false, false);  // dP
+        ptx::umma_commit_cg1(ptx::smem_u32(dp_full));
+        ptx::mbar_wait(ptx::smem_u32(ds_full), j & 1);
+        ptx::tc_fence_after();
+        mma_tile(tDQ, ptx::smem_u32(ds_s), ptx::smem_u32(k_s + s * NSUB * kTile), 2, 64 * NSUB, true, j > 0);  // dQ += dS K
+        ptx::umma_commit_cg1(ptx::smem_u32(&kv_empty[s]));
+        ptx::umma_commit_cg1(ptx::smem_u32(ds_free));
+      }
+    }
+  } else if (warp >= 4) {
+    const int r = (warp - 4) * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const int q = q0 + r;
+    const bool ok = q < a.S;
+    const int64_t o = (static_cast<int64_t>(b) * a.heads + h) * a.S + q;
+    const float lse2 = ok ? a.lse[o] * kLog2e : INFINITY;
+    const float dd = ok ? a.delta[o] : 0.f;
+    float p[128], ds[128];
+    for (int j = 0; j < nblk; ++j) {
+      const int kv0 = j * kBM;
+      ptx::mbar_wait(ptx::smem_u32(s_full), j & 1);
+      ptx::tc_fence_after();
+      load_row(tS + lane_off, p);
+      const bool diag = kv0 + kBM - 1 > q0;
+#pragma unroll
+      for (int c = 0; c < 128; ++c) {
+        const float x = ptx::ex2(p[c] * a.scale2 - lse2);
+        p[c] = (diag && kv0 + c > q) ? 0.f : x;
+      }
+      ptx::mbar_wait(ptx::smem_u32(dp_full), j & 1);
+      ptx::tc_fence_after();
+      load_row(tDP + lane_off, ds);
+#pragma unroll
+      for (int c = 0; c < 128; ++c) ds[c] = p[c] * (ds[c] - dd);
+      if (j >= 1) ptx::mbar_wait(ptx::smem_u32(ds_free), (j - 1) & 1);
+      store_row_bf16(ds_s, r, ds);
+      ptx::fence_proxy_async_smem();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_local(ptx::smem_u32(ds_full));
+    }
+    ptx::mbar_wait(ptx::smem_u32(ds_free), (nblk - 1) & 1);
+    ptx::tc_fence_after();
+    store_acc_row(tDQ + lane_off, NSUB, a.scale, a.dq + (static_cast<int64_t>(row0) + q) * a.lddq + h * a.hd, a.hd,
+                  ok);
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_cg1(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+template <int NSUB>
+constexpr int fwd_smem() {
+  return 1024 + NSUB * kTile + 2 * (NSUB == 1 ? 3 : 2) * NSUB * kTile + 2 * kTile + 256;
+}
+template <int NSUB>
+constexpr int dkv_smem() {
+  return 1024 + 4 * NSUB * kTile + 4 * kTile + 2048 + 256;
+}
+template <int NSUB>
+constexpr int dq_smem() {
+  return 1024 + 2 * NSUB * kTile + 4 * NSUB * kTile + 2 * kTile + 256;
+}
+static_assert(fwd_smem<2>() <= 232448 && dkv_smem<2>() <= 232448 && dq_smem<2>() <= 232448, "shared memory");
+
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static int encode(void* enc, CUtensorMap* m, const void* base, int64_t ld, int64_t rows, int heads, int hd) {
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(hd), static_cast<cuuint64_t>(heads), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(hd) * 2, static_cast<cuuint64_t>(ld) * 2};
+  cuuint32_t box[3] = {64, 1, 128};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = reinterpret_cast<EncodeFn>(enc)(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
+                                               strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : static_cast<int>(r);
+}
+
+template <int NSUB>
+static cudaError_t set_attrs() {
+  static bool done = false;
+  if (done) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<NSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem<NSUB>());
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(attn_dkv_kernel<NSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, dkv_smem<NSUB>());
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(attn_dq_kernel<NSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, dq_smem<NSUB>());
+  done = e == cudaSuccess;
+  return e;
+}
+
+int forward(void* enc, cudaStream_t st, const AttnShape& s, const void* q, int64_t ldq, const void* k, int64_t ldk,
+            const void* v, int64_t ldv, void* o, int64_t ldo, float* lse, const char** err) {
+  Args a;
+  std::memset(&a, 0, sizeof(a));
+  const int64_t rows = static_cast<int64_t>(s.B) * s.S;
+  if (encode(enc, &a.m.q, q, ldq, rows, s.heads, s.hd) || encode(enc, &a.m.k, k, ldk, rows, s.kvh, s.hd) ||
+      encode(enc, &a.m.v, v, ldv, rows, s.kvh, s.hd)) {
+    *err = "cuTensorMapEncodeTiled failed for an attention operand";
+    return 1;
+  }
+  a.o = static_cast<uint16_t*>(o);
+  a.ldo = ldo;
+  a.lse = lse;
+  a.B = s.B;
+  a.S = s.S;
+  a.heads = s.heads;
+  a.kvh = s.kvh;
+  a.hd = s.hd;
+  a.scale = 1.f / sqrtf(static_cast<float>(s.hd));
+  a.scale2 = a.scale * kLog2e;
+  a.nqb = (s.S + kBM - 1) / kBM;
+  const dim3 grid(static_cast<unsigned>(a.nqb * s.heads * s.B));
+  cudaError_t e;
+  if (s.hd <= 64) {
+    if ((e = set_attrs<1>()) != cudaSuccess) return *err = cudaGetErrorString(e), 2;
+    attn_fwd_kernel<1><<<grid, kThreads, fwd_smem<1>(), st>>>(a);
+  } else {
+    if ((e = set_attrs<2>()) != cudaSuccess) return *err = cudaGetErrorString(e), 2;
+    attn_fwd_kernel<2><<<grid, kThreads, fwd_smem<2>(), st>>>(a);
+  }
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return *err = cudaGetErrorString(e), 2;
+  return 0;
+}
+
+int backward(void* enc, cudaStream_t st, const AttnShape& s, const void* q, int64_t ldq, const void* k, int64_t ldk,
+             const void* v, int64_t ldv, const void* o, int64_t ldo, const void* dout, int64_t lddo, const float* lse,
+             void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv, int64_t lddv, float* delta, const char** err) {
+  Args a;
+  std::memset(&a, 0, sizeof(a));
+  const int64_t rows = static_cast<int64_t>(s.B) * s.S;
+  if (encode(enc, &a.m.q, q, ldq, rows, s.heads, s.hd) || encode(enc, &a.m.k, k, ldk, rows, s.kvh, s.hd) ||
+      encode(enc, &a.m.v, v, ldv, rows, s.kvh, s.hd) || encode(enc, &a.m.dout, dout, lddo, rows, s.heads, s.hd)) {
+    *err = "cuTensorMapEncodeTiled failed for an attention operand";
+    return 1;
+  }
+  a.lse = const_cast<float*>(lse);
+  a.delta = delta;
+  a.dq = static_cast<uint16_t*>(dq);
+  a.dk = static_cast<uint16_t*>(dk);
+  a.dv = static_cast<uint16_t*>(dv);
+  a.lddq = lddq;
+  a.lddk = lddk;
+  a.lddv = lddv;
+  a.B = s.B;
+  a.S = s.S;
+  a.heads = s.heads;
+  a.kvh = s.kvh;
+  a.hd = s.hd;
+  a.scale = 1.f / sqrtf(static_cast<float>(s.hd));
+  a.scale2 = a.scale * kLog2e;
+  a.nqb = (s.S + kBM - 1) / kBM;
+  const int64_t nrow = static_cast<int64_t>(s.B) * s.heads * s.S;
+  attn_delta_kernel<<<static_cast<unsigned>((nrow + 255) / 256), 256, 0, st>>>(
+      static_cast<const uint16_t*>(o), ldo, static_cast<const uint16_t*>(dout), lddo, delta, s.B, s.S, s.heads, s.hd);
+  const dim3 gkv(static_cast<unsigned>(a.nqb * s.kvh * s.B)), gq(static_cast<unsigned>(a.nqb * s.heads * s.B));
+  cudaError_t e;
+  if (s.hd <= 64) {
+    if ((e = set_attrs<1>()) != cudaSuccess) return *err = cudaGetErrorString(e), 2;
+    attn_dkv_kernel<1><<<gkv, kThreads, dkv_smem<1>(), st>>>(a);
+    attn_dq_kernel<1><<<gq, kThreads, dq_smem<1>(), st>>>(a);
+  } else {
+    if ((e = set_attrs<2>()) != cudaSuccess) return *err = cudaGetErrorString(e), 2;
+    attn_dkv_kernel<2><<<gkv, kThreads, dkv_smem<2>(), st>>>(a);
+    attn_dq_kernel<2><<<gq, kThreads, dq_smem<2>(), st>>>(a);
+  }
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return *err = cudaGetErrorString(e), 2;
+  return 0;
+}
+
+}  // namespace mst_attn

@@ -1,0 +1,22 @@
+// Causal GQA attention on tcgen05 (csrc/attention.cu); host entry points used
+// by the C ABI (mst_attention_forward / mst_attention_backward in mst.h).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace mst_attn {
+
+struct AttnShape {
+  int B, S, heads, kvh, hd;
+};
+
+// Return 0 on success; otherwise *err names the failure (1: tensor map, 2: CUDA).
+int forward(void* encode_fn, cudaStream_t st, const AttnShape& s, const void* q, int64_t ldq, const void* k,
+            int64_t ldk, const void* v, int64_t ldv, void* o, int64_t ldo, float* lse, const char** err);
+int backward(void* encode_fn, cudaStream_t st, const AttnShape& s, const void* q, int64_t ldq, const void* k,
+             int64_t ldk, const void* v, int64_t ldv, const void* o, int64_t ldo, const void* dout, int64_t lddo,
+             const float* lse, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv, int64_t lddv, float* delta,
+             const char** err);
+
+}  // namespace mst_attn

@@ -24,6 +24,7 @@
 
 #include "gemm.cuh"
 #include "mst/mst.h"
+#include "attention.cuh"
 #include "layers.cuh"
 #include "optim.cuh"
 
@@ -2268,6 +2269,77 @@ int mst_embedding_backward(mst_ctx* c, void* stream, const int32_t* order, const
   if (!accumulate) MST_CUDA(cudaMemsetAsync(dtable, 0, sizeof(float) * (size_t)vocab * (size_t)d, st));
   MST_CUDA(mst_layers::embed_bwd(st, c->num_sms, order, seg, uniq, (int)nseg, dx, dtable, (int)d, 1));
   c->launches++;
+  return MST_OK;
+}
+
+// ------------------------------------------------------------ attention (attention.cu)
+static int check_attn(const void* const* ptrs, const int64_t* lds, int n, int64_t batch, int64_t seq, int64_t heads,
+                      int64_t kvh, int64_t hd, int causal) {
+  if (batch < 1 || seq < 1 || heads < 1 || kvh < 1) return fail(MST_ERR_SHAPE, "attention extents must be >= 1");
+  if (heads % kvh) return fail(MST_ERR_CONFIG, "heads (%lld) must be a multiple of kv_heads (%lld)", (long long)heads,
+                               (long long)kvh);
+  if (hd < 8 || hd > 128 || hd % 8)
+    return fail(MST_ERR_SHAPE, "head_dim must be a multiple of 8 in [8, 128], got %lld", (long long)hd);
+  if (!causal) return fail(MST_ERR_CONFIG, "only causal attention is implemented (SPEC.md:235)");
+  if (batch * seq > (int64_t(1) << 31) || batch * heads * seq > (int64_t(1) << 40))
+    return fail(MST_ERR_BOUNDS, "attention problem too large");
+  for (int i = 0; i < n; ++i) {
+    if (!ptrs[i]) return fail(MST_ERR_CONFIG, "NULL attention tensor");
+    if ((reinterpret_cast<uintptr_t>(ptrs[i]) & 15) || lds[i] % 8)
+      return fail(MST_ERR_CONFIG, "attention tensors need 16-byte aligned rows (ld %% 8 == 0)");
+  }
+  return MST_OK;
+}
+
+int mst_attention_forward(mst_ctx* c, void* stream, const void* q, int64_t ldq, const void* k, int64_t ldk,
+                          const void* v, int64_t ldv, void* o, int64_t ldo, float* lse, int64_t batch, int64_t seq,
+                          int64_t heads, int64_t kv_heads, int64_t head_dim, int causal) {
+  MST_CALL(c, stream);
+  const void* ptrs[4] = {q, k, v, o};
+  const int64_t lds[4] = {ldq, ldk, ldv, ldo};
+  MST_TRY(check_attn(ptrs, lds, 4, batch, seq, heads, kv_heads, head_dim, causal));
+  if (!lse) return fail(MST_ERR_CONFIG, "NULL lse");
+  if (ldq < heads * head_dim || ldo < heads * head_dim || ldk < kv_heads * head_dim || ldv < kv_heads * head_dim)
+    return fail(MST_ERR_SHAPE, "row stride smaller than heads * head_dim");
+  const mst_attn::AttnShape sh{(int)batch, (int)seq, (int)heads, (int)kv_heads, (int)head_dim};
+  const char* err = "";
+  const int r = mst_attn::forward(reinterpret_cast<void*>(c->encode), static_cast<cudaStream_t>(stream), sh, q, ldq, k,
+                                  ldk, v, ldv, o, ldo, lse, &err);
+  if (r) return fail(r == 1 ? MST_ERR_CUDA : MST_ERR_CUDA, "attention forward: %s", err);
+  c->launches++;
+  // 2 GEMMs of the causal half: 2 * 2 * S^2/2 * hd per (batch, head)
+  cnt_op(c, (uint64_t)(2.0 * batch * heads * (double)seq * seq * head_dim), (uint64_t)(batch * seq * 4 * heads * head_dim));
+  return MST_OK;
+}
+
+int mst_attention_workspace(int64_t batch, int64_t seq, int64_t heads, size_t* bytes) {
+  if (!bytes) return fail(MST_ERR_CONFIG, "NULL output");
+  if (batch < 1 || seq < 1 || heads < 1) return fail(MST_ERR_SHAPE, "attention extents must be >= 1");
+  *bytes = align_up(size_t(batch) * heads * seq * 4, 256);  // D = rowsum(dO * O), fp32
+  return MST_OK;
+}
+
+int mst_attention_backward(mst_ctx* c, void* stream, const void* q, int64_t ldq, const void* k, int64_t ldk,
+                           const void* v, int64_t ldv, const void* o, int64_t ldo, const void* dout, int64_t lddo,
+                           const float* lse, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv, int64_t lddv,
+                           int64_t batch, int64_t seq, int64_t heads, int64_t kv_heads, int64_t head_dim, int causal,
+                           void* ws, size_t ws_bytes) {
+  MST_CALL(c, stream);
+  const void* ptrs[8] = {q, k, v, o, dout, dq, dk, dv};
+  const int64_t lds[8] = {ldq, ldk, ldv, ldo, lddo, lddq, lddk, lddv};
+  MST_TRY(check_attn(ptrs, lds, 8, batch, seq, heads, kv_heads, head_dim, causal));
+  if (!lse) return fail(MST_ERR_CONFIG, "NULL lse");
+  size_t need = 0;
+  MST_TRY(mst_attention_workspace(batch, seq, heads, &need));
+  if (!ws || ws_bytes < need) return fail(MST_ERR_CONFIG, "workspace too small (%zu < %zu)", ws_bytes, need);
+  const mst_attn::AttnShape sh{(int)batch, (int)seq, (int)heads, (int)kv_heads, (int)head_dim};
+  const char* err = "";
+  const int r = mst_attn::backward(reinterpret_cast<void*>(c->encode), static_cast<cudaStream_t>(stream), sh, q, ldq,
+                                   k, ldk, v, ldv, o, ldo, dout, lddo, lse, dq, lddq, dk, lddk, dv, lddv,
+                                   static_cast<float*>(ws), &err);
+  if (r) return fail(MST_ERR_CUDA, "attention backward: %s", err);
+  c->launches += 3;
+  cnt_op(c, (uint64_t)(5.0 * batch * heads * (double)seq * seq * head_dim), (uint64_t)(batch * seq * 8 * heads * head_dim));
   return MST_OK;
 }
 

@@ -173,6 +173,14 @@ _GRAD_READY_HOOK = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int, ctypes.
 _GRAD_SLAB_HOOK = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p)
 _SIGS["mst_ctx_set_grad_slab_hook"] = ([_VP, _VP, _VP, _I32], ctypes.c_int)
 _SIGS["mst_ctx_check"] = ([_VP, _VP], ctypes.c_int)
+_SIGS.update({  # causal GQA attention, used by attention.py
+    "mst_attention_forward": ([_VP, _VP, _VP, _I64, _VP, _I64, _VP, _I64, _VP, _I64, _VP, _I64, _I64, _I64, _I64,
+                               _I64, _I32], ctypes.c_int),
+    "mst_attention_workspace": ([_I64, _I64, _I64, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
+    "mst_attention_backward": ([_VP, _VP, _VP, _I64, _VP, _I64, _VP, _I64, _VP, _I64, _VP, _I64, _VP, _VP, _I64, _VP,
+                                _I64, _VP, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _VP, ctypes.c_size_t],
+                               ctypes.c_int),
+})
 
 
 class _Counters(ctypes.Structure):

@@ -2,6 +2,7 @@
 
   python tools/sweep.py sweep-m   # config 3: Llama2-7B widths, S=16384, M in {1,2,4,8}
   python tools/sweep.py sweep-m2  # config 2: Llama3-8B widths, S=8192, M in {1,2,4,8,16}
+  python tools/sweep.py sweep-pairs  # config 2: (M_mlp, M_head) pairs incl. the paper's (4, 16)
   python tools/sweep.py seq       # Llama3-8B widths, S = 8K..128K at chunk 1024 / 4096
   python tools/sweep.py max-seq   # config 4: Llama3-8B widths, bisection on S under the device budget
   python tools/sweep.py long      # config 4: S=65536, M=16, timed steps
@@ -102,6 +103,27 @@ def sweep_m2():
               flush=True)
 
 
+def sweep_pairs():
+    """Config 2 widths, S=8192, independent (M_mlp, M_head) -- the paper's
+    chosen setting is M=4 for the MLP and M=16 for the LM-Head (PAPER.md:449);
+    with nested plans block_step runs the chunk-wise schedule for all of them."""
+    dev = torch.device("cuda")
+    H, I, V, S = 4096, 14336, 128256, 8192
+    X, L, W = make(S, H, I, V, dev)
+    from paper_2407_15892_b200 import estimator
+
+    for mm, mh in ((1, 1), (4, 4), (4, 16), (8, 8), (8, 16), (2, 16), (16, 16)):
+        torch.cuda.reset_peak_memory_stats()
+        ms_step, loss = timed_steps(X, L, W, mm, mh)
+        print(json.dumps({"config": "2 (Llama3-8B widths, S=8192)", "M_mlp": mm, "M_head": mh,
+                          "ms_per_step": ms_step, "tokens_per_s": S / ms_step * 1e3,
+                          "executed_tflops": S * flops_per_token(H, I, V) / ms_step / 1e9,
+                          "tracked_peak_intermediate_gb": estimator.predict_block_peak(S, H, I, V, mm, mh)["inter."] / 1e9,
+                          "workspace_gb": ms.block_workspace_bytes(S, H, I, V, mm, mh, ms.Context.get(0)) / 1e9,
+                          "device_peak_allocated_gb": torch.cuda.max_memory_allocated() / 1e9, "loss": loss}),
+              flush=True)
+
+
 def seq_sweep():
     """Config-2 widths across sequence lengths at fixed chunk lengths (n = 1024
     and 4096 tokens): throughput and workspace versus S."""
@@ -172,5 +194,5 @@ def max_seq(chunk=8192):
 
 
 if __name__ == "__main__":
-    {"sweep-m": sweep_m, "sweep-m2": sweep_m2, "seq": seq_sweep, "max-seq": max_seq,
+    {"sweep-m": sweep_m, "sweep-m2": sweep_m2, "sweep-pairs": sweep_pairs, "seq": seq_sweep, "max-seq": max_seq,
      "long": long_context}[sys.argv[1]]()
