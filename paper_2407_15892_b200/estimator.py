@@ -126,10 +126,11 @@ def _paper_activation(d, I, V, G, L, N, M_mlp, M_head, recompute) -> Dict[str, i
     return {"saved": L * N * d * 2, "inter": layer_d + layer_i // M_mlp + head // M_head}
 
 
-def _repo_activation(d, I, V, G, L, N, M_mlp, M_head, recompute) -> Dict[str, int]:
+def _repo_activation(d, I, V, G, L, N, M_mlp, M_head, recompute, heads=1) -> Dict[str, int]:
     """model.py's saved set (bf16 unless noted): per layer the residual sum xs,
     and unless per-layer recompute: a = rmsnorm(xs), qkv [N, d + 2d/G], the
-    attention output o, x2, b = rmsnorm(x2) and two fp32 rstd rows; then the
+    attention output o and its fp32 log-sum-exp per head, x2, b = rmsnorm(x2)
+    and two fp32 rstd rows; then the
     final norm's input / rstd, the head-input gradient dF, the LM-Head lse and
     the int32 tokens / labels.  Intermediates: libmst's persistent context
     workspace (the largest of the MLP and LM-Head chunk workspaces) plus one
@@ -138,7 +139,7 @@ def _repo_activation(d, I, V, G, L, N, M_mlp, M_head, recompute) -> Dict[str, in
     from . import miniseq as ms
 
     kv = d // G
-    per_layer_full = N * (6 * d + 2 * kv) * 2 + 8 * N
+    per_layer_full = N * (6 * d + 2 * kv) * 2 + 8 * N + 4 * N * heads
     saved = L * (N * d * 2 if recompute else per_layer_full) + N * d * 2 * 3 + 4 * N * 2 + 8 * N
     lib = ms.load_library()
     import ctypes
@@ -171,8 +172,10 @@ def predict_peak(d: int, I: int, V: int, heads: int, G: int, layers: int, S: int
         raise ValueError("convention is 'paper' or 'repo'")
     N = S * B
     P = param_counts(d, I, V, heads, G, layers)
-    act_fn = _paper_activation if convention == "paper" else _repo_activation
-    act = act_fn(d, I, V, G, layers, N, M_mlp, M_head, recompute)
+    if convention == "paper":
+        act = _paper_activation(d, I, V, G, layers, N, M_mlp, M_head, recompute)
+    else:
+        act = _repo_activation(d, I, V, G, layers, N, M_mlp, M_head, recompute, heads)
     if convention == "paper":
         w = 2 * P["total"]
         g = 2 * P["total"]

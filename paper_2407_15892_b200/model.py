@@ -15,10 +15,12 @@ Where the arithmetic runs:
     engine (mst_gemm); Q, K, V come out of one fused [d, d + 2 d/G] weight;
   * RMSNorm (+ fused residual add) forward/backward, embedding gather /
     deterministic grouped scatter: libmst's HBM-bound kernels (csrc/layers.cu);
-  * causal grouped-query attention: torch's scaled_dot_product_attention
-    (the flash / cuDNN library kernel; the paper likewise treats attention as
-    an external FlashAttention2 kernel, "§3.1 general enough to work with any
-    attention", SPEC.md:247).
+  * causal grouped-query attention: libmst's tcgen05 attention kernels
+    (csrc/attention.cu, attention.py: forward with online softmax saving one
+    fp32 log-sum-exp per row and head, deterministic dK/dV and dQ backward
+    kernels), reading q / k / v as column slices of the fused qkv buffer and
+    writing dq / dk / dv into one d qkv buffer; the backward never re-runs
+    the forward (the paper uses FlashAttention2).
 bf16 activations, fp32 accumulation, fp32 weight gradients (and RMSNorm
 gains), token-weighted mean loss over non-ignored labels (-100).
 """
@@ -29,9 +31,9 @@ from dataclasses import dataclass, field
 from typing import Dict, List, Optional
 
 import torch
-import torch.nn.functional as F
 
 from . import miniseq as ms
+from .attention import attention_backward, attention_forward
 from .memtrack import MemTracker  # noqa: F401  (re-exported for callers)
 
 
@@ -206,6 +208,8 @@ class _LayerSaved:
     rstd1: Optional[torch.Tensor] = None
     qkv: Optional[torch.Tensor] = None
     o: Optional[torch.Tensor] = None     # attention output [N, d] (before W_o)
+    lse: Optional[torch.Tensor] = None   # attention log-sum-exp [B, heads, S] (fp32)
+    attn_graph: Optional[tuple] = None   # Ulysses: (o with its autograd graph, (q, k, v) leaves)
     x2: Optional[torch.Tensor] = None    # x + attn
     b: Optional[torch.Tensor] = None     # rmsnorm_mlp(x2)
     rstd2: Optional[torch.Tensor] = None
@@ -249,37 +253,35 @@ class Model:
                 raise ms.ConfigError("sequence parallelism shards one sequence: B must be 1")
 
     # ---------------------------------------------------------------- attention
-    def _attention(self, qkv: torch.Tensor, need_grad: bool):
-        """Causal GQA over qkv [N, d + 2d/G] -> (o [N, d], (q, k, v) autograd leaves)."""
+    def _attention(self, qkv: torch.Tensor):
+        """Causal GQA over qkv [N, d + 2d/G] -> (o [N, d], lse, graph).
+        One rank: libmst's kernel on the qkv column slices (lse saved for the
+        backward).  Sequence-parallel: Ulysses all-to-alls around the same
+        kernel under autograd; the graph is kept for the backward (no re-run)."""
         cfg = self.cfg
-        B, S, h, hd, kvh = cfg.B, cfg.S, cfg.heads, cfg.head_dim, cfg.heads // cfg.G
+        h, kvh = cfg.heads, cfg.heads // cfg.G
+        q, k, v = qkv[:, :cfg.d], qkv[:, cfg.d:cfg.d + cfg.kv], qkv[:, cfg.d + cfg.kv:]
         if self.world > 1:
             from . import ulysses
 
-            q, k, v = (qkv[:, :cfg.d].contiguous(), qkv[:, cfg.d:cfg.d + cfg.kv].contiguous(),
-                       qkv[:, cfg.d + cfg.kv:].contiguous())
-            if need_grad:
-                q, k, v = (t.requires_grad_(True) for t in (q, k, v))
-            return ulysses.attention(q, k, v, h, kvh, self.group), (q, k, v)
-        q = qkv[:, :cfg.d].reshape(B, S, h, hd).transpose(1, 2)
-        k = qkv[:, cfg.d:cfg.d + cfg.kv].reshape(B, S, kvh, hd).transpose(1, 2)
-        v = qkv[:, cfg.d + cfg.kv:].reshape(B, S, kvh, hd).transpose(1, 2)
-        if need_grad:
-            q, k, v = (t.detach().requires_grad_(True) for t in (q, k, v))
-        o = F.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=kvh != h)
-        return o.transpose(1, 2).reshape(B * S, cfg.d), (q, k, v)
+            q, k, v = (t.contiguous().requires_grad_(True) for t in (q, k, v))
+            with torch.enable_grad():
+                o = ulysses.attention(q, k, v, h, kvh, self.group)
+            return o.detach().contiguous(), None, (o, (q, k, v))
+        o, lse = attention_forward(q, k, v, cfg.B, cfg.S, h, kvh)
+        return o, lse, None
 
-    def _grad_qkv(self, leaves, N: int) -> torch.Tensor:
-        """Assemble d qkv [N, d + 2d/G] from the autograd leaves of _attention."""
+    def _attention_backward(self, qkv: torch.Tensor, o: torch.Tensor, lse, graph, do: torch.Tensor) -> torch.Tensor:
+        """d qkv [N, d + 2d/G] of the attention (dq | dk | dv written in place)."""
         cfg = self.cfg
-        q, k, v = leaves
-        if self.world > 1:
+        if graph is not None:  # Ulysses: backward through the saved graph (transposed all-to-alls)
+            o_g, (q, k, v) = graph
+            o_g.backward(do)
             return torch.cat([q.grad, k.grad, v.grad], dim=1)
-        kvh = cfg.heads // cfg.G
-        dqkv = torch.empty(N, cfg.d + 2 * cfg.kv, device=q.device, dtype=torch.bfloat16)
-        dqkv[:, :cfg.d] = q.grad.transpose(1, 2).reshape(N, cfg.d)
-        dqkv[:, cfg.d:cfg.d + cfg.kv] = k.grad.transpose(1, 2).reshape(N, kvh * cfg.head_dim)
-        dqkv[:, cfg.d + cfg.kv:] = v.grad.transpose(1, 2).reshape(N, kvh * cfg.head_dim)
+        d, kv = cfg.d, cfg.kv
+        dqkv = torch.empty_like(qkv)
+        attention_backward(qkv[:, :d], qkv[:, d:d + kv], qkv[:, d + kv:], o, do, lse, cfg.B, cfg.S, cfg.heads,
+                           cfg.heads // cfg.G, dq=dqkv[:, :d], dk=dqkv[:, d:d + kv], dv=dqkv[:, d + kv:])
         return dqkv
 
     # ---------------------------------------------------------------- forward
@@ -292,9 +294,7 @@ class Model:
         a, xs, rstd1 = rmsnorm_forward(x, lw.g_attn, cfg.eps, residual=resid)
         qkv = torch.empty(N, cfg.d + 2 * cfg.kv, device=x.device, dtype=torch.bfloat16)
         gemm(a, lw.W_qkv, N, cfg.d + 2 * cfg.kv, cfg.d, False, True, qkv)
-        with torch.no_grad():
-            o, _ = self._attention(qkv, need_grad=False)
-        o = o.contiguous()
+        o, lse, graph = self._attention(qkv)
         ao = torch.empty_like(o)
         gemm(o, lw.W_o, N, cfg.d, cfg.d, False, True, ao)
         b, x2, rstd2 = rmsnorm_forward(ao, lw.g_mlp, cfg.eps, residual=xs)
@@ -303,6 +303,7 @@ class Model:
         sv = _LayerSaved(x=xs)
         if not cfg.recompute:
             sv.a, sv.rstd1, sv.qkv, sv.o, sv.x2, sv.b, sv.rstd2, sv.mlp_saved = a, rstd1, qkv, o, x2, b, rstd2, msaved
+            sv.lse, sv.attn_graph = lse, graph
         return sv, m, x2
 
     def forward(self, tokens: torch.Tensor, labels: torch.Tensor, check: bool = True):
@@ -388,9 +389,7 @@ class Model:
             a, _, rstd1 = rmsnorm_forward(sv.x, lw.g_attn, cfg.eps)
             qkv = torch.empty(N, cfg.d + 2 * cfg.kv, device=a.device, dtype=torch.bfloat16)
             gemm(a, lw.W_qkv, N, cfg.d + 2 * cfg.kv, cfg.d, False, True, qkv)
-            with torch.no_grad():
-                o, _ = self._attention(qkv, need_grad=False)
-            o = o.contiguous()
+            o, lse, graph = self._attention(qkv)  # part of the per-layer recompute policy
             ao = torch.empty_like(o)
             gemm(o, lw.W_o, N, cfg.d, cfg.d, False, True, ao)
             b, x2, rstd2 = rmsnorm_forward(ao, lw.g_mlp, cfg.eps, residual=sv.x)
@@ -398,6 +397,7 @@ class Model:
                                                ms.make_chunk_plan(N, cfg.M_mlp))
         else:
             a, rstd1, qkv, o, x2, b, rstd2, msaved = sv.a, sv.rstd1, sv.qkv, sv.o, sv.x2, sv.b, sv.rstd2, sv.mlp_saved
+            lse, graph = sv.lse, sv.attn_graph
         mg = ms.MlpGrads(torch.empty(cfg.d, cfg.I, device=a.device), torch.empty(cfg.d, cfg.I, device=a.device),
                          torch.empty(cfg.I, cfg.d, device=a.device))
         db, _ = ms.miniseq_mlp_backward(dx3, msaved, ms.MlpWeights(lw.W_gate, lw.W_up, lw.W_down),
@@ -412,10 +412,8 @@ class Model:
         grads[f"{p}.W_o"] = dWo
         do = torch.empty_like(o)
         gemm(dx2, lw.W_o, N, cfg.d, cfg.d, False, False, do)              # dx2 W_o^T
-        # attention backward (library kernel through autograd; Ulysses all-to-alls when sharded)
-        o_re, leaves = self._attention(qkv, need_grad=True)
-        o_re.backward(do)
-        dqkv = self._grad_qkv(leaves, N).contiguous()
+        # attention backward (libmst kernels from the saved lse; Ulysses all-to-alls when sharded)
+        dqkv = self._attention_backward(qkv, o, lse, graph, do)
         dWqkv = torch.empty(cfg.d, cfg.d + 2 * cfg.kv, device=a.device, dtype=torch.float32)
         gemm(a, dqkv, cfg.d, cfg.d + 2 * cfg.kv, N, True, True, dWqkv)    # a^T dqkv
         grads[f"{p}.W_qkv"] = dWqkv

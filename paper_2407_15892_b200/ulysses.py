@@ -19,7 +19,6 @@ from typing import Optional
 
 import torch
 import torch.distributed as dist
-import torch.nn.functional as F
 from torch.distributed.nn.functional import all_to_all_single as _a2a
 
 
@@ -61,23 +60,40 @@ def head_to_seq(y: torch.Tensor, group=None) -> torch.Tensor:
     return recv.permute(1, 0, 2, 3).reshape(s, P * hp, hd)
 
 
+def _mst_attention(qh: torch.Tensor, kh: torch.Tensor, vh: torch.Tensor, heads: int, kv_heads: int) -> torch.Tensor:
+    """libmst's tcgen05 causal GQA attention (attention.CausalAttention) on the
+    head-sharded layout: q [S, h, hd], k / v [S, kvh, hd] -> [S, h, hd]."""
+    from .attention import CausalAttention
+
+    S, _, hd = qh.shape
+    o = CausalAttention.apply(qh.reshape(S, heads * hd), kh.reshape(S, kv_heads * hd), vh.reshape(S, kv_heads * hd),
+                              1, S, heads, kv_heads)
+    return o.reshape(S, heads, hd)
+
+
 def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, heads: int, kv_heads: int,
-              group=None) -> torch.Tensor:
+              group=None, attn_fn=None) -> torch.Tensor:
     """Causal grouped-query attention of one sequence sharded over `group`.
     q [S/P, heads*hd], k, v [S/P, kv_heads*hd] (this rank's tokens) ->
-    [S/P, heads*hd].  Differentiable (autograd through the all-to-alls)."""
+    [S/P, heads*hd].  Differentiable (autograd through the all-to-alls and
+    libmst's attention kernels, whose backward does not re-run the forward).
+    attn_fn(qh, kh, vh, heads_local, kv_heads_local) on [S, h, hd] views
+    replaces the kernel -- for host-tensor tests of the re-sharding only; CUDA
+    tensors always go through libmst."""
     P = _world(group)
     s = q.shape[0]
     hd = q.shape[1] // heads
     if heads % P or kv_heads % P:
         raise ValueError(f"Ulysses needs heads ({heads}) and kv heads ({kv_heads}) divisible by {P}")
+    if attn_fn is None or q.is_cuda:
+        if not q.is_cuda:
+            raise ValueError("ulysses.attention runs libmst's CUDA kernels: pass CUDA tensors")
+        attn_fn = _mst_attention
     qh = seq_to_head(q.reshape(s, heads, hd), heads, group)        # [S, h/P, hd]
     kh = seq_to_head(k.reshape(s, kv_heads, hd), kv_heads, group)  # [S, kvh/P, hd]
     vh = seq_to_head(v.reshape(s, kv_heads, hd), kv_heads, group)
-    o = F.scaled_dot_product_attention(qh.transpose(0, 1).unsqueeze(0), kh.transpose(0, 1).unsqueeze(0),
-                                       vh.transpose(0, 1).unsqueeze(0), is_causal=True,
-                                       enable_gqa=kv_heads != heads)           # [1, h/P, S, hd]
-    return head_to_seq(o[0].transpose(0, 1), group).reshape(s, heads * hd)
+    o = attn_fn(qh, kh, vh, heads // P, kv_heads // P)             # [S, h/P, hd]
+    return head_to_seq(o, group).reshape(s, heads * hd)
 
 
 def all_reduce_grads(grads: dict, group=None) -> None:

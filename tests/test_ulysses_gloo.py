@@ -26,6 +26,15 @@ def _full(q, k, v, heads, kvh):
     return o[0].transpose(0, 1).reshape(S, heads * hd)
 
 
+def _sdpa_heads(qh, kh, vh, h, kvh):
+    """Host stand-in for libmst's kernel on the head-sharded [S, h, hd] views
+    (this test checks the re-sharding collectives, not the kernel)."""
+    o = torch.nn.functional.scaled_dot_product_attention(qh.transpose(0, 1)[None], kh.transpose(0, 1)[None],
+                                                         vh.transpose(0, 1)[None], is_causal=True,
+                                                         enable_gqa=kvh != h)
+    return o[0].transpose(0, 1)
+
+
 def _worker(rank, world, port, ret, S, heads, kvh, hd):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -40,7 +49,7 @@ def _worker(rank, world, port, ret, S, heads, kvh, hd):
         s = S // world
         sl = slice(rank * s, (rank + 1) * s)
         ql, kl, vl = (t[sl].clone().requires_grad_(True) for t in (q, k, v))
-        o = ulysses.attention(ql, kl, vl, heads, kvh)
+        o = ulysses.attention(ql, kl, vl, heads, kvh, attn_fn=_sdpa_heads)
         o.backward(do[sl])
         qf, kf, vf = (t.clone().requires_grad_(True) for t in (q, k, v))
         of = _full(qf, kf, vf, heads, kvh)
