@@ -1,9 +1,27 @@
 """ncu driver: config-2 block once (warm), then ONE op under cudaProfilerStart/Stop.
-usage: ncu --profile-from-start off ... python tools/prof_op.py {mlp_fwd|head_fwd|head_bwd|mlp_bwd|step}"""
+usage: ncu --profile-from-start off ... python tools/prof_op.py {mlp_fwd|head_fwd|head_bwd|mlp_bwd|step|attn}
+(attn: libmst's causal GQA attention forward + backward at Llama3-8B heads, S=8192)"""
 import sys, torch
 sys.path.insert(0, '.')
 from paper_2407_15892_b200 import miniseq as ms
 op = sys.argv[1]
+if op == 'attn':
+    from paper_2407_15892_b200 import attention as A
+    Sa, Ha, KVa, hd = 8192, 32, 8, 128
+    torch.manual_seed(0)
+    q = torch.randn(Sa, Ha * hd, device='cuda').bfloat16()
+    k = torch.randn(Sa, KVa * hd, device='cuda').bfloat16()
+    v = torch.randn(Sa, KVa * hd, device='cuda').bfloat16()
+    do = torch.randn(Sa, Ha * hd, device='cuda').bfloat16()
+    o, lse = A.attention_forward(q, k, v, 1, Sa, Ha, KVa)
+    A.attention_backward(q, k, v, o, do, lse, 1, Sa, Ha, KVa)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
+    o, lse = A.attention_forward(q, k, v, 1, Sa, Ha, KVa)
+    A.attention_backward(q, k, v, o, do, lse, 1, Sa, Ha, KVa)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
+    sys.exit(0)
 S, M = 8192, 8
 H, I, V = 4096, 14336, 128256
 dev = 'cuda'
