@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 
 #include "attention.cuh"
@@ -288,6 +289,202 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_cg1(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------------------ forward, two q tiles per CTA
+// Ping-pong over two adjacent q tiles (A = 2p, B = 2p + 1) that share every
+// K / V tile: while the math warps of one tile run its online softmax, the
+// tensor core works on the other tile's GEMMs.  TMEM: per tile S (128 fp32
+// columns) and O (128); P is written back over the first 64 columns of S as
+// packed bf16 and read by the PV GEMM straight from TMEM (no shared-memory
+// round trip), so shared memory holds only Q (two tiles) and a 2-stage K/V
+// ring.  Softmax in two passes over TMEM (max, then exp / sum / pack), one
+// FFMA + one ex2 per element, ~70 registers per thread.
+template <int NSUB>
+__global__ void __launch_bounds__(384, 1) attn_fwd2_kernel(const __grid_constant__ Args a) {
+  constexpr int kST = 2;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* q_s = sm;                            // [2 tiles]
+  uint8_t* k_s = q_s + 2 * NSUB * kTile;        // [kST]
+  uint8_t* v_s = k_s + kST * NSUB * kTile;      // [kST]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(v_s + kST * NSUB * kTile);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;                  // [kST]
+  uint64_t* v_full = k_full + kST;              // [kST]
+  uint64_t* kv_empty = v_full + kST;            // [kST]
+  uint64_t* s_full = kv_empty + kST;            // [2 tiles]
+  uint64_t* p_full = s_full + 2;                // [2 tiles]
+  uint64_t* pv_done = p_full + 2;               // [2 tiles]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int hb = a.heads * a.B;
+  const int npair = (a.nqb + 1) / 2;
+  const int pr = npair - 1 - static_cast<int>(blockIdx.x) / hb;  // heaviest pairs first
+  const int h = static_cast<int>(blockIdx.x) % a.heads;
+  const int b = (static_cast<int>(blockIdx.x) % hb) / a.heads;
+  const int g = h / (a.heads / a.kvh);
+  const int tq[2] = {2 * pr, 2 * pr + 1};
+  const int nt[2] = {tq[0] + 1, tq[1] < a.nqb ? tq[1] + 1 : 0};  // kv tiles per q tile (causal)
+  const int ntiles = nt[1] ? 2 : 1;
+  const int nkv = nt[1] ? nt[1] : nt[0];
+  const int row0 = b * a.S;
+
+  if (warp == 1 && lane == 0) {
+    ptx::mbar_init(ptx::smem_u32(q_full), 1);
+    for (int s = 0; s < kST; ++s) {
+      ptx::mbar_init(ptx::smem_u32(&k_full[s]), 1);
+      ptx::mbar_init(ptx::smem_u32(&v_full[s]), 1);
+      ptx::mbar_init(ptx::smem_u32(&kv_empty[s]), 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      ptx::mbar_init(ptx::smem_u32(&s_full[t]), 1);
+      ptx::mbar_init(ptx::smem_u32(&p_full[t]), 4);
+      ptx::mbar_init(ptx::smem_u32(&pv_done[t]), 1);
+    }
+    ptx::fence_mbarrier_init();
+  }
+  if (warp == 0) ptx::tmem_alloc_cg1(ptx::smem_u32(tmem_slot), 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {  // warpgroup 0: TMA (w0) and MMA (w1) need few registers; the math warpgroups take them
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 72;\n" ::: "memory");
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer
+      ptx::prefetch_tmap(&a.m.q);
+      ptx::prefetch_tmap(&a.m.k);
+      ptx::prefetch_tmap(&a.m.v);
+      ptx::mbar_arrive_expect_tx(ptx::smem_u32(q_full), ntiles * NSUB * kTile);
+      for (int t = 0; t < ntiles; ++t)
+        load_tile<NSUB>(&a.m.q, ptx::smem_u32(q_s + t * NSUB * kTile), ptx::smem_u32(q_full), h, row0 + tq[t] * kBM);
+      for (int j = 0; j < nkv; ++j) {
+        const int s = j % kST;
+        ptx::mbar_wait(ptx::smem_u32(&kv_empty[s]), ((j / kST) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(ptx::smem_u32(&k_full[s]), NSUB * kTile);
+        load_tile<NSUB>(&a.m.k, ptx::smem_u32(k_s + s * NSUB * kTile), ptx::smem_u32(&k_full[s]), g, row0 + j * kBM);
+        ptx::mbar_arrive_expect_tx(ptx::smem_u32(&v_full[s]), NSUB * kTile);
+        load_tile<NSUB>(&a.m.v, ptx::smem_u32(v_s + s * NSUB * kTile), ptx::smem_u32(&v_full[s]), g, row0 + j * kBM);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      const uint32_t pv_idesc = ptx::idesc_bf16(128, 64 * NSUB, 0, 1);
+      auto qk = [&](int t, int j) {
+        const int s = j % kST;
+        ptx::mbar_wait(ptx::smem_u32(&k_full[s]), (j / kST) & 1);
+        ptx::tc_fence_after();
+        mma_tile(tmem + 256 * t, ptx::smem_u32(q_s + t * NSUB * kTile), ptx::smem_u32(k_s + s * NSUB * kTile), NSUB,
+                 128, false, false);
+        ptx::umma_commit_cg1(ptx::smem_u32(&s_full[t]));
+      };
+      ptx::mbar_wait(ptx::smem_u32(q_full), 0);
+      for (int t = 0; t < ntiles; ++t) qk(t, 0);
+      for (int j = 0; j < nkv; ++j) {
+        const int s = j % kST;
+        for (int t = 0; t < ntiles; ++t) {
+          if (j >= nt[t]) continue;
+          ptx::mbar_wait(ptx::smem_u32(&p_full[t]), j & 1);
+          ptx::mbar_wait(ptx::smem_u32(&v_full[s]), (j / kST) & 1);
+          ptx::tc_fence_after();
+          // O_t += P_t V_j: P (bf16, 64 packed columns over S_t) from TMEM, V MN-major
+          const uint32_t vb = ptx::smem_u32(v_s + s * NSUB * kTile);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            ptx::umma_bf16_tmem_a_cg1(tmem + 256 * t + 128, tmem + 256 * t + 8 * k, mdesc(vb + k * 2048), pv_idesc,
+                                      (j > 0 || k) ? 1u : 0u);
+          ptx::umma_commit_cg1(ptx::smem_u32(&pv_done[t]));
+        }
+        ptx::umma_commit_cg1(ptx::smem_u32(&kv_empty[s]));
+        for (int t = 0; t < ntiles; ++t) {
+          if (j + 1 >= nt[t]) continue;
+          ptx::mbar_wait(ptx::smem_u32(&pv_done[t]), j & 1);  // P_t consumed before S_t is overwritten
+          qk(t, j + 1);
+        }
+      }
+    }
+  }
+  } else {  // ---- online softmax: warps 4-7 tile A, 8-11 tile B, one q row per thread
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 216;\n" ::: "memory");
+    const int t = (warp - 4) >> 2;
+    if (t < ntiles) {
+      const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+      const uint32_t tS = tmem + 256 * t + lane_off, tO = tS + 128;
+      const int q0 = tq[t] * kBM;
+      const int q = q0 + ((warp & 3) * 32 + lane);
+      // Lazy rescaling: P is formed against a reference maximum `ref` (log2
+      // units) that moves only when a row's maximum exceeds it by more than 8
+      // (exact either way: P and l share the reference; p <= 2^8), so the O
+      // accumulator is rescaled only when the running maximum really jumps.
+      // The row's 128 scores come from TMEM in one batch (one load latency
+      // per tile) and stay in registers for the max and the exp passes; P is
+      // packed and written over S columns 0..63 chunk by chunk.
+      float m2 = -INFINITY, l = 0.f;
+      for (int j = 0; j < nt[t]; ++j) {
+        ptx::mbar_wait(ptx::smem_u32(&s_full[t]), j & 1);
+        ptx::tc_fence_after();
+        const int kv0 = j * kBM;
+        const int nvalid = kv0 + kBM - 1 > q0 ? q - kv0 + 1 : kBM;  // columns kv0 .. q are visible
+        float x[128];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) ptx::tmem_ld_32x32b_x32(tS + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(x + 32 * c));
+        ptx::tmem_ld_wait();
+        float mx = -INFINITY;
+#pragma unroll
+        for (int e = 0; e < 128; ++e) {
+          if (e >= nvalid) x[e] = -INFINITY;
+          mx = fmaxf(mx, x[e]);
+        }
+        const float mx2 = mx * a.scale2;
+        const float ref = (j == 0 || mx2 > m2 + 8.f) ? mx2 : m2;
+        float rs = 0.f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            const float p0 = ptx::ex2(fmaf(x[32 * c + e], a.scale2, -ref));
+            const float p1 = ptx::ex2(fmaf(x[32 * c + e + 1], a.scale2, -ref));
+            rs += p0 + p1;
+            pk[e >> 1] = ptx::pack_bf16(p0, p1);
+          }
+          ptx::tmem_st_32x32b_x16(tS + 16 * c, pk);  // P over already-read S columns
+        }
+        const float alpha = ptx::ex2(m2 - ref);  // 0 on the first tile, 1 when the reference stayed
+        // S_t(j) was issued after PV_t(j-1) completed: O_t is current here
+        if (j > 0 && !__all_sync(0xffffffffu, alpha == 1.f)) {
+          for (int c = 0; c < 2 * NSUB; ++c) {
+            uint32_t o[32];
+            ptx::tmem_ld_32x32b_x32(tO + 32 * c, o);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            ptx::tmem_st_32x32b_x32(tO + 32 * c, o);
+          }
+        }
+        l = l * alpha + rs;
+        m2 = ref;
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_local(ptx::smem_u32(&p_full[t]));
+      }
+      ptx::mbar_wait(ptx::smem_u32(&pv_done[t]), (nt[t] - 1) & 1);
+      ptx::tc_fence_after();
+      const bool ok = q < a.S;
+      store_acc_row(tO, NSUB, 1.f / l, a.o + (static_cast<int64_t>(row0) + q) * a.ldo + h * a.hd, a.hd, ok);
+      if (ok) a.lse[(static_cast<int64_t>(b) * a.heads + h) * a.S + q] = (m2 + __log2f(l)) * 0.69314718055994531f;
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc_cg1(tmem, 512);
   }
@@ -579,6 +776,10 @@ constexpr int fwd_smem() {
   return 1024 + NSUB * kTile + 2 * (NSUB == 1 ? 3 : 2) * NSUB * kTile + 2 * kTile + 256;
 }
 template <int NSUB>
+constexpr int fwd2_smem() {
+  return 1024 + 2 * NSUB * kTile + 4 * NSUB * kTile + 256;
+}
+template <int NSUB>
 constexpr int dkv_smem() {
   return 1024 + 4 * NSUB * kTile + 4 * kTile + 2048 + 256;
 }
@@ -586,7 +787,11 @@ template <int NSUB>
 constexpr int dq_smem() {
   return 1024 + 2 * NSUB * kTile + 4 * NSUB * kTile + 2 * kTile + 256;
 }
-static_assert(fwd_smem<2>() <= 232448 && dkv_smem<2>() <= 232448 && dq_smem<2>() <= 232448, "shared memory");
+static_assert(fwd_smem<2>() <= 232448 && fwd2_smem<2>() <= 232448 && dkv_smem<2>() <= 232448 &&
+                  dq_smem<2>() <= 232448,
+              "shared memory");
+
+int g_fwd_version = 2;  // attn_fwd2_kernel (ping-pong) by default; 1 = one q tile per CTA
 
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -609,6 +814,8 @@ static cudaError_t set_attrs() {
   static bool done = false;
   if (done) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<NSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem<NSUB>());
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(attn_fwd2_kernel<NSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd2_smem<NSUB>());
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(attn_dkv_kernel<NSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, dkv_smem<NSUB>());
   if (e == cudaSuccess)
@@ -639,16 +846,32 @@ int forward(void* enc, cudaStream_t st, const AttnShape& s, const void* q, int64
   a.scale2 = a.scale * kLog2e;
   a.nqb = (s.S + kBM - 1) / kBM;
   const dim3 grid(static_cast<unsigned>(a.nqb * s.heads * s.B));
+  const dim3 grid2(static_cast<unsigned>((a.nqb + 1) / 2 * s.heads * s.B));
   cudaError_t e;
+  static char msg[256];
   if (s.hd <= 64) {
     if ((e = set_attrs<1>()) != cudaSuccess) return *err = cudaGetErrorString(e), 2;
-    attn_fwd_kernel<1><<<grid, kThreads, fwd_smem<1>(), st>>>(a);
+    if (g_fwd_version == 2)
+      attn_fwd2_kernel<1><<<grid2, 384, fwd2_smem<1>(), st>>>(a);
+    else
+      attn_fwd_kernel<1><<<grid, kThreads, fwd_smem<1>(), st>>>(a);
   } else {
     if ((e = set_attrs<2>()) != cudaSuccess) return *err = cudaGetErrorString(e), 2;
-    attn_fwd_kernel<2><<<grid, kThreads, fwd_smem<2>(), st>>>(a);
+    if (g_fwd_version == 2)
+      attn_fwd2_kernel<2><<<grid2, 384, fwd2_smem<2>(), st>>>(a);
+    else
+      attn_fwd_kernel<2><<<grid, kThreads, fwd_smem<2>(), st>>>(a);
   }
   e = cudaGetLastError();
-  if (e != cudaSuccess) return *err = cudaGetErrorString(e), 2;
+  if (e != cudaSuccess) {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, s.hd <= 64 ? (const void*)attn_fwd2_kernel<1> : (const void*)attn_fwd2_kernel<2>);
+    snprintf(msg, sizeof(msg), "%s (fwd v%d: %d regs, max %d threads, %zu B static smem, %zu B local)",
+             cudaGetErrorString(e), g_fwd_version, fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes,
+             fa.localSizeBytes);
+    *err = msg;
+    return 2;
+  }
   return 0;
 }
 

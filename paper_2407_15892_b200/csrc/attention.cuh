@@ -7,6 +7,8 @@
 
 namespace mst_attn {
 
+extern int g_fwd_version;  // 2: two q tiles per CTA (default), 1: one (tuning "attn_fwd")
+
 struct AttnShape {
   int B, S, heads, kvh, hd;
 };

@@ -1138,6 +1138,9 @@ int mst_ctx_set_tuning(mst_ctx* c, const char* key, int value) {
   } else if (std::strcmp(key, "pairs") == 0) {  // diagnostics: run GEMMs on fewer CTA pairs
     if (value < 1 || value > c->max_pairs) return fail(MST_ERR_CONFIG, "pairs must be 1..%d", c->max_pairs);
     c->num_pairs = value;
+  } else if (std::strcmp(key, "attn_fwd") == 0) {  // attention forward kernel version (process-wide)
+    if (value != 1 && value != 2) return fail(MST_ERR_CONFIG, "attn_fwd must be 1 or 2");
+    mst_attn::g_fwd_version = value;
   } else if (std::strcmp(key, "tma3d") == 0) {
     c->tma3d = value != 0;
   } else {
