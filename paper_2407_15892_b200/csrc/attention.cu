@@ -435,15 +435,23 @@ __global__ void __launch_bounds__(384, 1) attn_fwd2_kernel(const __grid_constant
 #pragma unroll
         for (int c = 0; c < 4; ++c) ptx::tmem_ld_32x32b_x32(tS + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(x + 32 * c));
         ptx::tmem_ld_wait();
-        float mx = -INFINITY;
+        if (kv0 + kBM - 1 > q0) {  // the diagonal tile (warp-uniform): mask kv > q
 #pragma unroll
-        for (int e = 0; e < 128; ++e) {
-          if (e >= nvalid) x[e] = -INFINITY;
-          mx = fmaxf(mx, x[e]);
+          for (int e = 0; e < 128; ++e)
+            if (e >= nvalid) x[e] = -INFINITY;
         }
+        // 8 independent partial maxima / sums: no 128-long dependency chains
+        float m8[8], s8[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) m8[k] = x[k];
+#pragma unroll
+        for (int e = 8; e < 128; ++e) m8[e & 7] = fmaxf(m8[e & 7], x[e]);
+        const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                               fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
         const float mx2 = mx * a.scale2;
         const float ref = (j == 0 || mx2 > m2 + 8.f) ? mx2 : m2;
-        float rs = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) s8[k] = 0.f;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           uint32_t pk[16];
@@ -451,11 +459,13 @@ __global__ void __launch_bounds__(384, 1) attn_fwd2_kernel(const __grid_constant
           for (int e = 0; e < 32; e += 2) {
             const float p0 = ptx::ex2(fmaf(x[32 * c + e], a.scale2, -ref));
             const float p1 = ptx::ex2(fmaf(x[32 * c + e + 1], a.scale2, -ref));
-            rs += p0 + p1;
+            s8[e & 7] += p0;
+            s8[(e + 1) & 7] += p1;
             pk[e >> 1] = ptx::pack_bf16(p0, p1);
           }
           ptx::tmem_st_32x32b_x16(tS + 16 * c, pk);  // P over already-read S columns
         }
+        const float rs = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
         const float alpha = ptx::ex2(m2 - ref);  // 0 on the first tile, 1 when the reference stayed
         // S_t(j) was issued after PV_t(j-1) completed: O_t is current here
         if (j > 0 && !__all_sync(0xffffffffu, alpha == 1.f)) {
