@@ -54,6 +54,8 @@ struct Args {
   uint16_t* o;         // forward output (bf16)
   float* lse;          // [B, heads, S] natural-log units
   const float* delta;  // [B, heads, S] rowsum(dO * O)
+  const float* lse2p;  // [B, heads, nqb * 128] log2-units lse, +inf padded (backward v2)
+  const float* deltap; // [B, heads, nqb * 128] D, zero padded
   uint16_t *dq, *dk, *dv;
   int64_t ldo, lddq, lddk, lddv;
   int B, S, heads, kvh, hd;
@@ -780,6 +782,330 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dq_kernel(const __grid_const
   }
 }
 
+// ------------------------------------------------------------------ backward v2
+// Padded per-(b, head) rows of the log-sum-exp in log2 units (+inf past the
+// sequence: P = 0 there) and of D = rowsum(dO * O), nqb * 128 entries each,
+// so the dK/dV kernel's producer fetches a q tile's 128 values with one 512 B
+// bulk copy next to its Q / dO tiles.
+__global__ void attn_prep_kernel(const uint16_t* __restrict__ o, int64_t ldo, const uint16_t* __restrict__ dout,
+                                 int64_t lddo, const float* __restrict__ lse, float* __restrict__ lse2p,
+                                 float* __restrict__ deltap, int B, int S, int heads, int hd, int spad) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // (b, h, t < spad)
+  if (idx >= static_cast<int64_t>(B) * heads * spad) return;
+  const int t = static_cast<int>(idx % spad);
+  const int64_t bh = idx / spad;
+  const int h = static_cast<int>(bh % heads);
+  const int b = static_cast<int>(bh / heads);
+  if (t >= S) {
+    lse2p[idx] = INFINITY;
+    deltap[idx] = 0.f;
+    return;
+  }
+  const int64_t row = static_cast<int64_t>(b) * S + t;
+  const uint16_t* po = o + row * ldo + h * hd;
+  const uint16_t* pd = dout + row * lddo + h * hd;
+  float acc = 0.f;
+  for (int e = 0; e < hd; e += 8) {
+    const uint4 x = *reinterpret_cast<const uint4*>(po + e);
+    const uint4 y = *reinterpret_cast<const uint4*>(pd + e);
+    const uint32_t xa[4] = {x.x, x.y, x.z, x.w}, ya[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      acc += __uint_as_float(xa[k] << 16) * __uint_as_float(ya[k] << 16);
+      acc += __uint_as_float(xa[k] & 0xffff0000u) * __uint_as_float(ya[k] & 0xffff0000u);
+    }
+  }
+  lse2p[idx] = lse[bh * S + t] * kLog2e;
+  deltap[idx] = acc;
+}
+
+// Reads 64 columns (2 x 32) of this thread's TMEM row into v.
+__device__ __forceinline__ void load64(uint32_t taddr, float (&v)[64]) {
+  ptx::tmem_ld_32x32b_x32(taddr, *reinterpret_cast<uint32_t(*)[32]>(v));
+  ptx::tmem_ld_32x32b_x32(taddr + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+}
+
+// dK / dV, v2: P^T and dS^T go back into TMEM over the S^T / dP^T columns
+// they came from (packed bf16) and feed the dV / dK GEMMs as TMEM A operands,
+// so shared memory holds K, V and a 2-stage ring of {Q, dO, lse2, D} per q
+// tile: the next tile's loads overlap the current tile's math.
+template <int NSUB>
+__global__ void __launch_bounds__(kThreads, 1) attn_dkv2_kernel(const __grid_constant__ Args a) {
+  constexpr int kVec = 1024;  // lse2[128] + D[128]
+  constexpr int kStage = 2 * NSUB * kTile + kVec;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* k_s = sm;
+  uint8_t* v_s = k_s + NSUB * kTile;
+  uint8_t* ring = v_s + NSUB * kTile;  // [2] {Q, dO, vec}
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + 2 * kStage);
+  uint64_t* kv_full = bars;
+  uint64_t* qdo_full = bars + 1;   // [2]
+  uint64_t* qdo_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;
+  uint64_t* ps_full = bars + 6;
+  uint64_t* ps_free = bars + 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gb = a.kvh * a.B;
+  const int kblk = static_cast<int>(blockIdx.x) / gb;
+  const int g = static_cast<int>(blockIdx.x) % a.kvh;
+  const int b = (static_cast<int>(blockIdx.x) % gb) / a.kvh;
+  const int grp = a.heads / a.kvh;
+  const int k0 = kblk * kBM;
+  const int nq = a.nqb - kblk;
+  const int iters = grp * nq;
+  const int row0 = b * a.S;
+
+  if (warp == 1 && lane == 0) {
+    ptx::mbar_init(ptx::smem_u32(kv_full), 1);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(ptx::smem_u32(&qdo_full[i]), 1);
+      ptx::mbar_init(ptx::smem_u32(&qdo_empty[i]), 1);
+    }
+    ptx::mbar_init(ptx::smem_u32(s_full), 1);
+    ptx::mbar_init(ptx::smem_u32(ps_full), 4);
+    ptx::mbar_init(ptx::smem_u32(ps_free), 1);
+    ptx::fence_mbarrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc_cg1(ptx::smem_u32(tmem_slot), 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tDP = tmem + 128, tDV = tmem + 256, tDK = tmem + 384;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      ptx::mbar_arrive_expect_tx(ptx::smem_u32(kv_full), 2 * NSUB * kTile);
+      load_tile<NSUB>(&a.m.k, ptx::smem_u32(k_s), ptx::smem_u32(kv_full), g, row0 + k0);
+      load_tile<NSUB>(&a.m.v, ptx::smem_u32(v_s), ptx::smem_u32(kv_full), g, row0 + k0);
+      for (int t = 0; t < iters; ++t) {
+        const int hq = g * grp + t / nq, i = kblk + t % nq;
+        const int st = t & 1;
+        uint8_t* stage = ring + st * kStage;
+        ptx::mbar_wait(ptx::smem_u32(&qdo_empty[st]), ((t >> 1) & 1) ^ 1);
+        const uint32_t fb = ptx::smem_u32(&qdo_full[st]);
+        ptx::mbar_arrive_expect_tx(fb, 2 * NSUB * kTile + kVec);
+        load_tile<NSUB>(&a.m.q, ptx::smem_u32(stage), fb, hq, row0 + i * kBM);
+        load_tile<NSUB>(&a.m.dout, ptx::smem_u32(stage + NSUB * kTile), fb, hq, row0 + i * kBM);
+        const int64_t vo = ((static_cast<int64_t>(b) * a.heads + hq) * a.nqb + i) * kBM;
+        ptx::bulk_load_1d(ptx::smem_u32(stage + 2 * NSUB * kTile), a.lse2p + vo, 512, fb);
+        ptx::bulk_load_1d(ptx::smem_u32(stage + 2 * NSUB * kTile + 512), a.deltap + vo, 512, fb);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = ptx::idesc_bf16(128, 64 * NSUB, 0, 1);
+      ptx::mbar_wait(ptx::smem_u32(kv_full), 0);
+      for (int t = 0; t < iters; ++t) {
+        const int st = t & 1;
+        const uint32_t qs = ptx::smem_u32(ring + st * kStage), dos = qs + NSUB * kTile;
+        ptx::mbar_wait(ptx::smem_u32(&qdo_full[st]), (t >> 1) & 1);
+        if (t > 0) ptx::mbar_wait(ptx::smem_u32(ps_free), (t - 1) & 1);  // dV/dK(t-1) read P^T/dS^T
+        ptx::tc_fence_after();
+        mma_tile(tS, ptx::smem_u32(k_s), qs, NSUB, 128, false, false);    // S^T = K Q^T
+        mma_tile(tDP, ptx::smem_u32(v_s), dos, NSUB, 128, false, false);  // dP^T = V dO^T
+        ptx::umma_commit_cg1(ptx::smem_u32(s_full));
+        ptx::mbar_wait(ptx::smem_u32(ps_full), t & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {  // dV += P^T dO, dK += dS^T Q (A from TMEM, B MN-major)
+          ptx::umma_bf16_tmem_a_cg1(tDV, tS + 8 * k, mdesc(dos + k * 2048), idesc, (t > 0 || k) ? 1u : 0u);
+          ptx::umma_bf16_tmem_a_cg1(tDK, tDP + 8 * k, mdesc(qs + k * 2048), idesc, (t > 0 || k) ? 1u : 0u);
+        }
+        ptx::umma_commit_cg1(ptx::smem_u32(&qdo_empty[st]));
+        ptx::umma_commit_cg1(ptx::smem_u32(ps_free));
+      }
+    }
+  } else if (warp >= 4) {  // one kv row per thread
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const int r = (warp & 3) * 32 + lane;
+    const int kv = k0 + r;
+    for (int t = 0; t < iters; ++t) {
+      const int i = kblk + t % nq;
+      const int q0 = i * kBM;
+      const int st = t & 1;
+      const float* vec = reinterpret_cast<const float*>(ring + st * kStage + 2 * NSUB * kTile);
+      ptx::mbar_wait(ptx::smem_u32(&qdo_full[st]), (t >> 1) & 1);  // lse2 / D visible
+      ptx::mbar_wait(ptx::smem_u32(s_full), t & 1);
+      ptx::tc_fence_after();
+      const int nmask = q0 == k0 ? r : 0;  // diagonal tile: columns q < kv (c < r) are masked
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        float x[64], y[64];
+        load64(tS + lane_off + 64 * c, x);
+        load64(tDP + lane_off + 64 * c, y);
+        ptx::tmem_ld_wait();
+        uint32_t pp[32], dd[32];
+#pragma unroll
+        for (int e = 0; e < 64; e += 2) {
+          const int col = 64 * c + e;
+          float p0 = ptx::ex2(fmaf(x[e], a.scale2, -vec[col]));
+          float p1 = ptx::ex2(fmaf(x[e + 1], a.scale2, -vec[col + 1]));
+          if (col < nmask) p0 = 0.f;
+          if (col + 1 < nmask) p1 = 0.f;
+          const float d0 = p0 * (y[e] - vec[128 + col]);
+          const float d1 = p1 * (y[e + 1] - vec[128 + col + 1]);
+          pp[e >> 1] = ptx::pack_bf16(p0, p1);
+          dd[e >> 1] = ptx::pack_bf16(d0, d1);
+        }
+        ptx::tmem_st_32x32b_x32(tS + lane_off + 32 * c, pp);   // P^T over read S^T columns
+        ptx::tmem_st_32x32b_x32(tDP + lane_off + 32 * c, dd);  // dS^T over read dP^T columns
+      }
+      ptx::tmem_st_wait();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_local(ptx::smem_u32(ps_full));
+    }
+    ptx::mbar_wait(ptx::smem_u32(ps_free), (iters - 1) & 1);
+    ptx::tc_fence_after();
+    const bool ok = kv < a.S;
+    const int64_t row = static_cast<int64_t>(row0) + kv;
+    store_acc_row(tDV + lane_off, NSUB, 1.f, a.dv + row * a.lddv + g * a.hd, a.hd, ok);
+    store_acc_row(tDK + lane_off, NSUB, a.scale, a.dk + row * a.lddk + g * a.hd, a.hd, ok);
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_cg1(tmem, 512);
+  }
+}
+
+// dQ, v2: dS goes back into TMEM over the dP columns and feeds dQ += dS K as
+// the TMEM A operand; shared memory holds Q, dO and a 2-stage K/V ring.
+template <int NSUB>
+__global__ void __launch_bounds__(kThreads, 1) attn_dq2_kernel(const __grid_constant__ Args a) {
+  constexpr int kST = 2;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* q_s = sm;
+  uint8_t* do_s = q_s + NSUB * kTile;
+  uint8_t* k_s = do_s + NSUB * kTile;        // [kST]
+  uint8_t* v_s = k_s + kST * NSUB * kTile;   // [kST]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(v_s + kST * NSUB * kTile);
+  uint64_t* qdo_full = bars;
+  uint64_t* kv_full = bars + 1;        // [kST]
+  uint64_t* kv_empty = kv_full + kST;  // [kST]
+  uint64_t* s_full = kv_empty + kST;
+  uint64_t* ds_full = s_full + 1;
+  uint64_t* ds_free = ds_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ds_free + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int hb = a.heads * a.B;
+  const int qblk = a.nqb - 1 - static_cast<int>(blockIdx.x) / hb;
+  const int h = static_cast<int>(blockIdx.x) % a.heads;
+  const int b = (static_cast<int>(blockIdx.x) % hb) / a.heads;
+  const int g = h / (a.heads / a.kvh);
+  const int q0 = qblk * kBM;
+  const int nblk = qblk + 1;
+  const int row0 = b * a.S;
+
+  if (warp == 1 && lane == 0) {
+    ptx::mbar_init(ptx::smem_u32(qdo_full), 1);
+    for (int s = 0; s < kST; ++s) {
+      ptx::mbar_init(ptx::smem_u32(&kv_full[s]), 1);
+      ptx::mbar_init(ptx::smem_u32(&kv_empty[s]), 1);
+    }
+    ptx::mbar_init(ptx::smem_u32(s_full), 1);
+    ptx::mbar_init(ptx::smem_u32(ds_full), 4);
+    ptx::mbar_init(ptx::smem_u32(ds_free), 1);
+    ptx::fence_mbarrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc_cg1(ptx::smem_u32(tmem_slot), 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tDP = tmem + 128, tDQ = tmem + 256;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      ptx::mbar_arrive_expect_tx(ptx::smem_u32(qdo_full), 2 * NSUB * kTile);
+      load_tile<NSUB>(&a.m.q, ptx::smem_u32(q_s), ptx::smem_u32(qdo_full), h, row0 + q0);
+      load_tile<NSUB>(&a.m.dout, ptx::smem_u32(do_s), ptx::smem_u32(qdo_full), h, row0 + q0);
+      for (int j = 0; j < nblk; ++j) {
+        const int s = j % kST;
+        ptx::mbar_wait(ptx::smem_u32(&kv_empty[s]), ((j / kST) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(ptx::smem_u32(&kv_full[s]), 2 * NSUB * kTile);
+        load_tile<NSUB>(&a.m.k, ptx::smem_u32(k_s + s * NSUB * kTile), ptx::smem_u32(&kv_full[s]), g, row0 + j * kBM);
+        load_tile<NSUB>(&a.m.v, ptx::smem_u32(v_s + s * NSUB * kTile), ptx::smem_u32(&kv_full[s]), g, row0 + j * kBM);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = ptx::idesc_bf16(128, 64 * NSUB, 0, 1);
+      ptx::mbar_wait(ptx::smem_u32(qdo_full), 0);
+      for (int j = 0; j < nblk; ++j) {
+        const int s = j % kST;
+        const uint32_t ks = ptx::smem_u32(k_s + s * NSUB * kTile);
+        ptx::mbar_wait(ptx::smem_u32(&kv_full[s]), (j / kST) & 1);
+        if (j > 0) ptx::mbar_wait(ptx::smem_u32(ds_free), (j - 1) & 1);  // dQ(j-1) read dS
+        ptx::tc_fence_after();
+        mma_tile(tS, ptx::smem_u32(q_s), ks, NSUB, 128, false, false);                              // S
+        mma_tile(tDP, ptx::smem_u32(do_s), ptx::smem_u32(v_s + s * NSUB * kTile), NSUB, 128, false, false);  // dP
+        ptx::umma_commit_cg1(ptx::smem_u32(s_full));
+        ptx::mbar_wait(ptx::smem_u32(ds_full), j & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < 8; ++k)  // dQ += dS K (dS from TMEM, K MN-major)
+          ptx::umma_bf16_tmem_a_cg1(tDQ, tDP + 8 * k, mdesc(ks + k * 2048), idesc, (j > 0 || k) ? 1u : 0u);
+        ptx::umma_commit_cg1(ptx::smem_u32(&kv_empty[s]));
+        ptx::umma_commit_cg1(ptx::smem_u32(ds_free));
+      }
+    }
+  } else if (warp >= 4) {
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const int r = (warp & 3) * 32 + lane;
+    const int q = q0 + r;
+    const bool ok = q < a.S;
+    const int64_t o = (static_cast<int64_t>(b) * a.heads + h) * (a.nqb * kBM) + q;  // padded rows
+    const float lse2 = a.lse2p[o];
+    const float dd = a.deltap[o];
+    for (int j = 0; j < nblk; ++j) {
+      const int kv0 = j * kBM;
+      ptx::mbar_wait(ptx::smem_u32(s_full), j & 1);
+      ptx::tc_fence_after();
+      const int nvalid = kv0 + kBM - 1 > q0 ? q - kv0 + 1 : kBM;  // kv columns <= q
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        float x[64], y[64];
+        load64(tS + lane_off + 64 * c, x);
+        load64(tDP + lane_off + 64 * c, y);
+        ptx::tmem_ld_wait();
+        uint32_t d2[32];
+#pragma unroll
+        for (int e = 0; e < 64; e += 2) {
+          const int col = 64 * c + e;
+          float p0 = ptx::ex2(fmaf(x[e], a.scale2, -lse2));
+          float p1 = ptx::ex2(fmaf(x[e + 1], a.scale2, -lse2));
+          if (col >= nvalid) p0 = 0.f;
+          if (col + 1 >= nvalid) p1 = 0.f;
+          d2[e >> 1] = ptx::pack_bf16(p0 * (y[e] - dd), p1 * (y[e + 1] - dd));
+        }
+        ptx::tmem_st_32x32b_x32(tDP + lane_off + 32 * c, d2);  // dS over read dP columns
+      }
+      ptx::tmem_st_wait();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_local(ptx::smem_u32(ds_full));
+    }
+    ptx::mbar_wait(ptx::smem_u32(ds_free), (nblk - 1) & 1);
+    ptx::tc_fence_after();
+    store_acc_row(tDQ + lane_off, NSUB, a.scale, a.dq + (static_cast<int64_t>(row0) + q) * a.lddq + h * a.hd, a.hd,
+                  ok);
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_cg1(tmem, 512);
+  }
+}
+
 // ------------------------------------------------------------------ host side
 template <int NSUB>
 constexpr int fwd_smem() {
@@ -787,6 +1113,14 @@ constexpr int fwd_smem() {
 }
 template <int NSUB>
 constexpr int fwd2_smem() {
+  return 1024 + 2 * NSUB * kTile + 4 * NSUB * kTile + 256;
+}
+template <int NSUB>
+constexpr int dkv2_smem() {
+  return 1024 + 2 * NSUB * kTile + 2 * (2 * NSUB * kTile + 1024) + 256;
+}
+template <int NSUB>
+constexpr int dq2_smem() {
   return 1024 + 2 * NSUB * kTile + 4 * NSUB * kTile + 256;
 }
 template <int NSUB>
@@ -801,7 +1135,10 @@ static_assert(fwd_smem<2>() <= 232448 && fwd2_smem<2>() <= 232448 && dkv_smem<2>
                   dq_smem<2>() <= 232448,
               "shared memory");
 
+static_assert(dkv2_smem<2>() <= 232448 && dq2_smem<2>() <= 232448, "shared memory");
+
 int g_fwd_version = 2;  // attn_fwd2_kernel (ping-pong) by default; 1 = one q tile per CTA
+int g_bwd_version = 2;  // attn_dkv2 / attn_dq2 (TMEM A operands, 2-stage ring) by default; 1 = the first kernels
 
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -830,6 +1167,10 @@ static cudaError_t set_attrs() {
     e = cudaFuncSetAttribute(attn_dkv_kernel<NSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, dkv_smem<NSUB>());
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(attn_dq_kernel<NSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, dq_smem<NSUB>());
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(attn_dkv2_kernel<NSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, dkv2_smem<NSUB>());
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(attn_dq2_kernel<NSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, dq2_smem<NSUB>());
   done = e == cudaSuccess;
   return e;
 }
@@ -913,18 +1254,40 @@ int backward(void* enc, cudaStream_t st, const AttnShape& s, const void* q, int6
   a.scale2 = a.scale * kLog2e;
   a.nqb = (s.S + kBM - 1) / kBM;
   const int64_t nrow = static_cast<int64_t>(s.B) * s.heads * s.S;
-  attn_delta_kernel<<<static_cast<unsigned>((nrow + 255) / 256), 256, 0, st>>>(
-      static_cast<const uint16_t*>(o), ldo, static_cast<const uint16_t*>(dout), lddo, delta, s.B, s.S, s.heads, s.hd);
   const dim3 gkv(static_cast<unsigned>(a.nqb * s.kvh * s.B)), gq(static_cast<unsigned>(a.nqb * s.heads * s.B));
   cudaError_t e;
-  if (s.hd <= 64) {
-    if ((e = set_attrs<1>()) != cudaSuccess) return *err = cudaGetErrorString(e), 2;
-    attn_dkv_kernel<1><<<gkv, kThreads, dkv_smem<1>(), st>>>(a);
-    attn_dq_kernel<1><<<gq, kThreads, dq_smem<1>(), st>>>(a);
+  if (g_bwd_version == 2) {
+    // workspace: delta [B*heads*S] | lse2p [B*heads*spad] | deltap [B*heads*spad]
+    const int spad = a.nqb * kBM;
+    float* lse2p = delta + ((nrow + 63) / 64) * 64;
+    float* deltap = lse2p + static_cast<int64_t>(s.B) * s.heads * spad;
+    a.lse2p = lse2p;
+    a.deltap = deltap;
+    const int64_t np = static_cast<int64_t>(s.B) * s.heads * spad;
+    attn_prep_kernel<<<static_cast<unsigned>((np + 255) / 256), 256, 0, st>>>(
+        static_cast<const uint16_t*>(o), ldo, static_cast<const uint16_t*>(dout), lddo, lse, lse2p, deltap, s.B, s.S,
+        s.heads, s.hd, spad);
+    if (s.hd <= 64) {
+      if ((e = set_attrs<1>()) != cudaSuccess) return *err = cudaGetErrorString(e), 2;
+      attn_dkv2_kernel<1><<<gkv, kThreads, dkv2_smem<1>(), st>>>(a);
+      attn_dq2_kernel<1><<<gq, kThreads, dq2_smem<1>(), st>>>(a);
+    } else {
+      if ((e = set_attrs<2>()) != cudaSuccess) return *err = cudaGetErrorString(e), 2;
+      attn_dkv2_kernel<2><<<gkv, kThreads, dkv2_smem<2>(), st>>>(a);
+      attn_dq2_kernel<2><<<gq, kThreads, dq2_smem<2>(), st>>>(a);
+    }
   } else {
-    if ((e = set_attrs<2>()) != cudaSuccess) return *err = cudaGetErrorString(e), 2;
-    attn_dkv_kernel<2><<<gkv, kThreads, dkv_smem<2>(), st>>>(a);
-    attn_dq_kernel<2><<<gq, kThreads, dq_smem<2>(), st>>>(a);
+    attn_delta_kernel<<<static_cast<unsigned>((nrow + 255) / 256), 256, 0, st>>>(
+        static_cast<const uint16_t*>(o), ldo, static_cast<const uint16_t*>(dout), lddo, delta, s.B, s.S, s.heads, s.hd);
+    if (s.hd <= 64) {
+      if ((e = set_attrs<1>()) != cudaSuccess) return *err = cudaGetErrorString(e), 2;
+      attn_dkv_kernel<1><<<gkv, kThreads, dkv_smem<1>(), st>>>(a);
+      attn_dq_kernel<1><<<gq, kThreads, dq_smem<1>(), st>>>(a);
+    } else {
+      if ((e = set_attrs<2>()) != cudaSuccess) return *err = cudaGetErrorString(e), 2;
+      attn_dkv_kernel<2><<<gkv, kThreads, dkv_smem<2>(), st>>>(a);
+      attn_dq_kernel<2><<<gq, kThreads, dq_smem<2>(), st>>>(a);
+    }
   }
   e = cudaGetLastError();
   if (e != cudaSuccess) return *err = cudaGetErrorString(e), 2;

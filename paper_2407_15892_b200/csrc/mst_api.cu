@@ -1141,6 +1141,9 @@ int mst_ctx_set_tuning(mst_ctx* c, const char* key, int value) {
   } else if (std::strcmp(key, "attn_fwd") == 0) {  // attention forward kernel version (process-wide)
     if (value != 1 && value != 2) return fail(MST_ERR_CONFIG, "attn_fwd must be 1 or 2");
     mst_attn::g_fwd_version = value;
+  } else if (std::strcmp(key, "attn_bwd") == 0) {  // attention backward kernel version (process-wide)
+    if (value != 1 && value != 2) return fail(MST_ERR_CONFIG, "attn_bwd must be 1 or 2");
+    mst_attn::g_bwd_version = value;
   } else if (std::strcmp(key, "tma3d") == 0) {
     c->tma3d = value != 0;
   } else {
@@ -2318,7 +2321,9 @@ int mst_attention_forward(mst_ctx* c, void* stream, const void* q, int64_t ldq, 
 int mst_attention_workspace(int64_t batch, int64_t seq, int64_t heads, size_t* bytes) {
   if (!bytes) return fail(MST_ERR_CONFIG, "NULL output");
   if (batch < 1 || seq < 1 || heads < 1) return fail(MST_ERR_SHAPE, "attention extents must be >= 1");
-  *bytes = align_up(size_t(batch) * heads * seq * 4, 256);  // D = rowsum(dO * O), fp32
+  // D = rowsum(dO * O) [B, heads, S] fp32, then the 128-padded lse (log2 units) and D rows
+  const size_t spad = size_t((seq + 127) / 128) * 128;
+  *bytes = align_up((size_t(batch) * heads * seq + 63) / 64 * 64 * 4 + 2 * size_t(batch) * heads * spad * 4, 256);
   return MST_OK;
 }
 
