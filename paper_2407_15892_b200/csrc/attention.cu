@@ -62,6 +62,7 @@ struct Args {
   float scale2;        // softmax scale * log2(e)
   float scale;         // softmax scale
   int nqb;             // q (= kv) tiles per sequence
+  int inorder;         // g_mma_inorder
 };
 
 __device__ __forceinline__ uint64_t kdesc(uint32_t saddr) { return ptx::sdesc_sw128(saddr, 16, 1024); }
@@ -406,7 +407,7 @@ __global__ void __launch_bounds__(384, 1) attn_fwd2_kernel(const __grid_constant
         ptx::umma_commit_cg1(ptx::smem_u32(&kv_empty[s]));
         for (int t = 0; t < ntiles; ++t) {
           if (j + 1 >= nt[t]) continue;
-          ptx::mbar_wait(ptx::smem_u32(&pv_done[t]), j & 1);  // P_t consumed before S_t is overwritten
+          if (!a.inorder) ptx::mbar_wait(ptx::smem_u32(&pv_done[t]), j & 1);  // P_t consumed before S_t is overwritten
           qk(t, j + 1);
         }
       }
@@ -903,7 +904,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dkv2_kernel(const __grid_con
         const int st = t & 1;
         const uint32_t qs = ptx::smem_u32(ring + st * kStage), dos = qs + NSUB * kTile;
         ptx::mbar_wait(ptx::smem_u32(&qdo_full[st]), (t >> 1) & 1);
-        if (t > 0) ptx::mbar_wait(ptx::smem_u32(ps_free), (t - 1) & 1);  // dV/dK(t-1) read P^T/dS^T
+        if (t > 0 && !a.inorder) ptx::mbar_wait(ptx::smem_u32(ps_free), (t - 1) & 1);  // dV/dK(t-1) read P^T/dS^T
         ptx::tc_fence_after();
         mma_tile(tS, ptx::smem_u32(k_s), qs, NSUB, 128, false, false);    // S^T = K Q^T
         mma_tile(tDP, ptx::smem_u32(v_s), dos, NSUB, 128, false, false);  // dP^T = V dO^T
@@ -1043,7 +1044,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dq2_kernel(const __grid_cons
         const int s = j % kST;
         const uint32_t ks = ptx::smem_u32(k_s + s * NSUB * kTile);
         ptx::mbar_wait(ptx::smem_u32(&kv_full[s]), (j / kST) & 1);
-        if (j > 0) ptx::mbar_wait(ptx::smem_u32(ds_free), (j - 1) & 1);  // dQ(j-1) read dS
+        if (j > 0 && !a.inorder) ptx::mbar_wait(ptx::smem_u32(ds_free), (j - 1) & 1);  // dQ(j-1) read dS
         ptx::tc_fence_after();
         mma_tile(tS, ptx::smem_u32(q_s), ks, NSUB, 128, false, false);                              // S
         mma_tile(tDP, ptx::smem_u32(do_s), ptx::smem_u32(v_s + s * NSUB * kTile), NSUB, 128, false, false);  // dP
@@ -1139,6 +1140,10 @@ static_assert(dkv2_smem<2>() <= 232448 && dq2_smem<2>() <= 232448, "shared memor
 
 int g_fwd_version = 2;  // attn_fwd2_kernel (ping-pong) by default; 1 = one q tile per CTA
 int g_bwd_version = 2;  // attn_dkv2 / attn_dq2 (TMEM A operands, 2-stage ring) by default; 1 = the first kernels
+// 1: rely on tcgen05.mma executing in issue order (an MMA that overwrites TMEM
+// columns an earlier MMA of the same thread reads as its A operand is issued
+// without waiting for that MMA's completion); 0: wait for the commit first.
+int g_mma_inorder = 0;
 
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -1196,6 +1201,7 @@ int forward(void* enc, cudaStream_t st, const AttnShape& s, const void* q, int64
   a.scale = 1.f / sqrtf(static_cast<float>(s.hd));
   a.scale2 = a.scale * kLog2e;
   a.nqb = (s.S + kBM - 1) / kBM;
+  a.inorder = g_mma_inorder;
   const dim3 grid(static_cast<unsigned>(a.nqb * s.heads * s.B));
   const dim3 grid2(static_cast<unsigned>((a.nqb + 1) / 2 * s.heads * s.B));
   cudaError_t e;
@@ -1253,6 +1259,7 @@ int backward(void* enc, cudaStream_t st, const AttnShape& s, const void* q, int6
   a.scale = 1.f / sqrtf(static_cast<float>(s.hd));
   a.scale2 = a.scale * kLog2e;
   a.nqb = (s.S + kBM - 1) / kBM;
+  a.inorder = g_mma_inorder;
   const int64_t nrow = static_cast<int64_t>(s.B) * s.heads * s.S;
   const dim3 gkv(static_cast<unsigned>(a.nqb * s.kvh * s.B)), gq(static_cast<unsigned>(a.nqb * s.heads * s.B));
   cudaError_t e;
