@@ -843,10 +843,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dkv2_kernel(const __grid_con
   uint64_t* kv_full = bars;
   uint64_t* qdo_full = bars + 1;   // [2]
   uint64_t* qdo_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;
-  uint64_t* ps_full = bars + 6;
-  uint64_t* ps_free = bars + 7;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  uint64_t* s_full = bars + 5;   // S^T in TMEM
+  uint64_t* ps_full = bars + 6;  // dS^T written (math -> MMA)
+  uint64_t* ps_free = bars + 7;  // dV / dK of the tile done
+  uint64_t* dp_full = bars + 8;  // dP^T in TMEM
+  uint64_t* p_full = bars + 9;   // P^T written (math -> MMA)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gb = a.kvh * a.B;
@@ -868,6 +870,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dkv2_kernel(const __grid_con
     ptx::mbar_init(ptx::smem_u32(s_full), 1);
     ptx::mbar_init(ptx::smem_u32(ps_full), 4);
     ptx::mbar_init(ptx::smem_u32(ps_free), 1);
+    ptx::mbar_init(ptx::smem_u32(dp_full), 1);
+    ptx::mbar_init(ptx::smem_u32(p_full), 4);
     ptx::fence_mbarrier_init();
   }
   if (warp == 2) ptx::tmem_alloc_cg1(ptx::smem_u32(tmem_slot), 512);
@@ -907,15 +911,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dkv2_kernel(const __grid_con
         if (t > 0 && !a.inorder) ptx::mbar_wait(ptx::smem_u32(ps_free), (t - 1) & 1);  // dV/dK(t-1) read P^T/dS^T
         ptx::tc_fence_after();
         mma_tile(tS, ptx::smem_u32(k_s), qs, NSUB, 128, false, false);    // S^T = K Q^T
-        mma_tile(tDP, ptx::smem_u32(v_s), dos, NSUB, 128, false, false);  // dP^T = V dO^T
         ptx::umma_commit_cg1(ptx::smem_u32(s_full));
+        mma_tile(tDP, ptx::smem_u32(v_s), dos, NSUB, 128, false, false);  // dP^T = V dO^T (under the exp pass)
+        ptx::umma_commit_cg1(ptx::smem_u32(dp_full));
+        ptx::mbar_wait(ptx::smem_u32(p_full), t & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < 8; ++k)  // dV += P^T dO (under the dS pass)
+          ptx::umma_bf16_tmem_a_cg1(tDV, tS + 8 * k, mdesc(dos + k * 2048), idesc, (t > 0 || k) ? 1u : 0u);
         ptx::mbar_wait(ptx::smem_u32(ps_full), t & 1);
         ptx::tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {  // dV += P^T dO, dK += dS^T Q (A from TMEM, B MN-major)
-          ptx::umma_bf16_tmem_a_cg1(tDV, tS + 8 * k, mdesc(dos + k * 2048), idesc, (t > 0 || k) ? 1u : 0u);
+        for (int k = 0; k < 8; ++k)  // dK += dS^T Q
           ptx::umma_bf16_tmem_a_cg1(tDK, tDP + 8 * k, mdesc(qs + k * 2048), idesc, (t > 0 || k) ? 1u : 0u);
-        }
         ptx::umma_commit_cg1(ptx::smem_u32(&qdo_empty[st]));
         ptx::umma_commit_cg1(ptx::smem_u32(ps_free));
       }
@@ -933,27 +941,43 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dkv2_kernel(const __grid_con
       ptx::mbar_wait(ptx::smem_u32(s_full), t & 1);
       ptx::tc_fence_after();
       const int nmask = q0 == k0 ? r : 0;  // diagonal tile: columns q < kv (c < r) are masked
+      float p[128];
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        float x[64], y[64];
-        load64(tS + lane_off + 64 * c, x);
-        load64(tDP + lane_off + 64 * c, y);
+      for (int c = 0; c < 2; ++c) {  // P^T from S^T; packed over the read S^T columns
+        load64(tS + lane_off + 64 * c, *reinterpret_cast<float(*)[64]>(p + 64 * c));
         ptx::tmem_ld_wait();
-        uint32_t pp[32], dd[32];
+        uint32_t pp[32];
 #pragma unroll
         for (int e = 0; e < 64; e += 2) {
           const int col = 64 * c + e;
-          float p0 = ptx::ex2(fmaf(x[e], a.scale2, -vec[col]));
-          float p1 = ptx::ex2(fmaf(x[e + 1], a.scale2, -vec[col + 1]));
+          float p0 = ptx::ex2(fmaf(p[col], a.scale2, -vec[col]));
+          float p1 = ptx::ex2(fmaf(p[col + 1], a.scale2, -vec[col + 1]));
           if (col < nmask) p0 = 0.f;
           if (col + 1 < nmask) p1 = 0.f;
-          const float d0 = p0 * (y[e] - vec[128 + col]);
-          const float d1 = p1 * (y[e + 1] - vec[128 + col + 1]);
+          p[col] = p0;
+          p[col + 1] = p1;
           pp[e >> 1] = ptx::pack_bf16(p0, p1);
-          dd[e >> 1] = ptx::pack_bf16(d0, d1);
         }
-        ptx::tmem_st_32x32b_x32(tS + lane_off + 32 * c, pp);   // P^T over read S^T columns
-        ptx::tmem_st_32x32b_x32(tDP + lane_off + 32 * c, dd);  // dS^T over read dP^T columns
+        ptx::tmem_st_32x32b_x32(tS + lane_off + 32 * c, pp);
+      }
+      ptx::tmem_st_wait();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_local(ptx::smem_u32(p_full));  // dV GEMM may start
+      ptx::mbar_wait(ptx::smem_u32(dp_full), t & 1);
+      ptx::tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {  // dS^T = P^T (dP^T - D); packed over the read dP^T columns
+        float y[64];
+        load64(tDP + lane_off + 64 * c, y);
+        ptx::tmem_ld_wait();
+        uint32_t dd[32];
+#pragma unroll
+        for (int e = 0; e < 64; e += 2) {
+          const int col = 64 * c + e;
+          dd[e >> 1] = ptx::pack_bf16(p[col] * (y[e] - vec[128 + col]), p[col + 1] * (y[e + 1] - vec[128 + col + 1]));
+        }
+        ptx::tmem_st_32x32b_x32(tDP + lane_off + 32 * c, dd);
       }
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
@@ -993,7 +1017,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dq2_kernel(const __grid_cons
   uint64_t* s_full = kv_empty + kST;
   uint64_t* ds_full = s_full + 1;
   uint64_t* ds_free = ds_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ds_free + 1);
+  uint64_t* dp_full = ds_free + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dp_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int hb = a.heads * a.B;
@@ -1014,6 +1039,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dq2_kernel(const __grid_cons
     ptx::mbar_init(ptx::smem_u32(s_full), 1);
     ptx::mbar_init(ptx::smem_u32(ds_full), 4);
     ptx::mbar_init(ptx::smem_u32(ds_free), 1);
+    ptx::mbar_init(ptx::smem_u32(dp_full), 1);
     ptx::fence_mbarrier_init();
   }
   if (warp == 2) ptx::tmem_alloc_cg1(ptx::smem_u32(tmem_slot), 512);
@@ -1046,9 +1072,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dq2_kernel(const __grid_cons
         ptx::mbar_wait(ptx::smem_u32(&kv_full[s]), (j / kST) & 1);
         if (j > 0 && !a.inorder) ptx::mbar_wait(ptx::smem_u32(ds_free), (j - 1) & 1);  // dQ(j-1) read dS
         ptx::tc_fence_after();
-        mma_tile(tS, ptx::smem_u32(q_s), ks, NSUB, 128, false, false);                              // S
-        mma_tile(tDP, ptx::smem_u32(do_s), ptx::smem_u32(v_s + s * NSUB * kTile), NSUB, 128, false, false);  // dP
+        mma_tile(tS, ptx::smem_u32(q_s), ks, NSUB, 128, false, false);  // S
         ptx::umma_commit_cg1(ptx::smem_u32(s_full));
+        mma_tile(tDP, ptx::smem_u32(do_s), ptx::smem_u32(v_s + s * NSUB * kTile), NSUB, 128, false, false);  // dP
+        ptx::umma_commit_cg1(ptx::smem_u32(dp_full));
         ptx::mbar_wait(ptx::smem_u32(ds_full), j & 1);
         ptx::tc_fence_after();
 #pragma unroll
@@ -1071,21 +1098,27 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dq2_kernel(const __grid_cons
       ptx::mbar_wait(ptx::smem_u32(s_full), j & 1);
       ptx::tc_fence_after();
       const int nvalid = kv0 + kBM - 1 > q0 ? q - kv0 + 1 : kBM;  // kv columns <= q
+      float p[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) ptx::tmem_ld_32x32b_x32(tS + lane_off + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(p + 32 * c));
+      ptx::tmem_ld_wait();
+#pragma unroll
+      for (int e = 0; e < 128; ++e) {  // P (the exp pass runs under the dP GEMM)
+        const float x = ptx::ex2(fmaf(p[e], a.scale2, -lse2));
+        p[e] = e < nvalid ? x : 0.f;
+      }
+      ptx::mbar_wait(ptx::smem_u32(dp_full), j & 1);
+      ptx::tc_fence_after();
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        float x[64], y[64];
-        load64(tS + lane_off + 64 * c, x);
+        float y[64];
         load64(tDP + lane_off + 64 * c, y);
         ptx::tmem_ld_wait();
         uint32_t d2[32];
 #pragma unroll
         for (int e = 0; e < 64; e += 2) {
           const int col = 64 * c + e;
-          float p0 = ptx::ex2(fmaf(x[e], a.scale2, -lse2));
-          float p1 = ptx::ex2(fmaf(x[e + 1], a.scale2, -lse2));
-          if (col >= nvalid) p0 = 0.f;
-          if (col + 1 >= nvalid) p1 = 0.f;
-          d2[e >> 1] = ptx::pack_bf16(p0 * (y[e] - dd), p1 * (y[e + 1] - dd));
+          d2[e >> 1] = ptx::pack_bf16(p[col] * (y[e] - dd), p[col + 1] * (y[e + 1] - dd));
         }
         ptx::tmem_st_32x32b_x32(tDP + lane_off + 32 * c, d2);  // dS over read dP columns
       }
@@ -1118,7 +1151,7 @@ constexpr int fwd2_smem() {
 }
 template <int NSUB>
 constexpr int dkv2_smem() {
-  return 1024 + 2 * NSUB * kTile + 2 * (2 * NSUB * kTile + 1024) + 256;
+  return 1024 + 2 * NSUB * kTile + 2 * (2 * NSUB * kTile + 1024) + 256;  // bars: 10 x 8 B + TMEM slot
 }
 template <int NSUB>
 constexpr int dq2_smem() {
