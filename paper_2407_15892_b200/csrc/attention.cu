@@ -1014,8 +1014,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dq2_kernel(const __grid_cons
   uint64_t* qdo_full = bars;
   uint64_t* kv_full = bars + 1;        // [kST]
   uint64_t* kv_empty = kv_full + kST;  // [kST]
-  uint64_t* s_full = kv_empty + kST;
-  uint64_t* ds_full = s_full + 1;
+  uint64_t* s_full = kv_empty + kST;  // [2]: S double-buffered in TMEM
+  uint64_t* ds_full = s_full + 2;
   uint64_t* ds_free = ds_full + 1;
   uint64_t* dp_full = ds_free + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dp_full + 1);
@@ -1036,7 +1036,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dq2_kernel(const __grid_cons
       ptx::mbar_init(ptx::smem_u32(&kv_full[s]), 1);
       ptx::mbar_init(ptx::smem_u32(&kv_empty[s]), 1);
     }
-    ptx::mbar_init(ptx::smem_u32(s_full), 1);
+    ptx::mbar_init(ptx::smem_u32(&s_full[0]), 1);
+    ptx::mbar_init(ptx::smem_u32(&s_full[1]), 1);
     ptx::mbar_init(ptx::smem_u32(ds_full), 4);
     ptx::mbar_init(ptx::smem_u32(ds_free), 1);
     ptx::mbar_init(ptx::smem_u32(dp_full), 1);
@@ -1047,7 +1048,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dq2_kernel(const __grid_cons
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS = tmem, tDP = tmem + 128, tDQ = tmem + 256;
+  const uint32_t tS2[2] = {tmem, tmem + 128}, tDP = tmem + 256, tDQ = tmem + 384;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -1066,16 +1067,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dq2_kernel(const __grid_cons
     if (lane == 0) {
       const uint32_t idesc = ptx::idesc_bf16(128, 64 * NSUB, 0, 1);
       ptx::mbar_wait(ptx::smem_u32(qdo_full), 0);
+      auto s_mma = [&](int j) {  // S(j) = Q K_j^T into buffer j & 1
+        const int s = j % kST;
+        ptx::mbar_wait(ptx::smem_u32(&kv_full[s]), (j / kST) & 1);
+        ptx::tc_fence_after();
+        mma_tile(tS2[j & 1], ptx::smem_u32(q_s), ptx::smem_u32(k_s + s * NSUB * kTile), NSUB, 128, false, false);
+        ptx::umma_commit_cg1(ptx::smem_u32(&s_full[j & 1]));
+      };
+      s_mma(0);
       for (int j = 0; j < nblk; ++j) {
         const int s = j % kST;
         const uint32_t ks = ptx::smem_u32(k_s + s * NSUB * kTile);
-        ptx::mbar_wait(ptx::smem_u32(&kv_full[s]), (j / kST) & 1);
         if (j > 0 && !a.inorder) ptx::mbar_wait(ptx::smem_u32(ds_free), (j - 1) & 1);  // dQ(j-1) read dS
-        ptx::tc_fence_after();
-        mma_tile(tS, ptx::smem_u32(q_s), ks, NSUB, 128, false, false);  // S
-        ptx::umma_commit_cg1(ptx::smem_u32(s_full));
         mma_tile(tDP, ptx::smem_u32(do_s), ptx::smem_u32(v_s + s * NSUB * kTile), NSUB, 128, false, false);  // dP
         ptx::umma_commit_cg1(ptx::smem_u32(dp_full));
+        if (j + 1 < nblk) s_mma(j + 1);  // the next scores under this tile's dS pass
         ptx::mbar_wait(ptx::smem_u32(ds_full), j & 1);
         ptx::tc_fence_after();
 #pragma unroll
@@ -1095,12 +1101,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dq2_kernel(const __grid_cons
     const float dd = a.deltap[o];
     for (int j = 0; j < nblk; ++j) {
       const int kv0 = j * kBM;
-      ptx::mbar_wait(ptx::smem_u32(s_full), j & 1);
+      ptx::mbar_wait(ptx::smem_u32(&s_full[j & 1]), (j >> 1) & 1);
       ptx::tc_fence_after();
       const int nvalid = kv0 + kBM - 1 > q0 ? q - kv0 + 1 : kBM;  // kv columns <= q
       float p[128];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) ptx::tmem_ld_32x32b_x32(tS + lane_off + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(p + 32 * c));
+      for (int c = 0; c < 4; ++c)
+        ptx::tmem_ld_32x32b_x32(tS2[j & 1] + lane_off + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(p + 32 * c));
       ptx::tmem_ld_wait();
 #pragma unroll
       for (int e = 0; e < 128; ++e) {  // P (the exp pass runs under the dP GEMM)
