@@ -79,3 +79,27 @@ def test_two_rank_sequence_parallel_equals_single_gpu(slabs):
             err = float((ret[r][k].double() - ref).norm() / ref.norm())
             assert err <= 1e-5, (r, k, err)
         assert torch.equal(ret[r]["dWo"], ret[0]["dWo"])  # every rank holds the same reduced gradient
+
+
+def test_bench_multi_rank_path_runs():
+    """bench.py itself under torchrun with two ranks on one GPU (MST_SAME_DEVICE=1,
+    gloo): the N>1 code path (global valid count, slab all-reduces, max-over-ranks
+    timing, e2e with dX copied back) runs and prints one JSON line from rank 0."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    env = dict(__import__("os").environ, MST_SAME_DEVICE="1", MST_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), str(root / "bench.py"), "--gpus", "2", "--steps", "2",
+           "--warmup", "3", "--seq", "2048", "--no-max-seq"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["global_tokens"] == 4096 and d["value"] > 0
+    assert d["e2e"]["d2h_bytes_per_step"] == 4 + 2048 * 4096 * 2
+    assert "slab" in d["config"]["schedule"]
