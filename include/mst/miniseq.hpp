@@ -220,6 +220,37 @@ inline void block_step_host(Context& ctx, void* stream, const void* X_host, cons
                                ws.bytes));
 }
 
+// Deferred device-side errors (mst.h "Deferred errors"): synchronise `stream`
+// and throw DataError / NonFiniteError if an earlier call on the context hit
+// an all-ignored batch, invalid labels or a non-finite loss.
+inline void check(Context& ctx, void* stream) { throw_on(mst_ctx_check(ctx.get(), stream)); }
+
+// Causal grouped-query attention (attn_forward / attn_backward)
+// on the tcgen05 kernels: token-major bf16 tensors with row strides (ld) in
+// elements; lse fp32 [batch, heads, seq].
+struct AttnShape {
+  int64_t batch, seq, heads, kv_heads, head_dim;
+};
+inline void attention_forward(Context& ctx, void* stream, const AttnShape& s, const void* q, int64_t ldq,
+                              const void* k, int64_t ldk, const void* v, int64_t ldv, void* o, int64_t ldo,
+                              float* lse) {
+  throw_on(mst_attention_forward(ctx.get(), stream, q, ldq, k, ldk, v, ldv, o, ldo, lse, s.batch, s.seq, s.heads,
+                                 s.kv_heads, s.head_dim, 1));
+}
+inline size_t attention_workspace_bytes(const AttnShape& s) {
+  size_t b = 0;
+  throw_on(mst_attention_workspace(s.batch, s.seq, s.heads, &b));
+  return b;
+}
+inline void attention_backward(Context& ctx, void* stream, const AttnShape& s, const void* q, int64_t ldq,
+                               const void* k, int64_t ldk, const void* v, int64_t ldv, const void* o, int64_t ldo,
+                               const void* dout, int64_t lddo, const float* lse, void* dq, int64_t lddq, void* dk,
+                               int64_t lddk, void* dv, int64_t lddv, Workspace ws) {
+  throw_on(mst_attention_backward(ctx.get(), stream, q, ldq, k, ldk, v, ldv, o, ldo, dout, lddo, lse, dq, lddq, dk,
+                                  lddk, dv, lddv, s.batch, s.seq, s.heads, s.kv_heads, s.head_dim, 1, ws.data,
+                                  ws.bytes));
+}
+
 // Op counters of the context (memtrack.hpp:19-35 conventions; mst.h "memtrack").
 inline mst_counters counters(const Context& ctx) {
   mst_counters c{};

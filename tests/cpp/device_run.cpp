@@ -142,6 +142,29 @@ int main(int argc, char** argv) {
     std::printf("tracked inter. peak %llu\n", (unsigned long long)rs.report.peak_for_prefix("inter."));
     std::printf("tracked block flops %llu\n", (unsigned long long)rs.counters.flops);
 #endif
+    // causal GQA attention through the header: q = X viewed as [N, d] with
+    // d / 64 heads of 64, k / v = column slices of X (kv_heads = heads / 2)
+    if (d % 128 == 0) {
+      const mst::AttnShape as{1, N, d / 64, d / 128, 64};
+      const int64_t kvw = as.kv_heads * 64;
+      auto* lse_a = static_cast<float*>(zeros(as.heads * N * 4));
+      void* ao = zeros(N * d * 2);
+      mst::attention_forward(ctx, st, as, X, d, X, d, static_cast<const char*>(X) + kvw * 2, d, ao, d, lse_a);
+      const size_t awb = mst::attention_workspace_bytes(as);
+      mst::Workspace aws{zeros(awb), awb};
+      void* adq = zeros(N * d * 2);
+      void* adk = zeros(N * kvw * 2);
+      void* adv = zeros(N * kvw * 2);
+      mst::attention_backward(ctx, st, as, X, d, X, d, static_cast<const char*>(X) + kvw * 2, d, ao, d, O, d, lse_a,
+                              adq, d, adk, kvw, adv, kvw, aws);
+      CK(cudaStreamSynchronize(st));
+      download(dir + "/attn_o.bf16", ao, N * d * 2);
+      download(dir + "/attn_lse.f32", lse_a, as.heads * N * 4);
+      download(dir + "/attn_dq.bf16", adq, N * d * 2);
+      download(dir + "/attn_dk.bf16", adk, N * kvw * 2);
+      download(dir + "/attn_dv.bf16", adv, N * kvw * 2);
+    }
+    mst::check(ctx, st);  // no deferred error pending
     // errors still map onto the reference's types on the device path
     bool threw = false;
     try {

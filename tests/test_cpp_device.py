@@ -74,6 +74,20 @@ def test_cpp_binding_on_device_bitwise_equal_to_python(orc, tmp_path, shape):
                                ("blk_dWd", bg.W_down, "f32", (I, H)), ("blk_dWout", bg.W_out, "f32", (H, V))):
         got = load(name + (".bf16" if dt == "bf16" else ".f32"), dt, shp)
         assert torch.equal(got, ref.cpu()), name
+    if H % 128 == 0:  # attention through the header (device_run.cpp): q = X, k / v = column slices of X
+        from paper_2407_15892_b200 import attention as A
+
+        heads, kvh = H // 64, H // 128
+        kvw = kvh * 64
+        Xg = g["X"]
+        ao, alse = A.attention_forward(Xg, Xg[:, :kvw], Xg[:, kvw:2 * kvw], 1, N, heads, kvh)
+        dq, dk, dv = A.attention_backward(Xg, Xg[:, :kvw], Xg[:, kvw:2 * kvw], ao, O, alse, 1, N, heads, kvh)
+        torch.cuda.synchronize()
+        for name, ref, dt, shp in (("attn_o", ao, "bf16", (N, H)), ("attn_lse", alse.reshape(-1), "f32", (heads * N,)),
+                                   ("attn_dq", dq, "bf16", (N, H)), ("attn_dk", dk, "bf16", (N, kvw)),
+                                   ("attn_dv", dv, "bf16", (N, kvw))):
+            got = load(name + (".bf16" if dt == "bf16" else ".f32"), dt, shp)
+            assert torch.equal(got, ref.cpu()), name
     lines = dict(line.rsplit(" ", 1) for line in out.stdout.splitlines() if line.startswith("tracked"))
     if lines:  # built against the reference's minitrain/memtrack.hpp
         nested = {r[0] for r in pm.ranges} <= {r[0] for r in ph.ranges}
