@@ -123,6 +123,12 @@ struct mst_ctx {
   // Which GEMMs of the chunk-wise block use wide tiles (bit mask, tuning key
   // "wide_mask"): 1 K3', 2 K5, 4 K2, 8 K9, 16 K7a, 32 K1.
   int wide_mask = 0;
+  // Chunk-wise block: K8 / K10 of chunks (2k, 2k+1) as one K = 2n accumulation
+  // (one fp32 dW read-modify-write per two chunks; a second dG / dU / h^T /
+  // X^T chunk set stays live through the next chunk's head), and K9(j) in
+  // K1(j+1)'s launch instead of K2(j+1)'s (tuning "pair_dw", "k9_in_k1").
+  int pair_dw = 1;   // measured +1.6..1.9% at M = 4 / 8 / 16 (config 2)
+  int k9_in_k1 = 0;  // measured -0.5%: off
   int fuse_swiglu_bwd = 0;  // 1: chunk-wise block runs the SwiGLU backward in the dh GEMM epilogue (measured -0.7%: off)
   int debug_nblk = 1;     // N blocks per tile of mst_debug_gemm
   // mst_block_step_host: copy stream and chunk events (created on first use)
@@ -912,11 +918,22 @@ int build_plain(mst_ctx* c, Launch& L, const Operand& a, const Operand& b, void*
 // added to one grouped launch (Alg. 3 lines 5-7).
 // parts: bit 1 K9, bit 2 K8, bit 4 K10 restricted to the dW rows [k10_r0, k10_r1)
 // of H (row slabs of the final chunk, mst_ctx_set_grad_slab_hook).
-enum { kGradK9 = 1, kGradK8 = 2, kGradK10 = 4, kGradAll = 7 };
+enum { kGradK9 = 1, kGradK8 = 2, kGradK10 = 4, kGradAll = 7, kGradDW = 6 };
+// A second chunk's dW operands (chunk-wise block, tuning "pair_dw"): K8 and
+// K10 then run over both chunks as one accumulation (two phases, K = the two
+// chunk lengths) and read-modify-write the fp32 gradients once per pair.
+struct DwChunk {
+  const void* dg;
+  const void* du;
+  const void* ht;
+  const void* xt;
+  const void* doj;
+  int64_t rows;
+};
 int add_mlp_grads(mst_ctx* c, Launch& L, const void* dg, const void* du, const void* ht, const void* xt,
                   const void* doj, const void* wg, const void* wu, void* dxj, float* dwg, float* dwu, float* dwd,
                   int64_t rows, int64_t h, int64_t i, int64_t ldt, int beta, int parts = kGradAll,
-                  int64_t k10_r0 = 0, int64_t k10_r1 = -1) {
+                  int64_t k10_r0 = 0, int64_t k10_r1 = -1, const DwChunk* second = nullptr) {
   if (k10_r1 < 0) k10_r1 = h;
   if (parts & kGradK9) {  // K9: one accumulator over both phases (B K-major)
     ProblemDesc& P = L.p.prob[L.p.num_problems++];
@@ -950,9 +967,23 @@ int add_mlp_grads(mst_ctx* c, Launch& L, const void* dg, const void* du, const v
   }
   if (parts & kGradK9) cnt_op(c, (uint64_t)(rows * h), 3ull * rows * h);  // dX' + dX'' (fused: one K = 2I accumulation)
   // K8: dW_d[I,H] += h^T dO_j (A = h^T, K-major)
-  if (parts & kGradK8)
+  if (parts & kGradK8) {
     MST_TRY(build_plain(c, L, Operand{ht, i, rows, ldt, false}, Operand{doj, h, rows, h, true}, dwd, h,
                         mst::kEpiAccF32, beta));
+    if (second) {  // + h'^T dO' of the second chunk, same accumulator
+      ProblemDesc& P = L.p.prob[L.p.num_problems - 1];
+      PhaseSpec s{};
+      s.a = {second->ht, i, second->rows, ldt, false};
+      s.b0 = {second->doj, h, second->rows, h, true};
+      s.b1 = s.b0;
+      s.umma_n = 256;
+      s.b_off1 = 128;
+      s.acc_continue = true;
+      MST_TRY(add_phase(c, L, P, s));
+      L.flops += 2.0 * i * h * second->rows;
+      cnt_mm(c, i, second->rows, h, 0);
+    }
+  }
   if ((parts & kGradK10) && k10_r1 > k10_r0) {  // K10: [dW_g | dW_u][H, I] += X_j^T [dG | dU]  (A = X_j^T, K-major)
     const int64_t hs = k10_r1 - k10_r0;
     xt = bptr(xt, k10_r0 * ldt);
@@ -965,6 +996,17 @@ int add_mlp_grads(mst_ctx* c, Launch& L, const void* dg, const void* du, const v
     q.b1 = {du, i, rows, i, true};
     q.umma_n = 256;
     MST_TRY(add_phase(c, L, P, q));
+    if (second) {  // + X'^T [dG' | dU'] of the second chunk
+      PhaseSpec q2 = q;
+      q2.a = {bptr(second->xt, k10_r0 * ldt), hs, second->rows, ldt, false};
+      q2.b0 = {second->dg, i, second->rows, i, true};
+      q2.b1 = {second->du, i, second->rows, i, true};
+      q2.acc_continue = true;
+      MST_TRY(add_phase(c, L, P, q2));
+      L.flops += 2.0 * hs * (2.0 * i) * second->rows;
+      cnt_mm(c, hs, second->rows, i, 0);
+      cnt_mm(c, hs, second->rows, i, 0);
+    }
     P.m_tiles = (int)cdiv(hs, 256);
     P.tile_n = 128;
     P.n_tiles = (int)cdiv(i, 128);
@@ -1128,6 +1170,10 @@ int mst_ctx_set_tuning(mst_ctx* c, const char* key, int value) {
     c->chunked_block = value != 0;
   } else if (std::strcmp(key, "wide") == 0) {
     c->wide = value != 0;
+  } else if (std::strcmp(key, "pair_dw") == 0) {
+    c->pair_dw = value != 0;
+  } else if (std::strcmp(key, "k9_in_k1") == 0) {
+    c->k9_in_k1 = value != 0;
   } else if (std::strcmp(key, "fuse_swiglu_bwd") == 0) {
     c->fuse_swiglu_bwd = value != 0;
   } else if (std::strcmp(key, "wide_mask") == 0) {
@@ -1328,8 +1374,13 @@ static size_t chunked_fixed_bytes(int64_t n, int64_t h, int64_t m) {
 
 // Chunk-wise block (M_mlp == M_head): MLP and head chunk buffers coexist,
 // plus the forward's fp32 G, U accumulators of one chunk.
-static size_t chunked_extra_bytes(int64_t n, int64_t i, int64_t m) {
-  return 2 * align_up(size_t(max_chunk(n, m)) * i * 4, 256) + 512;
+static size_t chunked_extra_bytes(int64_t n, int64_t h, int64_t i, int64_t m, bool pair) {
+  const size_t g = 2 * align_up(size_t(max_chunk(n, m)) * i * 4, 256) + 512;
+  if (!pair || std::min(n, m) < 2) return g;
+  // second dW operand set {dG, dU, h^T, X^T} (tuning "pair_dw")
+  const int64_t nc = max_chunk(n, m), ldt = (nc + 7) / 8 * 8;
+  return g + 2 * align_up(size_t(nc) * i * 2, 256) + align_up(size_t(i) * ldt * 2, 256) +
+         align_up(size_t(h) * ldt * 2, 256) + 256;
 }
 
 // The head plan refines the MLP plan: every MLP chunk boundary is also a
@@ -1354,7 +1405,7 @@ int mst_block_workspace(int64_t n, int64_t h, int64_t i, int64_t v, int64_t m_ml
   MST_TRY(mst_lmhead_workspace(n, h, v, m_head, &b));
   const size_t two_pass = block_fixed_bytes(n, h) + 256 + std::max(a, b);
   const size_t chunked = plans_nest(n, m_mlp, m_head)
-                             ? chunked_fixed_bytes(n, h, m_mlp) + 256 + a + b + chunked_extra_bytes(n, i, m_mlp)
+                             ? chunked_fixed_bytes(n, h, m_mlp) + 256 + a + b + chunked_extra_bytes(n, h, i, m_mlp, true)
                              : 0;
   *bytes = std::max(two_pass, chunked);
   return MST_OK;
@@ -1371,7 +1422,7 @@ int mst_ctx_block_workspace(const mst_ctx* c, int64_t n, int64_t h, int64_t i, i
   MST_TRY(mst_mlp_workspace(n, h, i, m_mlp, &a));
   MST_TRY(mst_lmhead_workspace(n, h, v, m_head, &b));
   *bytes = uses_chunked_block(c, n, m_mlp, m_head)
-               ? chunked_fixed_bytes(n, h, m_mlp) + 256 + a + b + chunked_extra_bytes(n, i, m_mlp)
+               ? chunked_fixed_bytes(n, h, m_mlp) + 256 + a + b + chunked_extra_bytes(n, h, i, m_mlp, c->pair_dw != 0)
                : block_fixed_bytes(n, h) + 256 + std::max(a, b);
   return MST_OK;
 }
@@ -1847,6 +1898,19 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
   const int64_t ldt = ld_t(n, m), ldt_h = ld_t(n, mh);
   const std::vector<int64_t> b = plan_bounds(n, m);
   const int nch = (int)b.size() - 1;
+  // dW operand sets {dG, dU, h^T, X^T}: chunk j uses set j & 1 when K8 / K10
+  // run per chunk pair (pair_dw), else set 0.
+  const bool pair = c->pair_dw != 0 && nch > 1;
+  const bool k9k1 = c->k9_in_k1 != 0;
+  void *dgS[2] = {dg, dg}, *duS[2] = {du, du}, *htS[2] = {ht, ht}, *xtS[2] = {xt, xt};
+  if (pair) {
+    const int64_t nc = max_chunk(n, m);
+    dgS[1] = cv.take(size_t(nc) * i * 2);
+    duS[1] = cv.take(size_t(nc) * i * 2);
+    htS[1] = cv.take(size_t(i) * ldt * 2);
+    xtS[1] = cv.take(size_t(h) * ldt * 2);
+  }
+  auto set_of = [&](int j) { return pair ? (j & 1) : 0; };
   // Head plan: refines the MLP plan (plans_nest), head chunks hc0[j] ..
   // hc0[j+1]-1 lie inside MLP chunk j.
   const std::vector<int64_t> bh = plan_bounds(n, mh);
@@ -1941,14 +2005,33 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
     L.flops += 2.0 * rows * (2.0 * i) * h;
     return MST_OK;
   };
-  auto add_grads = [&](Launch& L, int j, int parts = kGradAll, int64_t k10_r0 = 0, int64_t k10_r1 = -1) -> int {
-    const int64_t rows = rows_of(j);
-    if (j == 0 && (parts & kGradK9))
-      for (int wi = 0; wi < 3; ++wi) grad_alloc(c, wi, (uint64_t)h * i * 4);
+  bool mlp_grads_alloced = false;
+  auto alloc_mlp_grads = [&]() {
+    if (mlp_grads_alloced) return;
+    mlp_grads_alloced = true;
+    for (int wi = 0; wi < 3; ++wi) grad_alloc(c, wi, (uint64_t)h * i * 4);
+  };
+  // K9 (dX_j) of chunk j
+  auto add_k9 = [&](Launch& L, int j) -> int {
+    alloc_mlp_grads();
+    const int s = set_of(j);
+    if (io) MST_CUDA(cudaStreamWaitEvent(st, io->dx_free[j & 1], 0));  // dX of chunk j-2 out
+    return add_mlp_grads(c, L, dgS[s], duS[s], htS[s], xtS[s], dO[j & 1], wg, wu, dxdev(j), dwg, dwu, dwd,
+                         rows_of(j), h, i, ldt, 0, kGradK9);
+  };
+  // K8 / K10 of chunk j, or of chunks j and j + 1 as one accumulation
+  auto add_dw = [&](Launch& L, int j, bool paired, int parts = kGradDW, int64_t k10_r0 = 0,
+                    int64_t k10_r1 = -1) -> int {
+    alloc_mlp_grads();
+    const int s = set_of(j);
     const int beta = (j > 0 || accumulate) ? 1 : 0;
-    if (io && (parts & kGradK9)) MST_CUDA(cudaStreamWaitEvent(st, io->dx_free[j & 1], 0));  // dX of chunk j-2 out
-    return add_mlp_grads(c, L, dg, du, ht, xt, dO[j & 1], wg, wu, dxdev(j),
-                         dwg, dwu, dwd, rows, h, i, ldt, beta, parts, k10_r0, k10_r1);
+    DwChunk second{};
+    if (paired) {
+      const int s2 = set_of(j + 1);
+      second = DwChunk{dgS[s2], duS[s2], htS[s2], xtS[s2], dO[(j + 1) & 1], rows_of(j + 1)};
+    }
+    return add_mlp_grads(c, L, dgS[s], duS[s], htS[s], xtS[s], dO[j & 1], wg, wu, nullptr, dwg, dwu, dwd,
+                         rows_of(j), h, i, ldt, beta, parts, k10_r0, k10_r1, paired ? &second : nullptr);
   };
   {
     Launch L;
@@ -1959,14 +2042,26 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
     const int64_t r0 = b[j], rows = rows_of(j);
     void* oj = o;
     void* doj = dO[j & 1];
-    {  // K2(j) + the weight/input gradients of chunk j-1
+    {  // K2(j) + the weight/input gradients of chunk j-1 (or of chunks j-2, j-1)
       Launch L;
       MST_TRY(build_plain(c, L, Operand{hb, rows, i, i, false}, Operand{wd, h, i, h, true}, oj, h, mst::kEpiStoreBf16,
                           0, (c->wide_mask & 4) ? 2 : 1));
-      if (j > 0) MST_TRY(add_grads(L, j - 1));
+      int freed0 = -1, freed1 = -1;
+      if (j > 0) {
+        if (!k9k1) MST_TRY(add_k9(L, j - 1));
+        if (!pair) {
+          MST_TRY(add_dw(L, j - 1, false));
+          freed0 = j - 1;
+        } else if ((j - 1) & 1) {  // chunk j-1 closes the pair (j-2, j-1)
+          MST_TRY(add_dw(L, j - 2, true));
+          freed0 = j - 2;
+          freed1 = j - 1;
+        }
+      }
       MST_TRY(launch(c, st, L));
-      if (j > 0) grads_live(j - 1, false);
-      if (io && j > 0) MST_TRY(d2h(j - 1));
+      if (freed0 >= 0) grads_live(freed0, false);
+      if (freed1 >= 0) grads_live(freed1, false);
+      if (io && j > 0 && !k9k1) MST_TRY(d2h(j - 1));
     }
     if (j == 0) grad_alloc(c, 3, (uint64_t)h * v * 4);
     for (int k = hc0[j]; k < hc0[j + 1]; ++k) {  // the head chunks of MLP chunk j
@@ -2025,14 +2120,14 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
       // TMEM; dG, dU come out directly (no dh round trip through HBM).
       grads_live(j, true);
       Launch L;
-      MST_TRY(build_plain(c, L, Operand{doj, rows, h, h, false}, Operand{wd, i, h, h, false}, dg, i,
+      MST_TRY(build_plain(c, L, Operand{doj, rows, h, h, false}, Operand{wd, i, h, h, false}, dgS[set_of(j)], i,
                           mst::kEpiStoreBf16, 0, (c->wide_mask & 16) ? 2 : 1));
       ProblemDesc& P = L.p.prob[0];
       P.epi = mst::kEpiDhSwigluBwd;
       P.aux = g32;
       P.aux2 = u32;
       P.ld_aux = i;
-      MST_TRY(add_out_map(c, L, du, i, rows, i, false, &P.map_out1));
+      MST_TRY(add_out_map(c, L, duS[set_of(j)], i, rows, i, false, &P.map_out1));
       MST_TRY(launch(c, st, L));
       cnt_op(c, 4ull * rows * i, 3ull * rows * i);  // silu_backward (fused epilogue)
       cnt_op(c, 2ull * rows * i, 6ull * rows * i);  // dG, dU products
@@ -2046,8 +2141,8 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
       }
       {  // SwiGLU backward from the saved accumulators
         const int64_t n4 = rows * i / 4;
-        swiglu_bwd_kernel<<<(unsigned)cdiv(n4, 256), 256, 0, st>>>(g32, u32, dhb, static_cast<uint16_t*>(dg),
-                                                                   static_cast<uint16_t*>(du), n4);
+        swiglu_bwd_kernel<<<(unsigned)cdiv(n4, 256), 256, 0, st>>>(
+            g32, u32, dhb, static_cast<uint16_t*>(dgS[set_of(j)]), static_cast<uint16_t*>(duS[set_of(j)]), n4);
         c->launches += 1;
         cnt_op(c, 4ull * rows * i, 3ull * rows * i);  // silu_backward
         cnt_op(c, 2ull * rows * i, 6ull * rows * i);  // dG, dU products
@@ -2055,26 +2150,32 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
       grads_live(j, true);
       mem_free(c, (uint64_t)rows * i * 4, "inter.mlp.dh");
     }
-    MST_TRY(transpose_bf16(c, st, hb, i, ht, ldt, rows, i));
-    MST_TRY(transpose_bf16(c, st, xdev(j), h, xt, ldt, rows, h));
+    MST_TRY(transpose_bf16(c, st, hb, i, htS[set_of(j)], ldt, rows, i));
+    MST_TRY(transpose_bf16(c, st, xdev(j), h, xtS[set_of(j)], ldt, rows, h));
     if (io) {  // last read of X_j: its buffer takes X_{j+2}
       MST_CUDA(cudaEventRecord(io->x_free[j & 1], st));
       if (j + 2 < nch) MST_TRY(h2d(j + 2));
     }
     mlp_fwd_live(j, false);
-    if (j + 1 < nch) {
+    if (j + 1 < nch) {  // K1(j+1) (+ K9(j))
       Launch L;
       MST_TRY(add_k1s(L, j + 1));
+      if (k9k1) MST_TRY(add_k9(L, j));
       MST_TRY(launch(c, st, L));
+      if (io && k9k1) MST_TRY(d2h(j));
     }
   }
   {  // the last chunk's K9 / K8 / K10 finalise dX and dW_{down,gate,up}; with a
      // slab hook K10 is cut into row slabs of H (K9 and K8 ride in the first)
     const int64_t per = (c->slab_fn && c->slabs > 1) ? cdiv(cdiv(h, 256), c->slabs) * 256 : h;
+    const int last = nch - 1;
+    const bool last_paired = pair && (last & 1);  // the pair (last-1, last)
+    const int dw0 = last_paired ? last - 1 : last;
     for (int64_t s0 = 0; s0 < h; s0 += per) {
       const int64_t s1 = std::min(h, s0 + per);
       Launch L;
-      MST_TRY(add_grads(L, nch - 1, s0 == 0 ? kGradAll : kGradK10, s0, s1));
+      if (s0 == 0) MST_TRY(add_k9(L, last));
+      MST_TRY(add_dw(L, dw0, last_paired, s0 == 0 ? kGradDW : kGradK10, s0, s1));
       MST_TRY(launch(c, st, L));
       if (s0 == 0) {
         grad_slab(c, 2, 0, i, st);
@@ -2083,7 +2184,8 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
       grad_slab(c, 0, s0, s1, st);
       grad_slab(c, 1, s0, s1, st);
     }
-    grads_live(nch - 1, false);
+    if (last_paired) grads_live(last - 1, false);
+    grads_live(last, false);
     if (io) {  // the compute stream joins the copies
       MST_CUDA(cudaEventRecord(io->done, io->cs));
       MST_CUDA(cudaStreamWaitEvent(st, io->done, 0));

@@ -51,24 +51,97 @@ def _chunk(N: int, M: int) -> int:
     return -(-N // c)  # the longest chunk of the balanced plan (App. A-1)
 
 
-def predict_block_peak(N: int, H: int, I: int, V: int, M: int, M_head: int | None = None) -> Dict[str, int]:
+def _bounds(N: int, M: int):
+    """Balanced chunk plan (make_chunk_plan): min(N, M)
+    chunks, the first N mod M one row longer."""
+    c = min(N, M)
+    q, r = divmod(N, c)
+    b = [0]
+    for j in range(c):
+        b.append(b[-1] + q + (1 if j < r else 0))
+    return b
+
+
+def predict_block_peak(N: int, H: int, I: int, V: int, M: int, M_head: int | None = None,
+                       pair_dw: bool = True) -> Dict[str, int]:
     """Peak live bytes per label class of one chunk-wise block step
     (mst_block_step; M_mlp = M, M_head = M unless given, head chunks nested in
-    the MLP chunks), as the library's memtrack events report them: the MLP
-    chunk buffers h (bf16), G and U (fp32, kept for the backward), dh (fp32),
-    dG, dU, h^T (bf16) -> 20 n I bytes at their common peak; one LM-Head
-    chunk's softmax numerators / dlogits (bf16) plus the per-256-column CE
-    partials and two fp32 row scalars; the activations: one O chunk and two
-    dO chunks of the MLP chunk length (bf16; dO_j is read by chunk j+1's
-    dW_down GEMM) and the sequence-wide lse (fp32)."""
+    the MLP chunks), as the library's memtrack events report them.  The
+    events are replayed in the library's order (block_step_chunked in
+    csrc/mst_api.cu), so ragged plans are exact too:
+
+      K1(j)        + inter.mlp.{h (bf16), G, U (fp32)} of chunk j
+      K2(j) launch - the dW operand sets whose K8 / K10 ran in it
+      head chunk k + act.oT, inter.head.{partials, dlogits}, then - all three
+      K7a(j)       + inter.mlp.dh (fp32); SwiGLU backward + inter.mlp.{dG, dU,
+                   hT} and act.xT (the dW operand set of chunk j); - dh
+      end of j     - h, G, U of chunk j; K1(j+1) + those of chunk j+1
+      last launch  - the remaining dW operand sets
+
+    With `pair_dw` (the library default, tuning "pair_dw") K8 / K10 run once
+    per chunk pair, so the set of an even chunk stays live through the next
+    chunk's head and MLP backward.  Fixed for the step: act.O (one MLP
+    chunk), act.dO (two), act.lse (sequence-wide, fp32)."""
+    MH = M if M_head is None else M_head
+    b, bh = _bounds(N, M), _bounds(N, MH)
+    nch = len(b) - 1
+    nparts = -(-V // 256)
     n = _chunk(N, M)
-    nh = _chunk(N, M if M_head is None else M_head)
-    head = nh * V * 2 + nh * (-(-V // 256)) * 8 + nh * 8
-    mlp = 20 * n * I
-    # the head's chunk buffers coexist with the forward MLP buffers of the same chunk (h, G, U = 10 n I)
-    inter = max(mlp, 10 * n * I + head)
-    return {"inter.mlp.": mlp, "inter.head.": head, "inter.": inter, "act.O": n * H * 2, "act.dO": 2 * n * H * 2,
-            "act.lse": N * 4}
+    live: Dict[str, int] = {}
+    peaks: Dict[str, int] = {}
+    prefixes = ("inter.mlp.", "inter.head.", "inter.", "act.O", "act.dO", "act.lse", "act.xT", "act.oT")
+
+    def ev(label: str, nbytes: int):
+        live[label] = live.get(label, 0) + nbytes
+        for p in prefixes:
+            if label.startswith(p):
+                peaks[p] = max(peaks.get(p, 0), sum(v for k, v in live.items() if k.startswith(p)))
+
+    def rows(j):
+        return b[j + 1] - b[j]
+
+    def mlp_fwd(j, on):
+        s = 1 if on else -1
+        for lab, eb in (("inter.mlp.h", 2), ("inter.mlp.G", 4), ("inter.mlp.U", 4)):
+            ev(lab, s * rows(j) * I * eb)
+
+    def grads(j, on):
+        s = 1 if on else -1
+        for lab in ("inter.mlp.dG", "inter.mlp.dU", "inter.mlp.hT"):
+            ev(lab, s * rows(j) * I * 2)
+        ev("act.xT", s * rows(j) * H * 2)
+
+    pair = pair_dw and nch > 1
+    ev("act.O", n * H * 2)
+    ev("act.dO", 2 * n * H * 2)
+    ev("act.lse", N * 4)
+    mlp_fwd(0, True)
+    for j in range(nch):
+        if j > 0:  # K2(j) launch: K8 / K10 of chunk j-1, or of the pair (j-2, j-1)
+            if not pair:
+                grads(j - 1, False)
+            elif (j - 1) & 1:
+                grads(j - 2, False)
+                grads(j - 1, False)
+        for k in range(len(bh) - 1):
+            if not (b[j] <= bh[k] < b[j + 1]):
+                continue
+            hr = bh[k + 1] - bh[k]
+            ev("act.oT", hr * H * 2)
+            ev("inter.head.partials", hr * nparts * 8 + hr * 8)
+            ev("inter.head.dlogits", hr * V * 2)
+            ev("inter.head.dlogits", -hr * V * 2)
+            ev("inter.head.partials", -(hr * nparts * 8 + hr * 8))
+            ev("act.oT", -hr * H * 2)
+        ev("inter.mlp.dh", rows(j) * I * 4)
+        grads(j, True)
+        ev("inter.mlp.dh", -rows(j) * I * 4)
+        mlp_fwd(j, False)
+        if j + 1 < nch:
+            mlp_fwd(j + 1, True)
+    return {"inter.mlp.": peaks["inter.mlp."], "inter.head.": peaks["inter.head."], "inter.": peaks["inter."],
+            "act.O": peaks["act.O"], "act.dO": peaks["act.dO"], "act.lse": peaks["act.lse"],
+            "act.xT": peaks["act.xT"]}
 
 
 # ------------------------------------------------------------------ predict_peak

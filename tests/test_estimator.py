@@ -48,9 +48,30 @@ def test_predict_flops_matches_oracle_counters(orc):
 
 
 def test_block_peak_scales_as_one_over_m():
-    p1, p8 = E.predict_block_peak(8192, 4096, 14336, 128256, 1), E.predict_block_peak(8192, 4096, 14336, 128256, 8)
+    """Per-chunk dW accumulation (pair_dw off): every chunk buffer is 1/M of
+    its M=1 size, so the peak is exactly 1/M of the M=1 peak."""
+    p1 = E.predict_block_peak(8192, 4096, 14336, 128256, 1, pair_dw=False)
+    p8 = E.predict_block_peak(8192, 4096, 14336, 128256, 8, pair_dw=False)
     assert p1["inter.head."] == 8 * p8["inter.head."] and p1["inter."] == 8 * p8["inter."]
     assert np.isclose(p8["inter.head."] / 1e6, 266.8, atol=0.1)  # dlogits [S/M, V] bf16 + CE partials at config 2
+
+
+def test_block_peak_paired_dw():
+    """pair_dw (library default): the dG / dU / h^T set of an even chunk stays
+    live through the next chunk's head, +6 n I bytes on the head phase; M=1
+    has nothing to pair."""
+    N, H, I, V = 8192, 4096, 14336, 128256
+    assert E.predict_block_peak(N, H, I, V, 1) == E.predict_block_peak(N, H, I, V, 1, pair_dw=False)
+    for M in (2, 4, 8, 16):
+        n = N // M
+        a, b = E.predict_block_peak(N, H, I, V, M), E.predict_block_peak(N, H, I, V, M, pair_dw=False)
+        assert a["inter.head."] == b["inter.head."]
+        assert a["inter."] == max(26 * n * I, 16 * n * I + a["inter.head."])
+        assert a["inter.mlp."] == 26 * n * I and b["inter.mlp."] == 20 * n * I
+        assert a["act.xT"] == 2 * b["act.xT"]
+    # ragged plans replay the same events: chunk 0 is one row longer
+    a = E.predict_block_peak(1001, 64, 96, 512, 4)
+    assert a["inter.mlp."] == (10 + 4 + 6) * 250 * 96 + 6 * 251 * 96  # at chunk 1: its h, G, U, dh, set + set 0
 
 
 def test_predict_peak_appendix_d_rows():

@@ -62,10 +62,11 @@ def test_mlp_counters_match_oracle(M):
     assert bwd.as_tuple() == (ref["flops"], ref["matmul_flops"], ref["hbm_elements"], ref["weight_read_elements"])
 
 
-def _block_counts(M, tracker=None):
+def _block_counts(M, tracker=None, pair_dw=1):
     _, g, L = _inputs()
     ctx = _ctx()
     ctx.attach_tracker(tracker)
+    ctx.set_tuning("pair_dw", pair_dw)
     try:
         if tracker is not None:
             tracker.region_begin("block")
@@ -77,6 +78,7 @@ def _block_counts(M, tracker=None):
         region = tracker.region_end("block") if tracker is not None else None
     finally:
         ctx.attach_tracker(None)
+        ctx.set_tuning("pair_dw", 1)
     return ctx.counters(), region
 
 
@@ -97,10 +99,14 @@ def test_block_weight_reads_linear_in_M_thm32():
 
 
 def test_tracked_peak_intermediate_scales_as_one_over_M():
+    """With per-chunk dW accumulation (pair_dw off) every chunk buffer is 1/M
+    of its M=1 size; the default pairs the dW GEMMs of two chunks and keeps
+    one extra dG / dU / h^T set (checked exactly against the estimator in
+    test_estimator_block_peak_matches_tracked_device_allocations)."""
     peaks = {}
     for M in (1, 8):
         t = mt.MemTracker()
-        _, reg = _block_counts(M, t)
+        _, reg = _block_counts(M, t, pair_dw=0)
         assert t.live_bytes() == 0 and reg.report.final_live() == 0  # every chunk buffer freed
         n = N // M
         head = reg.report.peak_for_prefix("inter.head.")
@@ -148,8 +154,9 @@ def test_estimator_block_peak_matches_tracked_device_allocations(M):
     here rather than within 10%)."""
     from paper_2407_15892_b200 import estimator
 
-    t = mt.MemTracker()
-    _, reg = _block_counts(M, t)
-    pred = estimator.predict_block_peak(N, H, I, V, M)
-    for prefix, b in pred.items():
-        assert reg.report.peak_for_prefix(prefix) == b, (prefix, reg.report.peak_for_prefix(prefix), b)
+    for pair in (1, 0):
+        t = mt.MemTracker()
+        _, reg = _block_counts(M, t, pair_dw=pair)
+        pred = estimator.predict_block_peak(N, H, I, V, M, pair_dw=bool(pair))
+        for prefix, b in pred.items():
+            assert reg.report.peak_for_prefix(prefix) == b, (pair, prefix, reg.report.peak_for_prefix(prefix), b)

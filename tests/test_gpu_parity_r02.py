@@ -384,3 +384,44 @@ def test_deferred_device_errors_surface_without_check():
     # sequence-parallel shard: no local valid label, global count 10 -> no error
     st, _ = ms.block_step(X, ignored, mlp, head, 2, 2, global_valid=torch.tensor([10.0], device="cuda"))
     ctx.check()
+
+
+# ----------------------------------------------------------------- paired dW GEMMs
+@pytest.mark.parametrize("shape", [(1024, 256, 688, 4096, 4), (1001, 128, 264, 1000, 5), (777, 64, 136, 520, 3),
+                                   (600, 64, 128, 512, 2)])
+def test_paired_dw_matches_per_chunk(shape):
+    """pair_dw (default): K8 / K10 of chunks (2k, 2k+1) run as one K = 2n
+    accumulation.  Against per-chunk accumulation (pair_dw=0): the loss and
+    dX are bitwise equal (K9 is unchanged), the weight gradients agree to
+    fp32 rounding (only the fp32 addition order of the chunk contributions
+    differs).  Covers ragged plans, an odd chunk count (the last chunk is
+    accumulated alone), two chunks (one pair) and K9 riding in K1's launch."""
+    N, H, I, V, M = shape
+    torch.manual_seed(11)
+    X = torch.randn(N, H, device="cuda").bfloat16()
+    W = [(0.05 * torch.randn(*s, device="cuda")).bfloat16() for s in ((H, I), (H, I), (I, H), (H, V))]
+    L = torch.randint(0, V, (N,), device="cuda", dtype=torch.int32)
+    L[::7] = -100
+    mlp, head = ms.MlpWeights(*W[:3]), ms.LmHeadWeights(W[3])
+    ctx = ms.Context.get(0)
+    out = {}
+    try:
+        for key, (pair, k9k1) in {"per_chunk": (0, 0), "pair": (1, 0), "pair_k9k1": (1, 1), "k9k1": (0, 1)}.items():
+            ctx.set_tuning("pair_dw", pair)
+            ctx.set_tuning("k9_in_k1", k9k1)
+            st, gr = ms.block_step(X, L, mlp, head, M, M)
+            torch.cuda.synchronize()
+            out[key] = (float(st[2]), gr.dX.clone(), gr.W_gate.clone(), gr.W_up.clone(), gr.W_down.clone(),
+                        gr.W_out.clone())
+    finally:
+        ctx.set_tuning("pair_dw", 1)
+        ctx.set_tuning("k9_in_k1", 0)
+    ref = out["per_chunk"]
+    for key in ("pair", "pair_k9k1", "k9k1"):
+        o = out[key]
+        assert o[0] == ref[0]
+        assert torch.equal(o[1], ref[1]), key
+        assert torch.equal(o[5], ref[5]), key  # dW_out: untouched by the MLP schedule
+        for a, b in zip(o[2:5], ref[2:5]):
+            e = rel(a, b.double().cpu().numpy())
+            assert e <= (0 if key == "k9k1" else 1e-5), (key, e)
