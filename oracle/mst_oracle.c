@@ -377,14 +377,70 @@ static void head_fwd_rows(const double* X, const int32_t* L, const double* Wout,
 
 /* Per-chunk backward: dl = (exp(z - lse) - onehot) * scale.
  * round == 2 additionally replays the GPU single-pass head's rounding
- * (mst_lmhead_fused / block_step): the softmax numerator
+ * (tuning dl_rowscale=0): the softmax numerator
  * exp(z - m_tile) relative to its 256-column vocabulary tile's maximum is
- * stored in bf16 first; the label column is computed from the fp32 logit. */
+ * stored in bf16 first; the label column is computed from the fp32 logit.
+ * round == 3 replays the row-scaled head (the GPU default): numerators
+ * 2^(z log2e - R) stored in bf16 with R = 0 while every tile maximum lies
+ * within +-64 (log2 units; else the tile maximum, then rescaled to the row
+ * reference R*), label column (p_label - 1) 2^(lse2 - R*), per-row factor
+ * f = scale 2^(R* - lse2); dX = bf16(f * (e' W_out^T)), dW_out += bf16(f X)^T e'. */
+#define ORC_CE_REF_WINDOW 64.0
+static void head_bwd_rows_rowscale(const double* X, const int32_t* L, const double* Wout, int64_t n, int64_t H,
+                                   int64_t V, const double* lse, double scale, double* dX, double* cWout, double* Z) {
+  const double log2e = 1.4426950408889634;
+  double* f = (double*)malloc(sizeof(double) * (size_t)n);
+  double* Xs = (double*)malloc(sizeof(double) * (size_t)(n * H));
+  for (int64_t r = 0; r < n; ++r) {
+    double* z = Z + r * V;
+    const int32_t lab = L[r];
+    const int valid = lab >= 0 && lab < V;
+    const double zlab = valid ? z[lab] : 0.0;
+    const double l2 = lse[r] * log2e;
+    int special = 0;
+    for (int64_t t0 = 0; t0 < V; t0 += 256) {
+      const int64_t t1 = t0 + 256 < V ? t0 + 256 : V;
+      double mt = -INFINITY;
+      for (int64_t v = t0; v < t1; ++v) mt = z[v] * log2e > mt ? z[v] * log2e : mt;
+      if (fabs(mt) > ORC_CE_REF_WINDOW) special = 1;
+    }
+    const double rs = (!special || fabs(l2) <= ORC_CE_REF_WINDOW) ? 0.0 : rint(l2);
+    for (int64_t t0 = 0; t0 < V; t0 += 256) {
+      const int64_t t1 = t0 + 256 < V ? t0 + 256 : V;
+      double mt = -INFINITY;
+      for (int64_t v = t0; v < t1; ++v) mt = z[v] * log2e > mt ? z[v] * log2e : mt;
+      const double ref = fabs(mt) <= ORC_CE_REF_WINDOW ? 0.0 : mt;
+      for (int64_t v = t0; v < t1; ++v) {
+        double e = rb(exp2(z[v] * log2e - ref), 1);
+        if (ref != rs) e = rb(e * exp2(ref - rs), 1);
+        z[v] = e;
+      }
+    }
+    if (valid) z[lab] = rb((exp(zlab - lse[r]) - 1.0) * exp2(l2 - rs), 1);
+    f[r] = valid ? scale * exp2(rs - l2) : 0.0;
+    for (int64_t k = 0; k < H; ++k) Xs[r * H + k] = rb(X[r * H + k] * f[r], 1);
+  }
+  count_op(5ull * n * V, (uint64_t)(2 * n * V + 2 * n));
+  matmul_nt(Z, Wout, dX, n, V, H); /* dX = f * (e' W_out^T) */
+  count_matmul(n, V, H, (uint64_t)(H * V));
+  for (int64_t r = 0; r < n; ++r)
+    for (int64_t k = 0; k < H; ++k) dX[r * H + k] = rb(dX[r * H + k] * f[r], 1);
+  matmul_tn(Xs, Z, cWout, H, n, V); /* dW_out = (f X)^T e' */
+  count_matmul(H, n, V, 0);
+  free(Xs);
+  free(f);
+}
+
 static void head_bwd_rows(const double* X, const int32_t* L, const double* Wout, int64_t n, int64_t H, int64_t V,
                           const double* lse, double scale, double* dX, double* cWout, int round) {
   double* Z = talloc(n * V, ORC_MEM_INTER_HEAD);
   orc_matmul_f64(X, Wout, Z, n, H, V);
   count_matmul(n, H, V, (uint64_t)(H * V));
+  if (round == 3) {
+    head_bwd_rows_rowscale(X, L, Wout, n, H, V, lse, scale, dX, cWout, Z);
+    tfree(Z, n * V, ORC_MEM_INTER_HEAD);
+    return;
+  }
   for (int64_t r = 0; r < n; ++r) {
     double* z = Z + r * V;
     const int32_t lab = L[r];

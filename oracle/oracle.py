@@ -299,10 +299,14 @@ def block(X, L, Wg, Wu, Wd, Wout, M_mlp, M_head, round_bf16=True, grad_loss=1.0,
     """MLP -> LM-Head block fwd+bwd in f64 (the GPU block_step's checker).
     With round_bf16 the intermediates libmst stores in bf16 are rounded here
     too; single_pass additionally replays the single-pass head's bf16
-    softmax numerators (block_step's default head)."""
+    rounding: True / "rowscale" the row-scaled head
+    (block_step's default: numerators relative to one reference per row,
+    per-row factor applied to dX and to the transposed head input),
+    "normalize" the per-tile numerators + normalize pass (dl_rowscale=0)."""
     O = miniseq_mlp_forward(X, Wg, Wu, Wd, M_mlp, round_bf16)
     loss, lse, _, _ = miniseq_lmhead_forward(O, L, Wout, M_head)
-    rnd = (2 if single_pass else 1) if round_bf16 else 0
+    sp = {False: 1, True: 3, "rowscale": 3, "normalize": 2}[single_pass]
+    rnd = sp if round_bf16 else 0
     dO, dWout = miniseq_lmhead_backward(O, L, Wout, M_head, 0, grad_loss, rnd)
     dX, dWg, dWu, dWd = miniseq_mlp_backward(dO, X, Wg, Wu, Wd, M_mlp, round_bf16)
     return dict(O=O, loss=loss, lse=lse, dO=dO, dWout=dWout, dX=dX, dWg=dWg, dWu=dWu, dWd=dWd)

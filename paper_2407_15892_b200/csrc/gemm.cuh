@@ -79,6 +79,11 @@ constexpr int kEpiBytes = kNumEpiWarps * kEpiBufs * kEpiBufBytes;
 constexpr int kMaxProblems = 8;
 constexpr int kMaxMaps = 24;
 constexpr int kTmemCols = 512;
+// Row-scaled LM-Head (ce_ref0): a vocabulary tile whose maximum z*log2e lies
+// within +-kCeRefWindow stores its softmax numerators relative to 2^0, so all
+// tiles of a row share one reference and the softmax normalisation becomes a
+// per-row factor applied by the consumers.
+constexpr float kCeRefWindow = 64.0f;
 constexpr int kSmemBytes = kSlots * kSlotBytes + kEpiBytes + 1024 /*align*/ + 512 /*barriers, tile ring*/;
 
 enum EpiKind : int32_t {
@@ -119,7 +124,7 @@ struct ProblemDesc {
   int32_t col_off0, col_off1;
   int32_t nparts;      // kEpiCeFwd: partials per row
   int32_t map_out0, map_out1, map_out2;  // output tensor maps (TMA store boxes)
-  int32_t _pad;
+  int32_t ce_ref0;     // kEpiCeFwdNum: numerators relative to 2^0 unless |tile max| > kCeRefWindow (row-scaled head)
   int64_t ld_aux;
   const float* aux;    // kEpiSwigluBwd: dh [rows, ld_aux] fp32; kEpiDhSwigluBwd: G
   const float* aux2;   // kEpiDhSwigluBwd: U [rows, ld_aux] fp32
@@ -128,6 +133,7 @@ struct ProblemDesc {
   const float* scale;  // kEpiCeBwd: device scalar gradient scale
   float2* part;        // kEpiCeFwd: [rows, nparts] (max*log2e, sum 2^(z*log2e - max))
   float* ztarget;      // kEpiCeFwd: [rows] target logit
+  const float* rowscale;  // kEpiStoreBf16: per output row factor applied before the bf16 store (or null)
 };
 
 struct GemmParams {
@@ -432,6 +438,8 @@ __device__ __forceinline__ void run_epilogue(const GemmParams& p, const ProblemD
   switch (P.epi) {
     case kEpiStoreBf16: {
       const int half = P.ph[0].umma_n >> 1;
+      const bool scaled = P.rowscale != nullptr;
+      const float rs = (scaled && row_ok) ? P.rowscale[row] : 1.0f;
       for (int g = 0; g < 2; ++g) {
         const CUtensorMap* m = &p.maps[g ? P.map_out1 : P.map_out0];
         const int col0 = tn * P.tile_n + (g ? P.col_off1 : P.col_off0);
@@ -441,6 +449,10 @@ __device__ __forceinline__ void run_epilogue(const GemmParams& p, const ProblemD
           for (int s = 0; s < 2; ++s) {
             float v[32];
             epi::load32(taddr + g * half + c + 32 * s, v);
+            if (scaled) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] *= rs;
+            }
             st.put_bf16x32(b, s, v);
           }
           st.issue(b, m, col0 + c, row0, false);
@@ -651,8 +663,11 @@ __device__ __forceinline__ void run_epilogue(const GemmParams& p, const ProblemD
       // pass 1 finds m = max z*log2e over the tile, pass 2 writes the
       // unnormalised softmax numerator e = 2^(z*log2e - m) (bf16, in (0,1])
       // into the dlogits buffer and accumulates s = sum e (fp32).  Logits
-      // themselves are never stored; after the row LSE is known,
-      // normalize_dlogits turns e into (e 2^(m - lse2) - onehot) * scale.
+      // themselves are never stored.  Row-scaled head (ce_ref0): tiles
+      // whose maximum lies within +-kCeRefWindow use reference 2^0 instead of
+      // m, so dlogits = f_row * e' with one factor per row (applied by the K5
+      // epilogue and folded into K6's A operand, ce_combine_rowscale_kernel);
+      // otherwise normalize_dlogits turns e into (e 2^(m - lse2) - onehot) * scale.
       const int v0 = tn * 256;
       const int lab = row_ok ? P.labels[row] : -1;
       float m = -INFINITY, zt = 0.0f;
@@ -671,6 +686,9 @@ __device__ __forceinline__ void run_epilogue(const GemmParams& p, const ProblemD
         }
       }
       float s = 0.0f;
+      // Reference of this tile's numerators: its maximum, or 2^0 (row-scaled
+      // head) when the maximum lies within the window; the partial records it.
+      if (P.ce_ref0 && fabsf(m) <= kCeRefWindow) m = 0.0f;
       const CUtensorMap* mo = &p.maps[P.map_out0];
       for (int c = 0; c < 256; c += 64) {
         const int b = st.acquire();

@@ -127,6 +127,10 @@ struct mst_ctx {
   // (one fp32 dW read-modify-write per two chunks; a second dG / dU / h^T /
   // X^T chunk set stays live through the next chunk's head), and K9(j) in
   // K1(j+1)'s launch instead of K2(j+1)'s (tuning "pair_dw", "k9_in_k1").
+  // Row-scaled LM-Head (tuning "dl_rowscale"): numerators relative to one
+  // reference per row, the softmax normalisation applied as a per-row factor
+  // by K5's epilogue and K6's transposed operand, no normalize pass.
+  int dl_rowscale = 1;
   int pair_dw = 1;   // measured +1.6..1.9% at M = 4 / 8 / 16 (config 2)
   int k9_in_k1 = 0;  // measured -0.5%: off
   int fuse_swiglu_bwd = 0;  // 1: chunk-wise block runs the SwiGLU backward in the dh GEMM epilogue (measured -0.7%: off)
@@ -564,6 +568,77 @@ __global__ void ce_combine_kernel(const float2* __restrict__ part, int nparts, c
   }
 }
 
+// Row-scaled LM-Head (block_step / mst_lmhead_fused default):
+// the K3' epilogue stored each vocabulary tile's numerators relative to 2^0
+// (or, outside the +-kCeRefWindow window, to the tile maximum recorded in
+// part[].x).  Per row (one warp): the LSE and the row loss as in
+// ce_combine_kernel, then
+//   R* = 0, unless some tile used its own maximum and |lse2| is outside the
+//        window (then R* = rint(lse2)); tiles stored relative to another
+//        reference are rescaled to R* in place (never taken for logits
+//        within +-44 nats);
+//   the label column becomes e'_label = (p_label - 1) 2^(lse2 - R*) from the
+//        fp32 target logit (confident rows keep the precision of 1 - p_label);
+//   rowf[r] = scale 2^(R* - lse2) (0 for ignored rows),
+// so that dlogits[r, :] = rowf[r] * e'[r, :]: K5 applies rowf in its epilogue,
+// K6 reads (rowf * X)^T.  rowf overwrites ztarget (read first, same warp).
+__global__ void ce_combine_rowscale_kernel(const float2* __restrict__ part, int nparts, float* ztarget_rowf,
+                                           const int32_t* __restrict__ labels, int rows, int vocab,
+                                           float* __restrict__ lse, float* __restrict__ loss_row,
+                                           float* __restrict__ bad, uint16_t* __restrict__ e, int64_t ld,
+                                           const float* __restrict__ scale) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const float2* pr = part + static_cast<int64_t>(warp) * nparts;
+  float m = -INFINITY;
+  bool special = false;
+  for (int j = lane; j < nparts; j += 32) {
+    const float x = pr[j].x;
+    m = fmaxf(m, x);
+    special |= x != 0.0f;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffff, m, o));
+  special = __any_sync(0xffffffff, special);
+  float s = 0.f;
+  for (int j = lane; j < nparts; j += 32) s += pr[j].y * exp2f(pr[j].x - m);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffff, s, o);
+  const float l2 = m + log2f(s);
+  const float rs = (!special || fabsf(l2) <= mst::kCeRefWindow) ? 0.0f : rintf(l2);
+  uint16_t* er = e + static_cast<int64_t>(warp) * ld;
+  if (special) {  // rare: rescale the tiles stored relative to another reference
+    for (int j = 0; j < nparts; ++j) {
+      const float ref = pr[j].x;
+      if (ref == rs) continue;
+      const float f = exp2f(ref - rs);
+      const int c0 = j * 256, c1 = min(vocab, c0 + 256);
+      for (int c = c0 + lane; c < c1; c += 32) {
+        const float x = __bfloat162float(__ushort_as_bfloat16(er[c])) * f;
+        er[c] = __bfloat16_as_ushort(__float2bfloat16_rn(x));
+      }
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    const float lse_r = l2 * 0.69314718055994531f;
+    lse[warp] = lse_r;
+    const int lab = labels[warp];
+    const bool valid = lab >= 0 && lab < vocab;
+    if (lab != -100 && !valid) atomicAdd(bad, 1.0f);
+    const float zt = ztarget_rowf[warp];
+    loss_row[warp] = valid ? lse_r - zt : 0.0f;
+    float f = 0.0f;
+    if (valid) {
+      const float p = exp2f((zt - lse_r) * 1.4426950408889634f);
+      er[lab] = __bfloat16_as_ushort(__float2bfloat16_rn((p - 1.0f) * exp2f(l2 - rs)));
+      f = *scale * exp2f(rs - l2);
+    }
+    ztarget_rowf[warp] = f;
+  }
+}
+
 // Per-chunk (loss_sum, valid) with a fixed-order block reduction
 // (deterministic; SPEC.md:90 bitwise reruns).
 __global__ void chunk_reduce_kernel(const float* __restrict__ loss_row, const int32_t* __restrict__ labels, int rows,
@@ -649,9 +724,15 @@ __global__ void grad_scale_kernel(const float* global_stats, const float* local_
 // ld_dst elements).  Feeds the dW GEMMs a K-major A operand (X^T, O^T, h^T):
 // MN-major A costs ~25% tensor throughput on sm_100a, a transpose of the
 // chunk costs ~0.1% of the step.  64x64 tiles, 16-byte global accesses.
+// Optional rowscale: source row r is multiplied by rowscale[r] (fp32, then
+// rounded to bf16) on the way: the row-scaled head's K6 operand (rowf * X)^T.
+__device__ __forceinline__ uint32_t scale_bf16x2(uint32_t w, float f) {
+  const float lo = __uint_as_float(w << 16) * f, hi = __uint_as_float(w & 0xffff0000u) * f;
+  return mst::ptx::pack_bf16(lo, hi);
+}
 __global__ void __launch_bounds__(256) transpose_bf16_kernel(const uint16_t* __restrict__ src, int64_t ld_src,
                                                               uint16_t* __restrict__ dst, int64_t ld_dst, int rows,
-                                                              int cols) {
+                                                              int cols, const float* __restrict__ rowscale) {
   __shared__ uint16_t tile[64][72];
   const int r0 = blockIdx.y * 64, c0 = blockIdx.x * 64;
   for (int i = threadIdx.x; i < 64 * 8; i += 256) {
@@ -659,13 +740,19 @@ __global__ void __launch_bounds__(256) transpose_bf16_kernel(const uint16_t* __r
     const int gr = r0 + r, gc = c0 + cc;
     if (gr < rows) {
       const uint16_t* p = src + static_cast<int64_t>(gr) * ld_src + gc;
+      const float f = rowscale ? rowscale[gr] : 1.0f;
       if (gc + 8 <= cols) {
-        const uint4 v = *reinterpret_cast<const uint4*>(p);
+        uint4 v = *reinterpret_cast<const uint4*>(p);
+        if (rowscale) v = make_uint4(scale_bf16x2(v.x, f), scale_bf16x2(v.y, f), scale_bf16x2(v.z, f), scale_bf16x2(v.w, f));
         const uint16_t* e = reinterpret_cast<const uint16_t*>(&v);
 #pragma unroll
         for (int k = 0; k < 8; ++k) tile[r][cc + k] = e[k];
       } else {
-        for (int k = 0; k < 8; ++k) tile[r][cc + k] = gc + k < cols ? p[k] : 0;
+        for (int k = 0; k < 8; ++k) {
+          uint16_t x = gc + k < cols ? p[k] : 0;
+          if (rowscale) x = __bfloat16_as_ushort(__float2bfloat16_rn(__bfloat162float(__ushort_as_bfloat16(x)) * f));
+          tile[r][cc + k] = x;
+        }
       }
     }
   }
@@ -694,7 +781,7 @@ __global__ void __launch_bounds__(256) transpose_bf16_kernel(const uint16_t* __r
 // rounded up to 8), which the consumers' tensor maps never read.
 __global__ void __launch_bounds__(256) transpose8_bf16_kernel(const uint16_t* __restrict__ src, int64_t ld_src,
                                                                uint16_t* __restrict__ dst, int64_t ld_dst, int rows,
-                                                               int cols) {
+                                                               int cols, const float* __restrict__ rowscale) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r0 = blockIdx.y * 256 + warp * 32 + (lane >> 3) * 8;  // this thread's 8 source rows
   const int c0 = blockIdx.x * 64 + (lane & 7) * 8;                 // and 8 source columns
@@ -703,7 +790,13 @@ __global__ void __launch_bounds__(256) transpose8_bf16_kernel(const uint16_t* __
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     uint4 v = make_uint4(0, 0, 0, 0);
-    if (r0 + k < rows) v = __ldcs(reinterpret_cast<const uint4*>(src + static_cast<int64_t>(r0 + k) * ld_src + c0));
+    if (r0 + k < rows) {
+      v = __ldcs(reinterpret_cast<const uint4*>(src + static_cast<int64_t>(r0 + k) * ld_src + c0));
+      if (rowscale) {
+        const float f = rowscale[r0 + k];
+        v = make_uint4(scale_bf16x2(v.x, f), scale_bf16x2(v.y, f), scale_bf16x2(v.z, f), scale_bf16x2(v.w, f));
+      }
+    }
     in[k][0] = v.x, in[k][1] = v.y, in[k][2] = v.z, in[k][3] = v.w;
   }
 #pragma unroll
@@ -716,19 +809,19 @@ __global__ void __launch_bounds__(256) transpose8_bf16_kernel(const uint16_t* __
 }
 
 int transpose_bf16(mst_ctx* c, cudaStream_t st, const void* src, int64_t ld_src, void* dst, int64_t ld_dst,
-                   int64_t rows, int64_t cols) {
+                   int64_t rows, int64_t cols, const float* rowscale = nullptr) {
   if (cols % 8 == 0 && ld_dst % 8 == 0 && ld_dst >= (rows + 7) / 8 * 8 && ld_src % 8 == 0 &&
       (reinterpret_cast<uintptr_t>(src) & 15) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
     dim3 grid((unsigned)cdiv(cols, 64), (unsigned)cdiv(rows, 256));
     transpose8_bf16_kernel<<<grid, 256, 0, st>>>(static_cast<const uint16_t*>(src), ld_src,
-                                                  static_cast<uint16_t*>(dst), ld_dst, (int)rows, (int)cols);
+                                                  static_cast<uint16_t*>(dst), ld_dst, (int)rows, (int)cols, rowscale);
     c->launches++;
     MST_CUDA(cudaGetLastError());
     return MST_OK;
   }
   dim3 grid((unsigned)cdiv(cols, 64), (unsigned)cdiv(rows, 64));
   transpose_bf16_kernel<<<grid, 256, 0, st>>>(static_cast<const uint16_t*>(src), ld_src, static_cast<uint16_t*>(dst),
-                                               ld_dst, (int)rows, (int)cols);
+                                               ld_dst, (int)rows, (int)cols, rowscale);
   c->launches++;
   MST_CUDA(cudaGetLastError());
   return MST_OK;
@@ -1170,6 +1263,8 @@ int mst_ctx_set_tuning(mst_ctx* c, const char* key, int value) {
     c->chunked_block = value != 0;
   } else if (std::strcmp(key, "wide") == 0) {
     c->wide = value != 0;
+  } else if (std::strcmp(key, "dl_rowscale") == 0) {
+    c->dl_rowscale = value != 0;
   } else if (std::strcmp(key, "pair_dw") == 0) {
     c->pair_dw = value != 0;
   } else if (std::strcmp(key, "k9_in_k1") == 0) {
@@ -1741,7 +1836,8 @@ int mst_lmhead_fused(mst_ctx* c, void* stream, const void* x, const int32_t* lab
     mem_alloc(c, (uint64_t)rows * v * 2, "inter.head.dlogits");
     cnt_op(c, 5ull * rows * v, (uint64_t)(rows * v + 2 * rows));      // cross-entropy forward
     cnt_op(c, 5ull * rows * v, (uint64_t)(2 * rows * v + 2 * rows));  // cross-entropy backward
-    MST_TRY(transpose_bf16(c, st, xj, h, ot, ldt, rows, h));  // (head input)_j^T: K-major A of K6
+    const bool rs = c->dl_rowscale != 0;
+    if (!rs) MST_TRY(transpose_bf16(c, st, xj, h, ot, ldt, rows, h));  // (head input)_j^T: K-major A of K6
     {  // K3': logits GEMM; epilogue = online-softmax partials + softmax numerators (bf16)
       Launch L;
       MST_TRY(build_plain(c, L, Operand{xj, rows, h, h, false}, Operand{wout, v, h, v, true}, dl, v,
@@ -1751,20 +1847,33 @@ int mst_lmhead_fused(mst_ctx* c, void* stream, const void* x, const int32_t* lab
       P.part = part;
       P.ztarget = zt;
       P.nparts = nparts;
+      P.ce_ref0 = rs ? 1 : 0;
       MST_TRY(launch(c, st, L));
     }
     const int threads = 256;
-    ce_combine_kernel<<<(unsigned)cdiv(rows * 32, threads), threads, 0, st>>>(part, nparts, zt, labels + r0, (int)rows,
-                                                                               (int)v, lse + r0, lrow, stats + 3);
-    chunk_reduce_kernel<<<1, 1024, 0, st>>>(lrow, labels + r0, (int)rows, (int)v, stats + 4 + j,
-                                            stats + 4 + nch + j);
-    normalize_dlogits_kernel<<<(unsigned)cdiv(rows * (v / 8), 256), 256, 0, st>>>(
-        static_cast<uint16_t*>(dl), v, (int)rows, (int)v, part, nparts, lse + r0, labels + r0, scales + j, zt);
-    c->launches += 3;
+    if (rs) {  // row-scaled head: rowf (into zt) and the label column; K6 reads (rowf * X_j)^T
+      ce_combine_rowscale_kernel<<<(unsigned)cdiv(rows * 32, threads), threads, 0, st>>>(
+          part, nparts, zt, labels + r0, (int)rows, (int)v, lse + r0, lrow, stats + 3, static_cast<uint16_t*>(dl), v,
+          scales + j);
+      chunk_reduce_kernel<<<1, 1024, 0, st>>>(lrow, labels + r0, (int)rows, (int)v, stats + 4 + j,
+                                              stats + 4 + nch + j);
+      c->launches += 2;
+      MST_TRY(transpose_bf16(c, st, xj, h, ot, ldt, rows, h, zt));
+    } else {
+      ce_combine_kernel<<<(unsigned)cdiv(rows * 32, threads), threads, 0, st>>>(part, nparts, zt, labels + r0,
+                                                                                 (int)rows, (int)v, lse + r0, lrow,
+                                                                                 stats + 3);
+      chunk_reduce_kernel<<<1, 1024, 0, st>>>(lrow, labels + r0, (int)rows, (int)v, stats + 4 + j,
+                                              stats + 4 + nch + j);
+      normalize_dlogits_kernel<<<(unsigned)cdiv(rows * (v / 8), 256), 256, 0, st>>>(
+          static_cast<uint16_t*>(dl), v, (int)rows, (int)v, part, nparts, lse + r0, labels + r0, scales + j, zt);
+      c->launches += 3;
+    }
     {  // K5 (dX = dl W_out^T) + K6 (dW_out += X^T dl), grouped.
       Launch L;
       MST_TRY(build_plain(c, L, Operand{dl, rows, v, v, false}, Operand{wout, h, v, v, false},
                           const_cast<char*>(bptr(dx, r0 * h)), h, mst::kEpiStoreBf16, 0));
+      if (rs) L.p.prob[0].rowscale = zt;
       MST_TRY(build_plain(c, L, Operand{ot, h, rows, ldt, false}, Operand{dl, v, rows, v, true}, dwout, v,
                           mst::kEpiAccF32, beta));
       MST_TRY(launch(c, st, L));
@@ -2075,7 +2184,8 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
       mem_alloc(c, (uint64_t)hrows * v * 2, "inter.head.dlogits");
       cnt_op(c, 5ull * hrows * v, (uint64_t)(hrows * v + 2 * hrows));      // cross-entropy forward
       cnt_op(c, 5ull * hrows * v, (uint64_t)(2 * hrows * v + 2 * hrows));  // cross-entropy backward
-      MST_TRY(transpose_bf16(c, st, ok, h, ot, ldt_h, hrows, h));
+      const bool rs = c->dl_rowscale != 0;
+      if (!rs) MST_TRY(transpose_bf16(c, st, ok, h, ot, ldt_h, hrows, h));
       {  // K3': logits GEMM, partials + softmax numerators
         Launch L;
         MST_TRY(build_plain(c, L, Operand{ok, hrows, h, h, false}, Operand{wout, v, h, v, true}, dl, v,
@@ -2085,15 +2195,26 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
         P.part = part;
         P.ztarget = zt;
         P.nparts = nparts;
+        P.ce_ref0 = rs ? 1 : 0;
         MST_TRY(launch(c, st, L));
       }
-      ce_combine_kernel<<<(unsigned)cdiv(hrows * 32, 256), 256, 0, st>>>(part, nparts, zt, labels + hr0, (int)hrows,
-                                                                        (int)v, lse + hr0, lrow, stats + 3);
-      chunk_reduce_kernel<<<1, 1024, 0, st>>>(lrow, labels + hr0, (int)hrows, (int)v, stats + 4 + k,
-                                              stats + 4 + nch_h + k);
-      normalize_dlogits_kernel<<<(unsigned)cdiv(hrows * (v / 8), 256), 256, 0, st>>>(
-          static_cast<uint16_t*>(dl), v, (int)hrows, (int)v, part, nparts, lse + hr0, labels + hr0, scales + k, zt);
-      c->launches += 3;
+      if (rs) {  // LSE + per-row factor rowf (into zt) + label column; then (rowf * O_k)^T for K6
+        ce_combine_rowscale_kernel<<<(unsigned)cdiv(hrows * 32, 256), 256, 0, st>>>(
+            part, nparts, zt, labels + hr0, (int)hrows, (int)v, lse + hr0, lrow, stats + 3,
+            static_cast<uint16_t*>(dl), v, scales + k);
+        chunk_reduce_kernel<<<1, 1024, 0, st>>>(lrow, labels + hr0, (int)hrows, (int)v, stats + 4 + k,
+                                                stats + 4 + nch_h + k);
+        c->launches += 2;
+        MST_TRY(transpose_bf16(c, st, ok, h, ot, ldt_h, hrows, h, zt));
+      } else {
+        ce_combine_kernel<<<(unsigned)cdiv(hrows * 32, 256), 256, 0, st>>>(part, nparts, zt, labels + hr0, (int)hrows,
+                                                                          (int)v, lse + hr0, lrow, stats + 3);
+        chunk_reduce_kernel<<<1, 1024, 0, st>>>(lrow, labels + hr0, (int)hrows, (int)v, stats + 4 + k,
+                                                stats + 4 + nch_h + k);
+        normalize_dlogits_kernel<<<(unsigned)cdiv(hrows * (v / 8), 256), 256, 0, st>>>(
+            static_cast<uint16_t*>(dl), v, (int)hrows, (int)v, part, nparts, lse + hr0, labels + hr0, scales + k, zt);
+        c->launches += 3;
+      }
       // K5 + K6.  The last head chunk's K6 finalises dW_out: with a slab hook
       // it is cut into row slabs of H, one launch each (K5 rides in the
       // first), and each slab is handed to the hook as soon as it is enqueued.
@@ -2102,9 +2223,11 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
       for (int64_t s0 = 0; s0 < h; s0 += per) {
         const int64_t s1 = std::min(h, s0 + per);
         Launch L;
-        if (s0 == 0)
+        if (s0 == 0) {
           MST_TRY(build_plain(c, L, Operand{dl, hrows, v, v, false}, Operand{wout, h, v, v, false}, dok, h,
                               mst::kEpiStoreBf16, 0, (c->wide_mask & 2) ? 2 : 1));
+          if (rs) L.p.prob[0].rowscale = zt;
+        }
         MST_TRY(build_plain(c, L, Operand{bptr(ot, s0 * ldt_h), s1 - s0, hrows, ldt_h, false},
                             Operand{dl, v, hrows, v, true}, dwout + s0 * v, v, mst::kEpiAccF32, hbeta));
         MST_TRY(launch(c, st, L));

@@ -251,14 +251,20 @@ def test_lmhead_fused_matches_oracle(orc, shape):
     g = to_gpu(c)
     head = ms.LmHeadWeights(g["Wout"])
     plan = ms.make_chunk_plan(N, M)
-    for mode in (ms.TOKEN_WEIGHTED, ms.PAPER_MEAN):
-        loss, stats, lse, dX, dW = ms.miniseq_lmhead_fused(g["X"], g["L"], head, plan, mode, grad_loss=0.7)
-        ref_loss, ref_lse, _, _ = orc.miniseq_lmhead_forward(c["X"], c["L"], c["Wout"], M, mode)
-        rdX, rdW = orc.miniseq_lmhead_backward(c["X"], c["L"], c["Wout"], M, mode, 0.7, 2)  # numerators replayed
-        assert abs(float(loss) - ref_loss) <= 1e-4 * abs(ref_loss)
-        assert np.abs(lse.cpu().numpy() - ref_lse).max() <= 2e-3 * max(1.0, np.abs(ref_lse).max())
-        assert rel(dX, rdX) <= TIGHT_BF16, rel(dX, rdX)
-        assert rel(dW, rdW) <= TIGHT_F32, rel(dW, rdW)
+    ctx = ms.Context.get(0)
+    try:
+        for knob, replay in ((1, 3), (0, 2)):  # row-scaled (default) / per-tile numerators + normalize
+            ctx.set_tuning("dl_rowscale", knob)
+            for mode in (ms.TOKEN_WEIGHTED, ms.PAPER_MEAN):
+                loss, stats, lse, dX, dW = ms.miniseq_lmhead_fused(g["X"], g["L"], head, plan, mode, grad_loss=0.7)
+                ref_loss, ref_lse, _, _ = orc.miniseq_lmhead_forward(c["X"], c["L"], c["Wout"], M, mode)
+                rdX, rdW = orc.miniseq_lmhead_backward(c["X"], c["L"], c["Wout"], M, mode, 0.7, replay)
+                assert abs(float(loss) - ref_loss) <= 1e-4 * abs(ref_loss)
+                assert np.abs(lse.cpu().numpy() - ref_lse).max() <= 2e-3 * max(1.0, np.abs(ref_lse).max())
+                assert rel(dX, rdX) <= TIGHT_BF16, (knob, rel(dX, rdX))
+                assert rel(dW, rdW) <= TIGHT_F32, (knob, rel(dW, rdW))
+    finally:
+        ctx.set_tuning("dl_rowscale", 1)
 
 
 def test_block_step_fused_vs_two_pass_head():

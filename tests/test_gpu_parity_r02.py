@@ -81,16 +81,22 @@ def test_confident_softmax_both_head_paths(orc, shape):
     plan = ms.make_chunk_plan(N, M)
     ref_loss, ref_lse, _, _ = orc.miniseq_lmhead_forward(c["X"], c["L"], c["Wout"], M, 0)
     eX, eW = orc.miniseq_lmhead_backward(c["X"], c["L"], c["Wout"], M, 0, 1.0, 0)
-    # single-pass head
-    loss, _, lse, dX, dW = ms.miniseq_lmhead_fused(g["X"], g["L"], head, plan)
-    tX, tW = orc.miniseq_lmhead_backward(c["X"], c["L"], c["Wout"], M, 0, 1.0, 2)
-    errs = dict(loss=abs(float(loss) - ref_loss) / abs(ref_loss), dX_t=rel(dX, tX), dW_t=rel(dW, tW),
-                dX_e=rel(dX, eX), dW_e=rel(dW, eW))
-    print("confident single-pass", shape, "median p_label %.4f" % np.median(p), errs)
-    assert np.abs(lse.cpu().numpy() - ref_lse).max() <= 2e-3 * max(1.0, np.abs(ref_lse).max())
-    assert errs["loss"] <= 2e-3
-    assert errs["dX_t"] <= TIGHT_BF16 and errs["dW_t"] <= TIGHT_F32
-    assert errs["dX_e"] <= LOOSE and errs["dW_e"] <= LOOSE
+    # single-pass head: row-scaled (default, replay mode 3) and per-tile numerators + normalize (mode 2)
+    ctx = ms.Context.get(0)
+    try:
+        for knob, replay in ((0, 2), (1, 3)):
+            ctx.set_tuning("dl_rowscale", knob)
+            loss, _, lse, dX, dW = ms.miniseq_lmhead_fused(g["X"], g["L"], head, plan)
+            tX, tW = orc.miniseq_lmhead_backward(c["X"], c["L"], c["Wout"], M, 0, 1.0, replay)
+            errs = dict(loss=abs(float(loss) - ref_loss) / abs(ref_loss), dX_t=rel(dX, tX), dW_t=rel(dW, tW),
+                        dX_e=rel(dX, eX), dW_e=rel(dW, eW))
+            print("confident single-pass dl_rowscale=%d" % knob, shape, "median p_label %.4f" % np.median(p), errs)
+            assert np.abs(lse.cpu().numpy() - ref_lse).max() <= 2e-3 * max(1.0, np.abs(ref_lse).max())
+            assert errs["loss"] <= 2e-3
+            assert errs["dX_t"] <= TIGHT_BF16 and errs["dW_t"] <= TIGHT_F32
+            assert errs["dX_e"] <= LOOSE and errs["dW_e"] <= LOOSE
+    finally:
+        ctx.set_tuning("dl_rowscale", 1)
     # two-pass head (logits recomputed in the backward)
     loss2, hs = ms.miniseq_lmhead_forward(g["X"], g["L"], head, plan)
     dX2, dW2 = ms.miniseq_lmhead_backward(hs, head, plan)
@@ -425,3 +431,49 @@ def test_paired_dw_matches_per_chunk(shape):
         for a, b in zip(o[2:5], ref[2:5]):
             e = rel(a, b.double().cpu().numpy())
             assert e <= (0 if key == "k9k1" else 1e-5), (key, e)
+
+
+# ----------------------------------------------------------------- row-scaled head outside its window
+@pytest.mark.parametrize("shift", ["wide", "offset"])
+def test_rowscale_head_outside_reference_window(orc, shift):
+    """The row-scaled head stores numerators relative to 2^0 while a tile's
+    maximum z*log2e lies within +-64.  'wide': logits up to ~+-70 nats, so
+    some tiles use their own maximum and rows whose LSE leaves the window
+    are rescaled to R* = rint(lse2) by the combine; 'offset': every logit
+    shifted by ~+60 nats (all rows outside the window).  Both against the
+    oracle replaying the same references (mode 3), the exact oracle, and the
+    per-tile normalize path (dl_rowscale=0)."""
+    N, H, V, M = 384, 128, 2048, 3
+    c = orc.make_inputs(53, N, H, 8, V, p_ignore=0.1)
+    W = c["Wout"].astype(np.float64)
+    X = c["X"].astype(np.float64)
+    # 'wide': logits up to ~55 nats (79 log2 units): some tiles outside the window, most rows inside;
+    # 'offset': up to ~100 nats: most rows' LSE outside the window (R* = rint(lse2))
+    W = W * ((55.0 if shift == "wide" else 100.0) / np.abs(X @ W).max())
+    c["Wout"] = torch.from_numpy(W).float().bfloat16().float().numpy()
+    Z = X @ c["Wout"].astype(np.float64)
+    assert np.abs(Z).max() * 1.4427 > 64.0  # outside the window
+    if shift == "offset":
+        lse2 = (Z.max(axis=1) + np.log(np.exp(Z - Z.max(axis=1, keepdims=True)).sum(axis=1))) * 1.4427
+        assert (np.abs(lse2) > 64.0).mean() > 0.5
+    g = to_gpu(c)
+    head = ms.LmHeadWeights(g["Wout"])
+    plan = ms.make_chunk_plan(N, M)
+    ref_loss, ref_lse, _, _ = orc.miniseq_lmhead_forward(c["X"], c["L"], c["Wout"], M, 0)
+    eX, eW = orc.miniseq_lmhead_backward(c["X"], c["L"], c["Wout"], M, 0, 1.0, 0)
+    ctx = ms.Context.get(0)
+    try:
+        for knob, replay in ((1, 3), (0, 2)):
+            ctx.set_tuning("dl_rowscale", knob)
+            loss, _, lse, dX, dW = ms.miniseq_lmhead_fused(g["X"], g["L"], head, plan)
+            tX, tW = orc.miniseq_lmhead_backward(c["X"], c["L"], c["Wout"], M, 0, 1.0, replay)
+            assert np.isfinite(dX.float().cpu().numpy()).all() and np.isfinite(dW.cpu().numpy()).all()
+            errs = dict(loss=abs(float(loss) - ref_loss) / abs(ref_loss), dX_t=rel(dX, tX), dW_t=rel(dW, tW),
+                        dX_e=rel(dX, eX), dW_e=rel(dW, eW))
+            print("outside window", shift, "dl_rowscale=%d" % knob, errs)
+            assert np.abs(lse.cpu().numpy() - ref_lse).max() <= 2e-3 * max(1.0, np.abs(ref_lse).max())
+            assert errs["loss"] <= 2e-3
+            assert errs["dX_t"] <= TIGHT_BF16 and errs["dW_t"] <= TIGHT_F32
+            assert errs["dX_e"] <= LOOSE and errs["dW_e"] <= LOOSE
+    finally:
+        ctx.set_tuning("dl_rowscale", 1)

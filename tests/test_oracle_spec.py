@@ -267,3 +267,21 @@ def test_determinism(orc):
     b = orc.block(c["X"], c["L"], c["Wg"], c["Wu"], c["Wd"], c["Wout"], 3, 5)
     for k in a:
         assert np.array_equal(np.asarray(a[k]), np.asarray(b[k]))
+
+
+@pytest.mark.parametrize("scale_to", [None, 55.0, 100.0])
+def test_rowscale_replay_close_to_exact(scale_to):
+    """Replay mode 3 (the GPU's row-scaled LM-Head: numerators relative to one
+    reference per row, per-row factor on dX and on the transposed head input)
+    stays within bf16-level error of the exact f64 backward, also for logits
+    far outside its +-64 log2-unit reference window."""
+    from oracle import oracle as orc
+
+    c = orc.make_inputs(41, 600, 128, 64, 1000, p_ignore=0.1)
+    W = c["Wout"].astype(np.float64)
+    if scale_to:
+        W = (W * (scale_to / np.abs(c["X"].astype(np.float64) @ W).max())).astype(np.float32)
+    e = orc.miniseq_lmhead_backward(c["X"], c["L"], W, 4, 0, 0.7, 0)
+    t = orc.miniseq_lmhead_backward(c["X"], c["L"], W, 4, 0, 0.7, 3)
+    for a, b in zip(t, e):
+        assert np.linalg.norm(a - b) / np.linalg.norm(b) <= 5e-3
