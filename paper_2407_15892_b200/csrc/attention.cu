@@ -32,6 +32,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <type_traits>
 
 #include "attention.cuh"
 #include "ptx.cuh"
@@ -63,7 +64,22 @@ struct Args {
   float scale;         // softmax scale
   int nqb;             // q (= kv) tiles per sequence
   int inorder;         // g_mma_inorder
+  int poly;            // g_poly_exp: exp2 pairs (of every 4) on the FMA pipe in the forward softmax
 };
+
+// 2^x on the FMA / integer pipes (FlashAttention-4's split of the softmax
+// exponentials between MUFU and the FMA units): round-to-nearest through the
+// 1.5 * 2^23 magic constant, a degree-3 polynomial for 2^f on [-0.5, 0.5]
+// (relative error 7.5e-5 with fp32 coefficients, below bf16's 2^-9 P
+// rounding), the integer part added to the exponent field.  x is clamped at
+// -126 (the result is then ~1e-38, not 0: used only where no score is masked).
+__device__ __forceinline__ float exp2_poly(float x) {
+  x = fmaxf(x, -126.0f);
+  const float t = x + 12582912.0f;
+  const float f = x - (t - 12582912.0f);
+  const float p = fmaf(fmaf(fmaf(0.05517084f, f, 0.24260935f), f, 0.69326097f), f, 0.99992818f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
 
 __device__ __forceinline__ uint64_t kdesc(uint32_t saddr) { return ptx::sdesc_sw128(saddr, 16, 1024); }
 // MN-major operand: 64-wide N blocks one 16 KB tile apart.
@@ -389,6 +405,15 @@ __global__ void __launch_bounds__(384, 1) attn_fwd2_kernel(const __grid_constant
       };
       ptx::mbar_wait(ptx::smem_u32(q_full), 0);
       for (int t = 0; t < ntiles; ++t) qk(t, 0);
+      // Ping-pong: as soon as tile t's softmax of step j is done, its PV(j)
+      // and its next scores QK(j+1) are issued back to back, so the tensor
+      // core works on tile t while the other tile's softmax runs (issuing all
+      // PVs of step j before any QK(j+1) would make each tile's next softmax
+      // wait for the other tile's current one: the two softmaxes then run at
+      // the same time and compete for MUFU instead of alternating; measured
+      // 846 -> 1001 TFLOP/s at S=8192, hd=128).  Blocking waits: a polling
+      // issuer that serves whichever tile is ready first steals issue slots
+      // from the softmax warps of its SM sub-partition (measured 800).
       for (int j = 0; j < nkv; ++j) {
         const int s = j % kST;
         for (int t = 0; t < ntiles; ++t) {
@@ -403,13 +428,12 @@ __global__ void __launch_bounds__(384, 1) attn_fwd2_kernel(const __grid_constant
             ptx::umma_bf16_tmem_a_cg1(tmem + 256 * t + 128, tmem + 256 * t + 8 * k, mdesc(vb + k * 2048), pv_idesc,
                                       (j > 0 || k) ? 1u : 0u);
           ptx::umma_commit_cg1(ptx::smem_u32(&pv_done[t]));
+          if (j + 1 < nt[t]) {
+            if (!a.inorder) ptx::mbar_wait(ptx::smem_u32(&pv_done[t]), j & 1);  // P_t consumed before S_t is overwritten
+            qk(t, j + 1);
+          }
         }
         ptx::umma_commit_cg1(ptx::smem_u32(&kv_empty[s]));
-        for (int t = 0; t < ntiles; ++t) {
-          if (j + 1 >= nt[t]) continue;
-          if (!a.inorder) ptx::mbar_wait(ptx::smem_u32(&pv_done[t]), j & 1);  // P_t consumed before S_t is overwritten
-          qk(t, j + 1);
-        }
       }
     }
   }
@@ -455,19 +479,37 @@ __global__ void __launch_bounds__(384, 1) attn_fwd2_kernel(const __grid_constant
         const float ref = (j == 0 || mx2 > m2 + 8.f) ? mx2 : m2;
 #pragma unroll
         for (int k = 0; k < 8; ++k) s8[k] = 0.f;
+        // P = 2^(s * scale2 - ref); `np` of every 4 column pairs on the FMA
+        // pipe (exp2_poly), the rest on MUFU; the diagonal tile (masked
+        // scores) stays on MUFU so masked entries are exactly 0.
+        auto exp_pass = [&](auto np_tag) {
+          constexpr int NP = decltype(np_tag)::value;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t pk[16];
+          for (int c = 0; c < 4; ++c) {
+            uint32_t pk[16];
 #pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            const float p0 = ptx::ex2(fmaf(x[32 * c + e], a.scale2, -ref));
-            const float p1 = ptx::ex2(fmaf(x[32 * c + e + 1], a.scale2, -ref));
-            s8[e & 7] += p0;
-            s8[(e + 1) & 7] += p1;
-            pk[e >> 1] = ptx::pack_bf16(p0, p1);
+            for (int e = 0; e < 32; e += 2) {
+              const bool fma_pipe = ((e >> 1) & 3) >= 4 - NP;
+              const float y0 = fmaf(x[32 * c + e], a.scale2, -ref);
+              const float y1 = fmaf(x[32 * c + e + 1], a.scale2, -ref);
+              const float p0 = fma_pipe ? exp2_poly(y0) : ptx::ex2(y0);
+              const float p1 = fma_pipe ? exp2_poly(y1) : ptx::ex2(y1);
+              s8[e & 7] += p0;
+              s8[(e + 1) & 7] += p1;
+              pk[e >> 1] = ptx::pack_bf16(p0, p1);
+            }
+            ptx::tmem_st_32x32b_x16(tS + 16 * c, pk);  // P over already-read S columns
           }
-          ptx::tmem_st_32x32b_x16(tS + 16 * c, pk);  // P over already-read S columns
-        }
+        };
+        const int np = kv0 + kBM - 1 > q0 ? 0 : a.poly;  // warp-uniform
+        if (np == 0)
+          exp_pass(std::integral_constant<int, 0>{});
+        else if (np == 1)
+          exp_pass(std::integral_constant<int, 1>{});
+        else if (np == 2)
+          exp_pass(std::integral_constant<int, 2>{});
+        else
+          exp_pass(std::integral_constant<int, 3>{});
         const float rs = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
         const float alpha = ptx::ex2(m2 - ref);  // 0 on the first tile, 1 when the reference stayed
         // S_t(j) was issued after PV_t(j-1) completed: O_t is current here
@@ -1184,6 +1226,7 @@ int g_bwd_version = 2;  // attn_dkv2 / attn_dq2 (TMEM A operands, 2-stage ring) 
 // columns an earlier MMA of the same thread reads as its A operand is issued
 // without waiting for that MMA's completion); 0: wait for the commit first.
 int g_mma_inorder = 0;
+int g_poly_exp = 0;  // forward softmax exp2 pairs (of 4) on the FMA pipe (tuning "attn_poly" 0..3; measured slower: off)
 
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -1242,6 +1285,7 @@ int forward(void* enc, cudaStream_t st, const AttnShape& s, const void* q, int64
   a.scale2 = a.scale * kLog2e;
   a.nqb = (s.S + kBM - 1) / kBM;
   a.inorder = g_mma_inorder;
+  a.poly = g_poly_exp;
   const dim3 grid(static_cast<unsigned>(a.nqb * s.heads * s.B));
   const dim3 grid2(static_cast<unsigned>((a.nqb + 1) / 2 * s.heads * s.B));
   cudaError_t e;
