@@ -16,6 +16,19 @@ for chunked in (1, 0):
     ctx.set_tuning("chunked_block", chunked)
     st, gr = ms.block_step(X, L, mlp, head, 3, 3, check=True)
 ctx.set_tuning("chunked_block", 1)
+# round-2 schedule variants: paired dW GEMMs (even / odd chunk counts), row-scaled head on / off
+for pair in (1, 0):
+    for rs in (1, 0):
+        ctx.set_tuning("pair_dw", pair)
+        ctx.set_tuning("dl_rowscale", rs)
+        for mm, mh in ((4, 4), (5, 5), (2, 6)):
+            ms.block_step(X, L, mlp, head, mm, mh, check=True)
+        ms.miniseq_lmhead_fused(X, L, head, ms.make_chunk_plan(N, 3))
+ctx.set_tuning("pair_dw", 1)
+ctx.set_tuning("dl_rowscale", 1)
+# host-resident X / labels / dX (mst_block_step_host)
+dXh = torch.empty(N, H, dtype=torch.bfloat16).pin_memory()
+ms.block_step_host(X.cpu().pin_memory(), L.cpu().pin_memory(), mlp, head, 4, dXh)
 plan = ms.make_chunk_plan(N, 4)
 O, sv = ms.miniseq_mlp_forward(X, mlp, plan)
 loss, hs = ms.miniseq_lmhead_forward(O, L, head, plan)
