@@ -265,7 +265,10 @@ MST_API int mst_ctx_block_workspace(const mst_ctx* ctx, int64_t n, int64_t h, in
  * schedule only (M_mlp == M_head == m); results are bitwise those of
  * mst_block_step.  Everything is ordered on `stream` (the copy stream is
  * joined back before the call's work ends).  Workspace from
- * mst_ctx_block_host_workspace. */
+ * mst_ctx_block_host_workspace (the block workspace: the two X and two dX
+ * chunk buffers and the labels are owned by the context, allocated on first
+ * use and grown when a larger shape needs them; consecutive calls on one
+ * context overlap a step's first X copy with the previous step's tail). */
 MST_API int mst_ctx_block_host_workspace(const mst_ctx* ctx, int64_t n, int64_t h, int64_t i, int64_t v, int64_t m,
                                          size_t* bytes);
 MST_API int mst_block_step_host(mst_ctx* ctx, void* stream, const void* x_host, const int32_t* labels_host,

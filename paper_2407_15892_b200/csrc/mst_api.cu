@@ -138,6 +138,11 @@ struct mst_ctx {
   // mst_block_step_host: copy stream and chunk events (created on first use)
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t io_ev[10] = {};
+  // Device chunk buffers of mst_block_step_host (2 X, 2 dX, labels): owned by
+  // the context, so only this entry point's own chunk events order them and
+  // a step's first X copy can run under the previous step's tail.
+  void* io_dev = nullptr;
+  size_t io_bytes = 0;
   // memtrack side (mst.h): counters per memtrack.hpp:19-35, event hooks
   mst_counters ctr{};
   mst_mem_hook mem_fn = nullptr;
@@ -1194,6 +1199,7 @@ void mst_ctx_destroy(mst_ctx* c) {
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   cudaFree(c->scratch_dev);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->io_dev) cudaFree(c->io_dev);
   for (cudaEvent_t e : c->io_ev)
     if (e) cudaEventDestroy(e);
   if (c->tail_ev) cudaEventDestroy(c->tail_ev);
@@ -2297,7 +2303,24 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
     const int last = nch - 1;
     const bool last_paired = pair && (last & 1);  // the pair (last-1, last)
     const int dw0 = last_paired ? last - 1 : last;
-    for (int64_t s0 = 0; s0 < h; s0 += per) {
+    if (io && per == h) {
+      // Host-resident dX: K9 + K8 first, then K10 alone, so the last dX
+      // chunk's D2H copy runs under the K10 launch instead of after the step.
+      {
+        Launch L;
+        MST_TRY(add_k9(L, last));
+        MST_TRY(add_dw(L, dw0, last_paired, kGradK8));
+        MST_TRY(launch(c, st, L));
+        grad_slab(c, 2, 0, i, st);
+        MST_TRY(d2h(nch - 1));
+      }
+      Launch L;
+      MST_TRY(add_dw(L, dw0, last_paired, kGradK10, 0, h));
+      MST_TRY(launch(c, st, L));
+      grad_slab(c, 0, 0, h, st);
+      grad_slab(c, 1, 0, h, st);
+    }
+    for (int64_t s0 = 0; s0 < (io && per == h ? 0 : h); s0 += per) {
       const int64_t s1 = std::min(h, s0 + per);
       Launch L;
       if (s0 == 0) MST_TRY(add_k9(L, last));
@@ -2332,8 +2355,7 @@ int mst_ctx_block_host_workspace(const mst_ctx* c, int64_t n, int64_t h, int64_t
   if (!c || !bytes) return fail(MST_ERR_STATE, "NULL context or output");
   if (!uses_chunked_block(c, n, m, m))
     return fail(MST_ERR_CONFIG, "host-resident X / dX need the chunk-wise schedule (tuning chunked_block=1, fused_head=1)");
-  MST_TRY(mst_ctx_block_workspace(c, n, h, i, v, m, m, bytes));
-  *bytes += host_io_bytes(n, h, m);
+  MST_TRY(mst_ctx_block_workspace(c, n, h, i, v, m, m, bytes));  // the chunk IO buffers are the context's own
   return MST_OK;
 }
 
@@ -2357,18 +2379,30 @@ int mst_block_step_host(mst_ctx* c, void* stream, const void* x_host, const int3
     for (cudaEvent_t& e : c->io_ev) MST_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  char* io_base = static_cast<char*>(ws) + align_up(dev_need, 1024);
+  const size_t io_need = host_io_bytes(n, h, m);
+  if (c->io_bytes < io_need) {  // grow (rare): everything that used the old buffers has finished
+    MST_CUDA(cudaDeviceSynchronize());
+    if (c->io_dev) MST_CUDA(cudaFree(c->io_dev));
+    c->io_dev = nullptr;
+    c->io_bytes = 0;
+    if (cudaMalloc(&c->io_dev, io_need) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(MST_ERR_CONFIG, "cannot allocate %zu bytes of host-streaming chunk buffers", io_need);
+    }
+    c->io_bytes = io_need;
+  }
+  char* io_base = static_cast<char*>(c->io_dev);
   const size_t xcb = align_up(size_t(max_chunk(n, m)) * h * 2, 256);
   HostIO io{static_cast<const char*>(x_host), static_cast<char*>(dx_host),
             {io_base, io_base + xcb}, {io_base + 2 * xcb, io_base + 3 * xcb}, c->copy_stream,
             {c->io_ev[0], c->io_ev[1]}, {c->io_ev[2], c->io_ev[3]}, {c->io_ev[4], c->io_ev[5]},
             {c->io_ev[6], c->io_ev[7]}, c->io_ev[8]};
   int32_t* labels_dev = reinterpret_cast<int32_t*>(io_base + 4 * xcb);
-  // The copy stream writes into workspace chunk buffers: it first waits for
-  // everything already queued on the compute stream (an earlier op that used
-  // the same workspace region, or a recycled allocator block).
-  MST_CUDA(cudaEventRecord(c->io_ev[9], st));
-  MST_CUDA(cudaStreamWaitEvent(c->copy_stream, c->io_ev[9], 0));
+  // The copy stream only writes the context's own X / dX chunk buffers, whose
+  // previous uses are ordered by the chunk events of the previous call
+  // (x_free, dx_ready / dx_free): no wait for the whole compute stream, so
+  // X_0 of this step is copied while the previous step still runs.  The
+  // labels go in order on the compute stream.
   MST_CUDA(cudaMemcpyAsync(labels_dev, labels_host, size_t(n) * 4, cudaMemcpyHostToDevice, st));
   return block_step_chunked(c, st, nullptr, labels_dev, wg, wu, wd, wout, n, h, i, v, m, m, loss_mode, grad_loss, stats,
                             nullptr, dwg, dwu, dwd, dwout, accumulate, ws, dev_need, nullptr, &io);

@@ -477,3 +477,40 @@ def test_rowscale_head_outside_reference_window(orc, shift):
             assert errs["dX_e"] <= LOOSE and errs["dW_e"] <= LOOSE
     finally:
         ctx.set_tuning("dl_rowscale", 1)
+
+
+# ----------------------------------------------------------------- host-streaming step, back to back
+def test_block_step_host_back_to_back_and_growth():
+    """mst_block_step_host keeps its X / dX chunk buffers in the context and
+    lets a step's first X copy start under the previous step's tail (no wait
+    for the whole compute stream).  Steps enqueued back to back without a
+    synchronisation, on different inputs, with a device-path step on the
+    same context in between and a larger shape that grows the buffers, must
+    each equal the device-resident mst_block_step bitwise."""
+    torch.manual_seed(17)
+    H, I, V, M = 128, 256, 1024, 4
+    W = [(0.05 * torch.randn(*s, device="cuda")).bfloat16() for s in ((H, I), (H, I), (I, H), (H, V))]
+    mlp, head = ms.MlpWeights(*W[:3]), ms.LmHeadWeights(W[3])
+    runs = []
+    for N in (512, 512, 777, 1536, 512):
+        X = torch.randn(N, H, device="cuda").bfloat16()
+        L = torch.randint(0, V, (N,), device="cuda", dtype=torch.int32)
+        L[::9] = -100
+        st, gr = ms.block_step(X, L, mlp, head, M, M)
+        runs.append((N, X.cpu().pin_memory(), L.cpu().pin_memory(), st[:3].clone(), gr.dX.cpu(),
+                     [g.clone() for g in (gr.W_gate, gr.W_up, gr.W_down, gr.W_out)]))
+    torch.cuda.synchronize()
+    outs = []
+    for k, (N, Xh, Lh, _, _, _) in enumerate(runs):
+        dXh = torch.full((N, H), float("nan"), dtype=torch.bfloat16).pin_memory()
+        sth, grh = ms.block_step_host(Xh, Lh, mlp, head, M, dXh)
+        outs.append((dXh, sth[:3].clone(), [g.clone() for g in (grh.W_gate, grh.W_up, grh.W_down, grh.W_out)]))
+        if k == 1:  # a device-path step on the same context between host steps
+            Xd = Xh.cuda()
+            ms.block_step(Xd, Lh.cuda(), mlp, head, M, M)
+    torch.cuda.synchronize()
+    for (N, _, _, st, dX, gw), (dXh, sth, gh) in zip(runs, outs):
+        assert torch.equal(sth, st), N
+        assert torch.equal(dXh, dX), N
+        for a, b in zip(gh, gw):
+            assert torch.equal(a, b), N
