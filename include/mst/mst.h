@@ -312,18 +312,18 @@ MST_API int mst_lmhead_backward(mst_ctx* ctx, void* stream, const mst_lmhead_sav
  * writes the unnormalised softmax numerators in-tile; an in-place pass turns
  * them into dlogits once the row LSE is known.  Logits are never stored and
  * the only [n/M, V] buffer is the dlogits chunk.  `global_valid` (device
- * float, nullable) overrides the local valid-token count for token-weighted
+ * fp64 integer count, nullable) overrides the local valid-token count for token-weighted
  * scaling under sequence sharding.  Writes stats (loss in [2]), lse, dX and
  * dW_out (accumulate as in mst_lmhead_backward). */
 MST_API int mst_lmhead_fused(mst_ctx* ctx, void* stream, const void* x, const int32_t* labels, const void* w_out,
                              int64_t n, int64_t h, int64_t v, int64_t m, int loss_mode, float grad_loss,
-                             const float* global_valid, float* stats, float* lse, void* grad_x, float* grad_w_out,
+                             const double* global_valid, float* stats, float* lse, void* grad_x, float* grad_w_out,
                              int accumulate, void* workspace, size_t workspace_bytes);
 
 /* Number of labels in [0, V) among the n labels, written to *out (device
- * float) — the local count a sequence shard all-reduces before
+ * fp64, an exact integer below 2^53) — the local count a sequence shard all-reduces before
  * mst_lmhead_fused. */
-MST_API int mst_count_valid(mst_ctx* ctx, void* stream, const int32_t* labels, int64_t n, int64_t v, float* out);
+MST_API int mst_count_valid(mst_ctx* ctx, void* stream, const int32_t* labels, int64_t n, int64_t v, double* out);
 
 /* Non-finite scan ("all elements finite after any op in this
  * module (NaN/Inf is an error surfaced, not propagated)"): writes the number
@@ -345,7 +345,7 @@ MST_API int mst_block_step(mst_ctx* ctx, void* stream, const void* x, const int3
                    int accumulate, void* workspace, size_t workspace_bytes);
 
 /* Sequence-parallel variant: identical, except that the
- * token-weighted dlogits scale uses the device scalar *global_valid (the
+ * token-weighted dlogits scale uses the device fp64 scalar *global_valid (the
  * valid-label count all-reduced over the ranks, mst_count_valid + SUM) so
  * the per-rank weight gradients sum to the single-device gradient.  `stats`
  * keeps the rank-local loss sum / count (entries 0..1, additive).  NULL
@@ -354,7 +354,7 @@ MST_API int mst_block_step_sp(mst_ctx* ctx, void* stream, const void* x, const i
                    const void* w_up, const void* w_down, const void* w_out, int64_t n, int64_t h, int64_t i,
                    int64_t v, int64_t m_mlp, int64_t m_head, int loss_mode, float grad_loss, float* stats,
                    void* grad_x, float* grad_w_gate, float* grad_w_up, float* grad_w_down, float* grad_w_out,
-                   int accumulate, void* workspace, size_t workspace_bytes, const float* global_valid);
+                   int accumulate, void* workspace, size_t workspace_bytes, const double* global_valid);
 
 /* ---------------------------------------------------------------- decoder layer
  * The plumbing around the MsT blocks in the reference's Llama-style decoder

@@ -36,10 +36,6 @@ namespace {
 
 thread_local std::string g_last_error;
 
-struct Status {
-  int code = MST_OK;
-};
-
 int fail(int code, const char* fmt, ...) {
   char buf[1024];
   va_list ap;
@@ -680,7 +676,7 @@ __global__ void chunk_reduce_kernel(const float* __restrict__ loss_row, const in
 // SPEC's data errors are also raised into the context's sticky error word
 // (host-mapped; mst.h "Deferred errors"): 1 = every label ignored
 // (SPEC.md:219), 2 = labels outside [0, V) other than -100, 4 = non-finite loss.
-__global__ void finalize_loss_kernel(float* stats, int m, int mode, unsigned int* err, const float* gvalid) {
+__global__ void finalize_loss_kernel(float* stats, int m, int mode, unsigned int* err, const double* gvalid) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double s = 0, v = 0, pm = 0;
   int nonempty = 0;
@@ -698,7 +694,7 @@ __global__ void finalize_loss_kernel(float* stats, int m, int mode, unsigned int
   stats[2] = mode == MST_LOSS_PAPER_MEAN ? (float)(pm / m) : (float)(s / v);
   if (err) {
     // a sequence shard with no valid label is fine when the global count is not 0
-    const double vall = gvalid ? (double)*gvalid : v;
+    const double vall = gvalid ? *gvalid : v;
     const unsigned int f =
         (vall == 0 ? 1u : 0u) | (stats[3] > 0.f ? 2u : 0u) | ((v > 0 && !isfinite(stats[2])) ? 4u : 0u);
     if (f) {
@@ -710,8 +706,13 @@ __global__ void finalize_loss_kernel(float* stats, int m, int mode, unsigned int
 
 // Per-chunk dlogits scale: grad_loss / valid_global (token-weighted) or
 // grad_loss / (M * valid_chunk) (paper-mean).
-__global__ void grad_scale_kernel(const float* global_stats, const float* local_stats, int m, int mode,
-                                  float grad_loss, float* scales) {
+// The global count is exact: the caller's fp64 device scalar `gvalid`
+// (sequence-parallel: an integer count summed over ranks, exact
+// to 2^53 tokens), else the SPEC-op stats pair `gstats[1]`, else the sum of
+// this call's per-chunk counts formed in fp64 (each chunk count is an exact
+// fp32 integer, < 2^24 rows per chunk).
+__global__ void grad_scale_kernel(const double* gvalid, const float* gstats, const float* local_stats, int m,
+                                  int mode, float grad_loss, float* scales) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= m) return;
   float sc;
@@ -719,8 +720,16 @@ __global__ void grad_scale_kernel(const float* global_stats, const float* local_
     const float cv = local_stats[4 + m + c];
     sc = cv > 0 ? grad_loss / (float(m) * cv) : 0.f;
   } else {
-    const float gv = global_stats[1];
-    sc = gv > 0 ? grad_loss / gv : 0.f;
+    double gv;
+    if (gvalid) {
+      gv = *gvalid;
+    } else if (gstats) {
+      gv = gstats[1];
+    } else {
+      gv = 0;
+      for (int k = 0; k < m; ++k) gv += local_stats[4 + m + k];
+    }
+    sc = gv > 0 ? (float)((double)grad_loss / gv) : 0.f;
   }
   scales[c] = sc;
 }
@@ -836,23 +845,43 @@ int transpose_bf16(mst_ctx* c, cudaStream_t st, const void* src, int64_t ld_src,
 // plan recomputed in-kernel), so the single-pass head knows every dlogits
 // scale before its first chunk: stats[4+M+c] and stats[1] (total).
 __global__ void chunk_valid_kernel(const int32_t* __restrict__ labels, int64_t n, int m, int vocab, float* stats) {
-  __shared__ float sv[32];
+  __shared__ int sv[32];
   const int c = blockIdx.x;
   const int64_t q = n / m, r = n % m;
   const int64_t s0 = c * q + (c < r ? c : r), s1 = s0 + q + (c < r ? 1 : 0);
-  float v = 0.f;
+  int v = 0;  // integer count: exact; stored as an fp32 integer (< 2^24 rows per chunk)
   for (int64_t i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
     const int lab = labels[i];
-    v += (lab >= 0 && lab < vocab) ? 1.f : 0.f;
+    v += (lab >= 0 && lab < vocab) ? 1 : 0;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
   if ((threadIdx.x & 31) == 0) sv[threadIdx.x >> 5] = v;
   __syncthreads();
   if (threadIdx.x == 0) {
-    float t = 0.f;
+    long long t = 0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sv[w];
-    stats[4 + m + c] = t;
+    stats[4 + m + c] = (float)t;
+  }
+}
+
+// Exact valid-label count of a whole label vector as an fp64 integer
+// (mst_count_valid: the per-rank term of the sequence-parallel all-reduce).
+__global__ void count_valid_kernel(const int32_t* __restrict__ labels, int64_t n, int vocab, double* out) {
+  __shared__ long long sv[32];
+  long long v = 0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const int lab = labels[i];
+    v += (lab >= 0 && lab < vocab) ? 1 : 0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
+  if ((threadIdx.x & 31) == 0) sv[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sv[w];
+    *out = (double)t;
   }
 }
 
@@ -1763,8 +1792,8 @@ int mst_lmhead_backward(mst_ctx* c, void* stream, const mst_lmhead_saved* s, con
   const int64_t ldt = ld_t(n, m);
   const std::vector<int64_t> b = plan_bounds(n, m);
   const int nch = (int)b.size() - 1;
-  grad_scale_kernel<<<(nch + 255) / 256, 256, 0, st>>>(global_stats ? global_stats : s->stats, s->stats, nch,
-                                                           s->loss_mode, grad_loss, scales);
+  grad_scale_kernel<<<(nch + 255) / 256, 256, 0, st>>>(nullptr, global_stats, s->stats, nch, s->loss_mode,
+                                                           grad_loss, scales);
   c->launches += 1;
   WeightScope ws_(c, wout);
   for (int j = 0; j < nch; ++j) {
@@ -1801,7 +1830,7 @@ int mst_lmhead_backward(mst_ctx* c, void* stream, const mst_lmhead_saved* s, con
 }
 
 int mst_lmhead_fused(mst_ctx* c, void* stream, const void* x, const int32_t* labels, const void* wout, int64_t n,
-                     int64_t h, int64_t v, int64_t m, int loss_mode, float grad_loss, const float* global_valid,
+                     int64_t h, int64_t v, int64_t m, int loss_mode, float grad_loss, const double* global_valid,
                      float* stats, float* lse, void* dx, float* dwout, int accumulate, void* ws, size_t ws_bytes) {
   MST_CALL(c, stream);
   MST_TRY(check_dims(n, h, v, m, "V"));
@@ -1826,13 +1855,8 @@ int mst_lmhead_fused(mst_ctx* c, void* stream, const void* x, const int32_t* lab
   MST_CUDA(cudaMemsetAsync(stats, 0, sizeof(float) * MST_STATS_LEN(nch), st));
   chunk_valid_kernel<<<nch, 256, 0, st>>>(labels, n, nch, (int)v, stats);
   sum_valid_kernel<<<1, 32, 0, st>>>(stats, nch);
-  float* gstats = c->scratch_dev + 64;  // [2]: (unused, global valid)
-  if (global_valid) {
-    MST_CUDA(cudaMemcpyAsync(gstats + 1, global_valid, sizeof(float), cudaMemcpyDeviceToDevice, st));
-  } else {
-    MST_CUDA(cudaMemcpyAsync(gstats + 1, stats + 1, sizeof(float), cudaMemcpyDeviceToDevice, st));
-  }
-  grad_scale_kernel<<<(nch + 255) / 256, 256, 0, st>>>(gstats, stats, nch, loss_mode, grad_loss, scales);
+  grad_scale_kernel<<<(nch + 255) / 256, 256, 0, st>>>(global_valid, nullptr, stats, nch, loss_mode, grad_loss,
+                                                      scales);
   c->launches += 3;
   WeightScope ws_(c, wout);
   for (int j = 0; j < nch; ++j) {
@@ -1952,16 +1976,13 @@ int mst_count_nonfinite(mst_ctx* c, void* stream, const void* data, int64_t n, i
   return MST_OK;
 }
 
-int mst_count_valid(mst_ctx* c, void* stream, const int32_t* labels, int64_t n, int64_t v, float* out) {
+int mst_count_valid(mst_ctx* c, void* stream, const int32_t* labels, int64_t n, int64_t v, double* out) {
   MST_CALL(c, stream);
   if (!labels || !out) return fail(MST_ERR_CONFIG, "NULL pointer");
   if (n <= 0) return fail(MST_ERR_DATA, "N must be >= 1");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  float* tmp = c->scratch_dev + 128;  // MST_STATS_LEN(1) scratch floats
-  chunk_valid_kernel<<<1, 1024, 0, st>>>(labels, n, 1, (int)v, tmp);
-  sum_valid_kernel<<<1, 32, 0, st>>>(tmp, 1);
-  MST_CUDA(cudaMemcpyAsync(out, tmp + 1, sizeof(float), cudaMemcpyDeviceToDevice, st));
-  c->launches += 2;
+  count_valid_kernel<<<1, 1024, 0, st>>>(labels, n, (int)v, out);
+  c->launches += 1;
   MST_CUDA(cudaGetLastError());
   return MST_OK;
 }
@@ -1997,7 +2018,7 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
                               const void* wu, const void* wd, const void* wout, int64_t n, int64_t h, int64_t i,
                               int64_t v, int64_t m, int64_t mh, int loss_mode, float grad_loss, float* stats, void* dx, float* dwg,
                               float* dwu, float* dwd, float* dwout, int accumulate, void* ws, size_t ws_bytes,
-                              const float* global_valid, const HostIO* io = nullptr) {
+                              const double* global_valid, const HostIO* io = nullptr) {
   char* base = static_cast<char*>(ws);
   // O_j is consumed within chunk j; dO_j also by chunk j's dW_down GEMM,
   // which runs in chunk j+1's K2 launch: one O chunk, two dO chunks.
@@ -2044,12 +2065,9 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
   MST_CUDA(cudaMemsetAsync(stats, 0, sizeof(float) * MST_STATS_LEN(nch_h), st));
   chunk_valid_kernel<<<nch_h, 256, 0, st>>>(labels, n, nch_h, (int)v, stats);
   sum_valid_kernel<<<1, 32, 0, st>>>(stats, nch_h);
-  float* gstats = stats;
-  if (global_valid) {  // sequence-parallel caller: dlogits scaled by the all-reduced token count
-    gstats = c->scratch_dev + 64;
-    MST_CUDA(cudaMemcpyAsync(gstats + 1, global_valid, sizeof(float), cudaMemcpyDeviceToDevice, st));
-  }
-  grad_scale_kernel<<<(nch_h + 255) / 256, 256, 0, st>>>(gstats, stats, nch_h, loss_mode, grad_loss, scales);
+  // a sequence-parallel caller's global_valid is the all-reduced token count
+  grad_scale_kernel<<<(nch_h + 255) / 256, 256, 0, st>>>(global_valid, nullptr, stats, nch_h, loss_mode, grad_loss,
+                                                        scales);
   c->launches += 3;
   WeightScope ws_(c, wg, wu, wd, wout);
   const uint64_t act_bytes = (uint64_t)max_chunk(n, m) * h * 2;  // one chunk of O, two of dO
@@ -2419,7 +2437,7 @@ int mst_block_step(mst_ctx* c, void* stream, const void* x, const int32_t* label
 int mst_block_step_sp(mst_ctx* c, void* stream, const void* x, const int32_t* labels, const void* wg, const void* wu,
                       const void* wd, const void* wout, int64_t n, int64_t h, int64_t i, int64_t v, int64_t m_mlp,
                       int64_t m_head, int loss_mode, float grad_loss, float* stats, void* dx, float* dwg, float* dwu,
-                      float* dwd, float* dwout, int accumulate, void* ws, size_t ws_bytes, const float* global_valid) {
+                      float* dwd, float* dwout, int accumulate, void* ws, size_t ws_bytes, const double* global_valid) {
   MST_CALL(c, stream);
   size_t need = 0;
   MST_TRY(mst_ctx_block_workspace(c, n, h, i, v, m_mlp, m_head, &need));

@@ -567,9 +567,10 @@ def check_finite(**tensors: torch.Tensor) -> None:
 
 
 def count_valid(L: torch.Tensor, V: int) -> torch.Tensor:
-    """Device count of labels in [0, V) (1-element float tensor, no sync)."""
+    """Device count of labels in [0, V) (1-element fp64 tensor holding an
+    exact integer, no sync): the term a sequence shard SUM-all-reduces."""
     ctx = Context.get(L.device.index)
-    out = torch.empty(1, dtype=torch.float32, device=L.device)
+    out = torch.empty(1, dtype=torch.float64, device=L.device)
     _check(ctx.lib.mst_count_valid(ctx.handle, _stream(L), L.data_ptr(), L.shape[0], V, out.data_ptr()))
     return out
 
@@ -580,7 +581,7 @@ def miniseq_lmhead_fused(X: torch.Tensor, L: torch.Tensor, w: LmHeadWeights, pla
                          accumulate: bool = False):
     """LM-Head forward + backward in one pass over the chunks (SPEC.md:313-330
     back to back): returns (loss, stats, lse, dX, dW_out).  `global_valid`
-    (0-d/1-elem device float) overrides the local valid count (sequence sharding)."""
+    (1-elem device fp64 count) overrides the local valid count (sequence sharding)."""
     ctx = Context.get(X.device.index)
     N, H = X.shape
     V = w.W_out.shape[1]
@@ -592,6 +593,8 @@ def miniseq_lmhead_fused(X: torch.Tensor, L: torch.Tensor, w: LmHeadWeights, pla
         dW_out = torch.empty(H, V, dtype=torch.float32, device=X.device)
         accumulate = False
     _req(dW_out, "dW_out", torch.float32, (H, V))
+    if global_valid is not None:
+        _req(global_valid, "global_valid", torch.float64, (1,))
     stats = torch.empty(stats_len(len(plan)), dtype=torch.float32, device=X.device)
     lse = torch.empty(N, dtype=torch.float32, device=X.device)
     dX = torch.empty_like(X)
@@ -645,7 +648,7 @@ def block_step(X: torch.Tensor, L: torch.Tensor, mlp: MlpWeights, head: LmHeadWe
     check=True surfaces the SPEC's errors synchronously: NonFiniteError for
     NaN/Inf inputs or outputs, DataError for invalid labels or an
     all-ignored batch.
-    global_valid: device fp32 [1] valid-label count all-reduced over a
+    global_valid: device fp64 [1] valid-label count all-reduced over a
     sequence-parallel group (mst_block_step_sp).  grad_ready(which): called
     while the step is enqueued, right after the launch that makes gradient
     `which` (0 W_gate, 1 W_up, 2 W_down, 3 W_out) final in stream order
@@ -674,7 +677,7 @@ def block_step(X: torch.Tensor, L: torch.Tensor, mlp: MlpWeights, head: LmHeadWe
     need = block_workspace_bytes(N, H, I, V, M_mlp, M_head, ctx)
     ws = workspace if workspace is not None else ctx.workspace(need)
     if global_valid is not None:
-        _req(global_valid, "global_valid", torch.float32, (1,))
+        _req(global_valid, "global_valid", torch.float64, (1,))
     hook = slab_hook = None
     errors = []
 

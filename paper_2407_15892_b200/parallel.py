@@ -110,11 +110,8 @@ def sp_block_step_fused(ops, X: torch.Tensor, L: torch.Tensor, w: tuple, Wout: t
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     valid = ops.count_valid(L, Wout.shape[1])
     if world > 1:
-        # fp32 counts are exact integers per rank (< 2^24 tokens); the sum is
-        # formed in fp64 and rounded once
-        v64 = valid.double()
-        dist.all_reduce(v64, op=dist.ReduceOp.SUM, group=group)
-        valid.copy_(v64)
+        # fp64 integer counts: the SUM is exact up to 2^53 tokens
+        dist.all_reduce(valid, op=dist.ReduceOp.SUM, group=group)
     works = []
     reported = {}
     gl = (grads.W_gate, grads.W_up, grads.W_down, grads.W_out) if hasattr(grads, "W_out") else tuple(grads)

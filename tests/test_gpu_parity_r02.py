@@ -388,7 +388,7 @@ def test_deferred_device_errors_surface_without_check():
         ctx.check()
     ctx.check()  # nothing pending
     # sequence-parallel shard: no local valid label, global count 10 -> no error
-    st, _ = ms.block_step(X, ignored, mlp, head, 2, 2, global_valid=torch.tensor([10.0], device="cuda"))
+    st, _ = ms.block_step(X, ignored, mlp, head, 2, 2, global_valid=torch.tensor([10.0], dtype=torch.float64, device="cuda"))
     ctx.check()
 
 
