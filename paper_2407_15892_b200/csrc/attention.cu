@@ -65,6 +65,7 @@ struct Args {
   int nqb;             // q (= kv) tiles per sequence
   int inorder;         // g_mma_inorder
   int poly;            // g_poly_exp: exp2 pairs (of every 4) on the FMA pipe in the forward softmax
+  int bwd_order;       // g_bwd_order: backward GEMM issue orders (bit 0 dK/dV, bit 1 dQ)
 };
 
 // 2^x on the FMA / integer pipes (FlashAttention-4's split of the softmax
@@ -862,6 +863,13 @@ __global__ void attn_prep_kernel(const uint16_t* __restrict__ o, int64_t ldo, co
   deltap[idx] = acc;
 }
 
+constexpr int kThreads2 = 384;  // backward v2: TMA / MMA / TMEM warpgroup + 8 math warps
+
+// TMEM column of the k-th 16-deep K chunk of a packed bf16 A operand written
+// by two math warps per row: q (or kv) columns 0..63 packed at base + 0..31,
+// columns 64..127 at base + 64..95 (each half over its own fp32 columns).
+__device__ __forceinline__ uint32_t pk(uint32_t base, int k) { return base + 8 * k + (k >= 4 ? 32 : 0); }
+
 // Reads 64 columns (2 x 32) of this thread's TMEM row into v.
 __device__ __forceinline__ void load64(uint32_t taddr, float (&v)[64]) {
   ptx::tmem_ld_32x32b_x32(taddr, *reinterpret_cast<uint32_t(*)[32]>(v));
@@ -873,11 +881,13 @@ __device__ __forceinline__ void load64(uint32_t taddr, float (&v)[64]) {
 // so shared memory holds K, V and a 2-stage ring of {Q, dO, lse2, D} per q
 // tile: the next tile's loads overlap the current tile's math.
 template <int NSUB>
-__global__ void __launch_bounds__(kThreads, 1) attn_dkv2_kernel(const __grid_constant__ Args a) {
+__global__ void __launch_bounds__(kThreads2, 1) attn_dkv2_kernel(const __grid_constant__ Args a) {
   constexpr int kVec = 1024;  // lse2[128] + D[128]
   constexpr int kStage = 2 * NSUB * kTile + kVec;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-aligned by offsetting smem_raw itself (not through an integer cast), so
+  // the compiler keeps the shared address space: LDS, not generic LD.E.
+  uint8_t* sm = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* k_s = sm;
   uint8_t* v_s = k_s + NSUB * kTile;
   uint8_t* ring = v_s + NSUB * kTile;  // [2] {Q, dO, vec}
@@ -890,7 +900,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dkv2_kernel(const __grid_con
   uint64_t* ps_free = bars + 7;  // dV / dK of the tile done
   uint64_t* dp_full = bars + 8;  // dP^T in TMEM
   uint64_t* p_full = bars + 9;   // P^T written (math -> MMA)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  uint64_t* dv_done = bars + 10; // dV(t) has read P^T(t) (bwd_order 1)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gb = a.kvh * a.B;
@@ -910,10 +921,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dkv2_kernel(const __grid_con
       ptx::mbar_init(ptx::smem_u32(&qdo_empty[i]), 1);
     }
     ptx::mbar_init(ptx::smem_u32(s_full), 1);
-    ptx::mbar_init(ptx::smem_u32(ps_full), 4);
+    ptx::mbar_init(ptx::smem_u32(ps_full), 8);
     ptx::mbar_init(ptx::smem_u32(ps_free), 1);
     ptx::mbar_init(ptx::smem_u32(dp_full), 1);
-    ptx::mbar_init(ptx::smem_u32(p_full), 4);
+    ptx::mbar_init(ptx::smem_u32(p_full), 8);
+    ptx::mbar_init(ptx::smem_u32(dv_done), 1);
     ptx::fence_mbarrier_init();
   }
   if (warp == 2) ptx::tmem_alloc_cg1(ptx::smem_u32(tmem_slot), 512);
@@ -923,6 +935,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dkv2_kernel(const __grid_con
   const uint32_t tmem = *tmem_slot;
   const uint32_t tS = tmem, tDP = tmem + 128, tDV = tmem + 256, tDK = tmem + 384;
 
+  // Register pool (launched at 168 per thread): warpgroup 0 (TMA, MMA, TMEM
+  // allocator) gives up 128 x (168 - 96) = 9216, the two math warpgroups take
+  // 256 x (200 - 168) = 8192 of them (an .inc the pool cannot cover blocks forever).
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 96;\n" ::: "memory");
   if (warp == 0) {
     if (lane == 0) {
       ptx::mbar_arrive_expect_tx(ptx::smem_u32(kv_full), 2 * NSUB * kTile);
@@ -940,6 +957,62 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dkv2_kernel(const __grid_con
         const int64_t vo = ((static_cast<int64_t>(b) * a.heads + hq) * a.nqb + i) * kBM;
         ptx::bulk_load_1d(ptx::smem_u32(stage + 2 * NSUB * kTile), a.lse2p + vo, 512, fb);
         ptx::bulk_load_1d(ptx::smem_u32(stage + 2 * NSUB * kTile + 512), a.deltap + vo, 512, fb);
+      }
+    }
+  } else if (warp == 1 && (a.bwd_order & 1)) {
+    // Issue order with the next tile's scores under this tile's dS pass:
+    //   S^T(0) dP^T(0) | per t: [P^T(t)] dV(t), S^T(t+1) | [dS^T(t)] dK(t), dP^T(t+1)
+    // S^T(t+1) overwrites the P^T(t) columns once dV(t) has read them and
+    // dP^T(t+1) the dS^T(t) columns once dK(t) has; the math warps run the
+    // dS pass of t while the tensor core runs dV(t) + S^T(t+1), and the exp
+    // pass of t+1 while it runs dK(t) + dP^T(t+1).  (Order 0 issues S^T(t+1)
+    // only after dK(t) completes: the exp pass of t+1 then waits for dK(t)
+    // and S^T(t+1) in series.)
+    if (lane == 0) {
+      const uint32_t idesc = ptx::idesc_bf16(128, 64 * NSUB, 0, 1);
+      ptx::mbar_wait(ptx::smem_u32(kv_full), 0);
+      ptx::mbar_wait(ptx::smem_u32(&qdo_full[0]), 0);
+      ptx::tc_fence_after();
+      {
+        const uint32_t qs = ptx::smem_u32(ring), dos = qs + NSUB * kTile;
+        mma_tile(tS, ptx::smem_u32(k_s), qs, NSUB, 128, false, false);    // S^T = K Q^T
+        ptx::umma_commit_cg1(ptx::smem_u32(s_full));
+        mma_tile(tDP, ptx::smem_u32(v_s), dos, NSUB, 128, false, false);  // dP^T = V dO^T
+        ptx::umma_commit_cg1(ptx::smem_u32(dp_full));
+      }
+      for (int t = 0; t < iters; ++t) {
+        const int st = t & 1;
+        const uint32_t qs = ptx::smem_u32(ring + st * kStage), dos = qs + NSUB * kTile;
+        const bool more = t + 1 < iters;
+        const uint32_t qn = ptx::smem_u32(ring + (st ^ 1) * kStage), don = qn + NSUB * kTile;
+        ptx::mbar_wait(ptx::smem_u32(p_full), t & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < 8; ++k)  // dV += P^T dO (under the dS pass)
+          ptx::umma_bf16_tmem_a_cg1(tDV, pk(tS, k), mdesc(dos + k * 2048), idesc, (t > 0 || k) ? 1u : 0u);
+        if (more) {
+          ptx::mbar_wait(ptx::smem_u32(&qdo_full[st ^ 1]), ((t + 1) >> 1) & 1);
+          if (!a.inorder) {
+            ptx::umma_commit_cg1(ptx::smem_u32(dv_done));
+            ptx::mbar_wait(ptx::smem_u32(dv_done), t & 1);
+          }
+          ptx::tc_fence_after();
+          mma_tile(tS, ptx::smem_u32(k_s), qn, NSUB, 128, false, false);  // S^T(t+1) (under the dS pass)
+          ptx::umma_commit_cg1(ptx::smem_u32(s_full));
+        }
+        ptx::mbar_wait(ptx::smem_u32(ps_full), t & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < 8; ++k)  // dK += dS^T Q (under the next exp pass)
+          ptx::umma_bf16_tmem_a_cg1(tDK, pk(tDP, k), mdesc(qs + k * 2048), idesc, (t > 0 || k) ? 1u : 0u);
+        ptx::umma_commit_cg1(ptx::smem_u32(&qdo_empty[st]));
+        ptx::umma_commit_cg1(ptx::smem_u32(ps_free));
+        if (more) {
+          if (!a.inorder) ptx::mbar_wait(ptx::smem_u32(ps_free), t & 1);  // dK(t) read dS^T(t)
+          ptx::tc_fence_after();
+          mma_tile(tDP, ptx::smem_u32(v_s), don, NSUB, 128, false, false);  // dP^T(t+1)
+          ptx::umma_commit_cg1(ptx::smem_u32(dp_full));
+        }
       }
     }
   } else if (warp == 1) {
@@ -960,17 +1033,26 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dkv2_kernel(const __grid_con
         ptx::tc_fence_after();
 #pragma unroll
         for (int k = 0; k < 8; ++k)  // dV += P^T dO (under the dS pass)
-          ptx::umma_bf16_tmem_a_cg1(tDV, tS + 8 * k, mdesc(dos + k * 2048), idesc, (t > 0 || k) ? 1u : 0u);
+          ptx::umma_bf16_tmem_a_cg1(tDV, pk(tS, k), mdesc(dos + k * 2048), idesc, (t > 0 || k) ? 1u : 0u);
         ptx::mbar_wait(ptx::smem_u32(ps_full), t & 1);
         ptx::tc_fence_after();
 #pragma unroll
         for (int k = 0; k < 8; ++k)  // dK += dS^T Q
-          ptx::umma_bf16_tmem_a_cg1(tDK, tDP + 8 * k, mdesc(qs + k * 2048), idesc, (t > 0 || k) ? 1u : 0u);
+          ptx::umma_bf16_tmem_a_cg1(tDK, pk(tDP, k), mdesc(qs + k * 2048), idesc, (t > 0 || k) ? 1u : 0u);
         ptx::umma_commit_cg1(ptx::smem_u32(&qdo_empty[st]));
         ptx::umma_commit_cg1(ptx::smem_u32(ps_free));
       }
     }
-  } else if (warp >= 4) {  // one kv row per thread
+  }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 200;\n" ::: "memory");
+    // 8 math warps: kv row (warp & 3) * 32 + lane (the TMEM lane quadrant of
+    // the warp), q columns [64 hf, 64 hf + 64): two warps per SM sub-partition
+    // interleave their dependency chains.  Each half packs its bf16 P^T / dS^T
+    // over its OWN fp32 columns (cb .. cb + 31), so the halves never overwrite
+    // columns the other still reads; the GEMMs read the two packed halves
+    // through pk().
+    const int hf = (warp - 4) >> 2, cb = 64 * hf;
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const int r = (warp & 3) * 32 + lane;
     const int kv = k0 + r;
@@ -978,30 +1060,35 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dkv2_kernel(const __grid_con
       const int i = kblk + t % nq;
       const int q0 = i * kBM;
       const int st = t & 1;
-      const float* vec = reinterpret_cast<const float*>(ring + st * kStage + 2 * NSUB * kTile);
+      const float* vec = reinterpret_cast<const float*>(ring + st * kStage + 2 * NSUB * kTile) + cb;
       ptx::mbar_wait(ptx::smem_u32(&qdo_full[st]), (t >> 1) & 1);  // lse2 / D visible
       ptx::mbar_wait(ptx::smem_u32(s_full), t & 1);
       ptx::tc_fence_after();
-      const int nmask = q0 == k0 ? r : 0;  // diagonal tile: columns q < kv (c < r) are masked
-      float p[128];
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {  // P^T from S^T; packed over the read S^T columns
-        load64(tS + lane_off + 64 * c, *reinterpret_cast<float(*)[64]>(p + 64 * c));
-        ptx::tmem_ld_wait();
-        uint32_t pp[32];
+      const int nmask = (q0 == k0 ? r : 0) - cb;  // diagonal tile: columns q < kv are masked
+      float p[64];
+      load64(tS + lane_off + cb, p);
+      ptx::tmem_ld_wait();
+      uint32_t pp[32];
+      if (nmask > 0) {
 #pragma unroll
         for (int e = 0; e < 64; e += 2) {
-          const int col = 64 * c + e;
-          float p0 = ptx::ex2(fmaf(p[col], a.scale2, -vec[col]));
-          float p1 = ptx::ex2(fmaf(p[col + 1], a.scale2, -vec[col + 1]));
-          if (col < nmask) p0 = 0.f;
-          if (col + 1 < nmask) p1 = 0.f;
-          p[col] = p0;
-          p[col + 1] = p1;
+          float p0 = ptx::ex2(fmaf(p[e], a.scale2, -vec[e]));
+          float p1 = ptx::ex2(fmaf(p[e + 1], a.scale2, -vec[e + 1]));
+          if (e < nmask) p0 = 0.f;
+          if (e + 1 < nmask) p1 = 0.f;
+          p[e] = p0;
+          p[e + 1] = p1;
           pp[e >> 1] = ptx::pack_bf16(p0, p1);
         }
-        ptx::tmem_st_32x32b_x32(tS + lane_off + 32 * c, pp);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 64; e += 2) {
+          p[e] = ptx::ex2(fmaf(p[e], a.scale2, -vec[e]));
+          p[e + 1] = ptx::ex2(fmaf(p[e + 1], a.scale2, -vec[e + 1]));
+          pp[e >> 1] = ptx::pack_bf16(p[e], p[e + 1]);
+        }
       }
+      ptx::tmem_st_32x32b_x32(tS + lane_off + cb, pp);  // P^T half, packed over its own columns
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
       __syncwarp();
@@ -1009,17 +1096,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dkv2_kernel(const __grid_con
       ptx::mbar_wait(ptx::smem_u32(dp_full), t & 1);
       ptx::tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {  // dS^T = P^T (dP^T - D); packed over the read dP^T columns
-        float y[64];
-        load64(tDP + lane_off + 64 * c, y);
+      for (int c = 0; c < 2; ++c) {  // dS^T = P^T (dP^T - D), 32 columns at a time (register budget)
+        uint32_t y[32];
+        ptx::tmem_ld_32x32b_x32(tDP + lane_off + cb + 32 * c, y);
         ptx::tmem_ld_wait();
-        uint32_t dd[32];
+        uint32_t dd[16];
 #pragma unroll
-        for (int e = 0; e < 64; e += 2) {
-          const int col = 64 * c + e;
-          dd[e >> 1] = ptx::pack_bf16(p[col] * (y[e] - vec[128 + col]), p[col + 1] * (y[e + 1] - vec[128 + col + 1]));
+        for (int e = 0; e < 32; e += 2) {
+          const int col = 32 * c + e;
+          dd[e >> 1] = ptx::pack_bf16(p[col] * (__uint_as_float(y[e]) - vec[128 + col]),
+                                      p[col + 1] * (__uint_as_float(y[e + 1]) - vec[128 + col + 1]));
         }
-        ptx::tmem_st_32x32b_x32(tDP + lane_off + 32 * c, dd);
+        ptx::tmem_st_32x32b_x16(tDP + lane_off + cb + 16 * c, dd);  // packed over its own columns
       }
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
@@ -1030,8 +1118,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dkv2_kernel(const __grid_con
     ptx::tc_fence_after();
     const bool ok = kv < a.S;
     const int64_t row = static_cast<int64_t>(row0) + kv;
-    store_acc_row(tDV + lane_off, NSUB, 1.f, a.dv + row * a.lddv + g * a.hd, a.hd, ok);
-    store_acc_row(tDK + lane_off, NSUB, a.scale, a.dk + row * a.lddk + g * a.hd, a.hd, ok);
+    if (hf == 0)
+      store_acc_row(tDV + lane_off, NSUB, 1.f, a.dv + row * a.lddv + g * a.hd, a.hd, ok);
+    else
+      store_acc_row(tDK + lane_off, NSUB, a.scale, a.dk + row * a.lddk + g * a.hd, a.hd, ok);
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -1044,10 +1134,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dkv2_kernel(const __grid_con
 // dQ, v2: dS goes back into TMEM over the dP columns and feeds dQ += dS K as
 // the TMEM A operand; shared memory holds Q, dO and a 2-stage K/V ring.
 template <int NSUB>
-__global__ void __launch_bounds__(kThreads, 1) attn_dq2_kernel(const __grid_constant__ Args a) {
+__global__ void __launch_bounds__(kThreads2, 1) attn_dq2_kernel(const __grid_constant__ Args a) {
   constexpr int kST = 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-aligned by offsetting smem_raw itself (not through an integer cast), so
+  // the compiler keeps the shared address space: LDS, not generic LD.E.
+  uint8_t* sm = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* q_s = sm;
   uint8_t* do_s = q_s + NSUB * kTile;
   uint8_t* k_s = do_s + NSUB * kTile;        // [kST]
@@ -1080,7 +1172,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dq2_kernel(const __grid_cons
     }
     ptx::mbar_init(ptx::smem_u32(&s_full[0]), 1);
     ptx::mbar_init(ptx::smem_u32(&s_full[1]), 1);
-    ptx::mbar_init(ptx::smem_u32(ds_full), 4);
+    ptx::mbar_init(ptx::smem_u32(ds_full), 8);
     ptx::mbar_init(ptx::smem_u32(ds_free), 1);
     ptx::mbar_init(ptx::smem_u32(dp_full), 1);
     ptx::fence_mbarrier_init();
@@ -1092,6 +1184,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dq2_kernel(const __grid_cons
   const uint32_t tmem = *tmem_slot;
   const uint32_t tS2[2] = {tmem, tmem + 128}, tDP = tmem + 256, tDQ = tmem + 384;
 
+  // Register pool (launched at 168 per thread): warpgroup 0 (TMA, MMA, TMEM
+  // allocator) gives up 128 x (168 - 96) = 9216, the two math warpgroups take
+  // 256 x (200 - 168) = 8192 of them (an .inc the pool cannot cover blocks forever).
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 96;\n" ::: "memory");
   if (warp == 0) {
     if (lane == 0) {
       ptx::mbar_arrive_expect_tx(ptx::smem_u32(qdo_full), 2 * NSUB * kTile);
@@ -1103,6 +1200,44 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dq2_kernel(const __grid_cons
         ptx::mbar_arrive_expect_tx(ptx::smem_u32(&kv_full[s]), 2 * NSUB * kTile);
         load_tile<NSUB>(&a.m.k, ptx::smem_u32(k_s + s * NSUB * kTile), ptx::smem_u32(&kv_full[s]), g, row0 + j * kBM);
         load_tile<NSUB>(&a.m.v, ptx::smem_u32(v_s + s * NSUB * kTile), ptx::smem_u32(&kv_full[s]), g, row0 + j * kBM);
+      }
+    }
+  } else if (warp == 1 && (a.bwd_order & 2)) {
+    // dS(j) goes over S(j)'s buffer (the exp pass has read it into registers),
+    // so dP(j+1) needs only the dS pass of j to be done, not dQ(j):
+    //   S(0) dP(0) S(1) | per j: [dS(j)] dQ(j), dP(j+1), S(j+2) once dQ(j) has read dS(j)
+    if (lane == 0) {
+      const uint32_t idesc = ptx::idesc_bf16(128, 64 * NSUB, 0, 1);
+      ptx::mbar_wait(ptx::smem_u32(qdo_full), 0);
+      auto s_mma = [&](int j) {  // S(j) = Q K_j^T into buffer j & 1
+        const int s = j % kST;
+        ptx::mbar_wait(ptx::smem_u32(&kv_full[s]), (j / kST) & 1);
+        ptx::tc_fence_after();
+        mma_tile(tS2[j & 1], ptx::smem_u32(q_s), ptx::smem_u32(k_s + s * NSUB * kTile), NSUB, 128, false, false);
+        ptx::umma_commit_cg1(ptx::smem_u32(&s_full[j & 1]));
+      };
+      auto dp_mma = [&](int j) {  // dP(j) = dO V_j^T (K/V(j) landed: S(j) waited for them)
+        mma_tile(tDP, ptx::smem_u32(do_s), ptx::smem_u32(v_s + (j % kST) * NSUB * kTile), NSUB, 128, false, false);
+        ptx::umma_commit_cg1(ptx::smem_u32(dp_full));
+      };
+      s_mma(0);
+      dp_mma(0);
+      if (nblk > 1) s_mma(1);
+      for (int j = 0; j < nblk; ++j) {
+        const int s = j % kST;
+        const uint32_t ks = ptx::smem_u32(k_s + s * NSUB * kTile);
+        ptx::mbar_wait(ptx::smem_u32(ds_full), j & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < 8; ++k)  // dQ += dS K (dS from TMEM over S(j), K MN-major)
+          ptx::umma_bf16_tmem_a_cg1(tDQ, pk(tS2[j & 1], k), mdesc(ks + k * 2048), idesc, (j > 0 || k) ? 1u : 0u);
+        ptx::umma_commit_cg1(ptx::smem_u32(&kv_empty[s]));
+        ptx::umma_commit_cg1(ptx::smem_u32(ds_free));
+        if (j + 1 < nblk) dp_mma(j + 1);  // the dS pass of j has read dP(j)
+        if (j + 2 < nblk) {
+          if (!a.inorder) ptx::mbar_wait(ptx::smem_u32(ds_free), j & 1);  // dQ(j) read dS(j)
+          s_mma(j + 2);
+        }
       }
     }
   } else if (warp == 1) {
@@ -1128,12 +1263,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dq2_kernel(const __grid_cons
         ptx::tc_fence_after();
 #pragma unroll
         for (int k = 0; k < 8; ++k)  // dQ += dS K (dS from TMEM, K MN-major)
-          ptx::umma_bf16_tmem_a_cg1(tDQ, tDP + 8 * k, mdesc(ks + k * 2048), idesc, (j > 0 || k) ? 1u : 0u);
+          ptx::umma_bf16_tmem_a_cg1(tDQ, pk(tDP, k), mdesc(ks + k * 2048), idesc, (j > 0 || k) ? 1u : 0u);
         ptx::umma_commit_cg1(ptx::smem_u32(&kv_empty[s]));
         ptx::umma_commit_cg1(ptx::smem_u32(ds_free));
       }
     }
-  } else if (warp >= 4) {
+  }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 200;\n" ::: "memory");
+    // 8 math warps: q row (warp & 3) * 32 + lane, kv columns [64 hf, 64 hf + 64)
+    // (two warps per sub-partition; each half packs dS over its own columns, pk()).
+    const int hf = (warp - 4) >> 2, cb = 64 * hf;
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const int r = (warp & 3) * 32 + lane;
     const int q = q0 + r;
@@ -1145,31 +1285,36 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dq2_kernel(const __grid_cons
       const int kv0 = j * kBM;
       ptx::mbar_wait(ptx::smem_u32(&s_full[j & 1]), (j >> 1) & 1);
       ptx::tc_fence_after();
-      const int nvalid = kv0 + kBM - 1 > q0 ? q - kv0 + 1 : kBM;  // kv columns <= q
-      float p[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        ptx::tmem_ld_32x32b_x32(tS2[j & 1] + lane_off + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(p + 32 * c));
+      const int nvalid = (kv0 + kBM - 1 > q0 ? q - kv0 + 1 : kBM) - cb;  // kv columns <= q
+      float p[64];
+      load64(tS2[j & 1] + lane_off + cb, p);
       ptx::tmem_ld_wait();
+      if (nvalid < 64) {
 #pragma unroll
-      for (int e = 0; e < 128; ++e) {  // P (the exp pass runs under the dP GEMM)
-        const float x = ptx::ex2(fmaf(p[e], a.scale2, -lse2));
-        p[e] = e < nvalid ? x : 0.f;
+        for (int e = 0; e < 64; ++e) {  // P (the exp pass runs under the dP GEMM)
+          const float x = ptx::ex2(fmaf(p[e], a.scale2, -lse2));
+          p[e] = e < nvalid ? x : 0.f;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 64; ++e) p[e] = ptx::ex2(fmaf(p[e], a.scale2, -lse2));
       }
       ptx::mbar_wait(ptx::smem_u32(dp_full), j & 1);
       ptx::tc_fence_after();
+      const uint32_t tDS = (a.bwd_order & 2) ? tS2[j & 1] : tDP;
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        float y[64];
-        load64(tDP + lane_off + 64 * c, y);
+      for (int c = 0; c < 2; ++c) {  // 32 columns at a time (register budget)
+        uint32_t y[32];
+        ptx::tmem_ld_32x32b_x32(tDP + lane_off + cb + 32 * c, y);
         ptx::tmem_ld_wait();
-        uint32_t d2[32];
+        uint32_t d2[16];
 #pragma unroll
-        for (int e = 0; e < 64; e += 2) {
-          const int col = 64 * c + e;
-          d2[e >> 1] = ptx::pack_bf16(p[col] * (y[e] - dd), p[col + 1] * (y[e + 1] - dd));
+        for (int e = 0; e < 32; e += 2) {
+          const int col = 32 * c + e;
+          d2[e >> 1] = ptx::pack_bf16(p[col] * (__uint_as_float(y[e]) - dd), p[col + 1] * (__uint_as_float(y[e + 1]) - dd));
         }
-        ptx::tmem_st_32x32b_x32(tDP + lane_off + 32 * c, d2);  // dS over read dP columns
+        // dS over read S (order bit 1) or dP columns
+        ptx::tmem_st_32x32b_x16(tDS + lane_off + cb + 16 * c, d2);
       }
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
@@ -1178,8 +1323,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_dq2_kernel(const __grid_cons
     }
     ptx::mbar_wait(ptx::smem_u32(ds_free), (nblk - 1) & 1);
     ptx::tc_fence_after();
-    store_acc_row(tDQ + lane_off, NSUB, a.scale, a.dq + (static_cast<int64_t>(row0) + q) * a.lddq + h * a.hd, a.hd,
-                  ok);
+    // dQ columns [64 hf, 64 hf + 64) of this row
+    if (cb < a.hd)
+      store_acc_row(tDQ + lane_off + cb, 1, a.scale,
+                    a.dq + (static_cast<int64_t>(row0) + q) * a.lddq + h * a.hd + cb, a.hd - cb, ok);
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -1200,7 +1347,7 @@ constexpr int fwd2_smem() {
 }
 template <int NSUB>
 constexpr int dkv2_smem() {
-  return 1024 + 2 * NSUB * kTile + 2 * (2 * NSUB * kTile + 1024) + 256;  // bars: 10 x 8 B + TMEM slot
+  return 1024 + 2 * NSUB * kTile + 2 * (2 * NSUB * kTile + 1024) + 256;  // bars: 11 x 8 B + TMEM slot
 }
 template <int NSUB>
 constexpr int dq2_smem() {
@@ -1226,6 +1373,10 @@ int g_bwd_version = 2;  // attn_dkv2 / attn_dq2 (TMEM A operands, 2-stage ring) 
 // columns an earlier MMA of the same thread reads as its A operand is issued
 // without waiting for that MMA's completion); 0: wait for the commit first.
 int g_mma_inorder = 0;
+// Backward issue orders (tuning "attn_bwd_order", bit mask): bit 0 = dK/dV
+// kernel issues the next tile's scores under the dS pass; bit 1 = dQ kernel
+// writes dS over S so dP(j+1) does not wait for dQ(j).  0 = round-2 orders.
+int g_bwd_order = 3;
 int g_poly_exp = 0;  // forward softmax exp2 pairs (of 4) on the FMA pipe (tuning "attn_poly" 0..3; measured slower: off)
 
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -1344,6 +1495,7 @@ int backward(void* enc, cudaStream_t st, const AttnShape& s, const void* q, int6
   a.scale2 = a.scale * kLog2e;
   a.nqb = (s.S + kBM - 1) / kBM;
   a.inorder = g_mma_inorder;
+  a.bwd_order = g_bwd_order;
   const int64_t nrow = static_cast<int64_t>(s.B) * s.heads * s.S;
   const dim3 gkv(static_cast<unsigned>(a.nqb * s.kvh * s.B)), gq(static_cast<unsigned>(a.nqb * s.heads * s.B));
   cudaError_t e;
@@ -1360,12 +1512,12 @@ int backward(void* enc, cudaStream_t st, const AttnShape& s, const void* q, int6
         s.heads, s.hd, spad);
     if (s.hd <= 64) {
       if ((e = set_attrs<1>()) != cudaSuccess) return *err = cudaGetErrorString(e), 2;
-      attn_dkv2_kernel<1><<<gkv, kThreads, dkv2_smem<1>(), st>>>(a);
-      attn_dq2_kernel<1><<<gq, kThreads, dq2_smem<1>(), st>>>(a);
+      attn_dkv2_kernel<1><<<gkv, kThreads2, dkv2_smem<1>(), st>>>(a);
+      attn_dq2_kernel<1><<<gq, kThreads2, dq2_smem<1>(), st>>>(a);
     } else {
       if ((e = set_attrs<2>()) != cudaSuccess) return *err = cudaGetErrorString(e), 2;
-      attn_dkv2_kernel<2><<<gkv, kThreads, dkv2_smem<2>(), st>>>(a);
-      attn_dq2_kernel<2><<<gq, kThreads, dq2_smem<2>(), st>>>(a);
+      attn_dkv2_kernel<2><<<gkv, kThreads2, dkv2_smem<2>(), st>>>(a);
+      attn_dq2_kernel<2><<<gq, kThreads2, dq2_smem<2>(), st>>>(a);
     }
   } else {
     attn_delta_kernel<<<static_cast<unsigned>((nrow + 255) / 256), 256, 0, st>>>(

@@ -9,6 +9,7 @@ namespace mst_attn {
 
 extern int g_fwd_version;  // 2: two q tiles per CTA (default), 1: one (tuning "attn_fwd")
 extern int g_mma_inorder;  // 1: no completion wait between dependent MMAs of one thread (tuning "attn_inorder")
+extern int g_bwd_order;    // backward issue orders, bit 0 dK/dV, bit 1 dQ (tuning "attn_bwd_order")
 extern int g_poly_exp;     // forward softmax exp2 pairs (of 4) on the FMA pipe, 0..3 (tuning "attn_poly")
 extern int g_bwd_version;  // 2: TMEM A operands + 2-stage ring (default), 1: the first kernels (tuning "attn_bwd")
 

@@ -1320,6 +1320,9 @@ int mst_ctx_set_tuning(mst_ctx* c, const char* key, int value) {
   } else if (std::strcmp(key, "attn_poly") == 0) {  // forward softmax exp2 pairs of 4 on the FMA pipe (process-wide)
     if (value < 0 || value > 3) return fail(MST_ERR_CONFIG, "attn_poly must be 0..3");
     mst_attn::g_poly_exp = value;
+  } else if (std::strcmp(key, "attn_bwd_order") == 0) {  // dK/dV GEMM issue order (process-wide)
+    if (value < 0 || value > 3) return fail(MST_ERR_CONFIG, "attn_bwd_order must be 0..3 (bit 0 dK/dV, bit 1 dQ)");
+    mst_attn::g_bwd_order = value;
   } else if (std::strcmp(key, "attn_inorder") == 0) {
     mst_attn::g_mma_inorder = value != 0;
   } else if (std::strcmp(key, "attn_bwd") == 0) {  // attention backward kernel version (process-wide)
