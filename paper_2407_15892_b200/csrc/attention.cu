@@ -1095,19 +1095,15 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_dkv2_kernel(const __grid_co
       if (lane == 0) ptx::mbar_arrive_local(ptx::smem_u32(p_full));  // dV GEMM may start
       ptx::mbar_wait(ptx::smem_u32(dp_full), t & 1);
       ptx::tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {  // dS^T = P^T (dP^T - D), 32 columns at a time (register budget)
-        uint32_t y[32];
-        ptx::tmem_ld_32x32b_x32(tDP + lane_off + cb + 32 * c, y);
+      {  // dS^T = P^T (dP^T - D): one TMEM load of the 64 columns (one exposed load latency)
+        float y[64];
+        load64(tDP + lane_off + cb, y);
         ptx::tmem_ld_wait();
-        uint32_t dd[16];
+        uint32_t dd[32];
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          const int col = 32 * c + e;
-          dd[e >> 1] = ptx::pack_bf16(p[col] * (__uint_as_float(y[e]) - vec[128 + col]),
-                                      p[col + 1] * (__uint_as_float(y[e + 1]) - vec[128 + col + 1]));
-        }
-        ptx::tmem_st_32x32b_x16(tDP + lane_off + cb + 16 * c, dd);  // packed over its own columns
+        for (int e = 0; e < 64; e += 2)
+          dd[e >> 1] = ptx::pack_bf16(p[e] * (y[e] - vec[128 + e]), p[e + 1] * (y[e + 1] - vec[128 + e + 1]));
+        ptx::tmem_st_32x32b_x32(tDP + lane_off + cb, dd);  // packed over its own columns
       }
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
@@ -1302,19 +1298,14 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_dq2_kernel(const __grid_con
       ptx::mbar_wait(ptx::smem_u32(dp_full), j & 1);
       ptx::tc_fence_after();
       const uint32_t tDS = (a.bwd_order & 2) ? tS2[j & 1] : tDP;
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {  // 32 columns at a time (register budget)
-        uint32_t y[32];
-        ptx::tmem_ld_32x32b_x32(tDP + lane_off + cb + 32 * c, y);
+      {  // one TMEM load of the 64 columns (one exposed load latency)
+        float y[64];
+        load64(tDP + lane_off + cb, y);
         ptx::tmem_ld_wait();
-        uint32_t d2[16];
+        uint32_t d2[32];
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          const int col = 32 * c + e;
-          d2[e >> 1] = ptx::pack_bf16(p[col] * (__uint_as_float(y[e]) - dd), p[col + 1] * (__uint_as_float(y[e + 1]) - dd));
-        }
-        // dS over read S (order bit 1) or dP columns
-        ptx::tmem_st_32x32b_x16(tDS + lane_off + cb + 16 * c, d2);
+        for (int e = 0; e < 64; e += 2) d2[e >> 1] = ptx::pack_bf16(p[e] * (y[e] - dd), p[e + 1] * (y[e + 1] - dd));
+        ptx::tmem_st_32x32b_x32(tDS + lane_off + cb, d2);  // dS over read S (order bit 1) or dP columns
       }
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
