@@ -1127,24 +1127,29 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_dkv2_kernel(const __grid_co
   }
 }
 
-// dQ, v2: dS goes back into TMEM over the dP columns and feeds dQ += dS K as
-// the TMEM A operand; shared memory holds Q, dO and a 2-stage K/V ring.
+// dQ, v2: dS goes back into TMEM (over S, order bit 1, or over dP) and feeds
+// dQ += dS K as the TMEM A operand; shared memory holds Q, dO, a 3-stage K
+// ring and a 2-stage V ring (K(j) is held until dQ(j), V(j) only until dP(j),
+// so with three K stages the scores two tiles ahead never wait for a K load
+// that could only start after dQ(j)).
 template <int NSUB>
 __global__ void __launch_bounds__(kThreads2, 1) attn_dq2_kernel(const __grid_constant__ Args a) {
-  constexpr int kST = 2;
+  constexpr int kKS = 3, kVS = 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-aligned by offsetting smem_raw itself (not through an integer cast), so
   // the compiler keeps the shared address space: LDS, not generic LD.E.
   uint8_t* sm = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* q_s = sm;
   uint8_t* do_s = q_s + NSUB * kTile;
-  uint8_t* k_s = do_s + NSUB * kTile;        // [kST]
-  uint8_t* v_s = k_s + kST * NSUB * kTile;   // [kST]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(v_s + kST * NSUB * kTile);
+  uint8_t* k_s = do_s + NSUB * kTile;        // [kKS]
+  uint8_t* v_s = k_s + kKS * NSUB * kTile;   // [kVS]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(v_s + kVS * NSUB * kTile);
   uint64_t* qdo_full = bars;
-  uint64_t* kv_full = bars + 1;        // [kST]
-  uint64_t* kv_empty = kv_full + kST;  // [kST]
-  uint64_t* s_full = kv_empty + kST;  // [2]: S double-buffered in TMEM
+  uint64_t* k_full = bars + 1;        // [kKS]
+  uint64_t* k_empty = k_full + kKS;   // [kKS]
+  uint64_t* v_full = k_empty + kKS;   // [kVS]
+  uint64_t* v_empty = v_full + kVS;   // [kVS]
+  uint64_t* s_full = v_empty + kVS;   // [2]: S double-buffered in TMEM
   uint64_t* ds_full = s_full + 2;
   uint64_t* ds_free = ds_full + 1;
   uint64_t* dp_full = ds_free + 1;
@@ -1162,9 +1167,13 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_dq2_kernel(const __grid_con
 
   if (warp == 1 && lane == 0) {
     ptx::mbar_init(ptx::smem_u32(qdo_full), 1);
-    for (int s = 0; s < kST; ++s) {
-      ptx::mbar_init(ptx::smem_u32(&kv_full[s]), 1);
-      ptx::mbar_init(ptx::smem_u32(&kv_empty[s]), 1);
+    for (int s = 0; s < kKS; ++s) {
+      ptx::mbar_init(ptx::smem_u32(&k_full[s]), 1);
+      ptx::mbar_init(ptx::smem_u32(&k_empty[s]), 1);
+    }
+    for (int s = 0; s < kVS; ++s) {
+      ptx::mbar_init(ptx::smem_u32(&v_full[s]), 1);
+      ptx::mbar_init(ptx::smem_u32(&v_empty[s]), 1);
     }
     ptx::mbar_init(ptx::smem_u32(&s_full[0]), 1);
     ptx::mbar_init(ptx::smem_u32(&s_full[1]), 1);
@@ -1179,89 +1188,88 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_dq2_kernel(const __grid_con
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tS2[2] = {tmem, tmem + 128}, tDP = tmem + 256, tDQ = tmem + 384;
+  auto kst = [&](int j) { return ptx::smem_u32(k_s + (j % kKS) * NSUB * kTile); };
+  auto vst = [&](int j) { return ptx::smem_u32(v_s + (j % kVS) * NSUB * kTile); };
 
   // Register pool (launched at 168 per thread): warpgroup 0 (TMA, MMA, TMEM
   // allocator) gives up 128 x (168 - 96) = 9216, the two math warpgroups take
   // 256 x (200 - 168) = 8192 of them (an .inc the pool cannot cover blocks forever).
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 96;\n" ::: "memory");
-  if (warp == 0) {
+  if (warp == 0) {  // Q, dO, then the K ring
     if (lane == 0) {
       ptx::mbar_arrive_expect_tx(ptx::smem_u32(qdo_full), 2 * NSUB * kTile);
       load_tile<NSUB>(&a.m.q, ptx::smem_u32(q_s), ptx::smem_u32(qdo_full), h, row0 + q0);
       load_tile<NSUB>(&a.m.dout, ptx::smem_u32(do_s), ptx::smem_u32(qdo_full), h, row0 + q0);
       for (int j = 0; j < nblk; ++j) {
-        const int s = j % kST;
-        ptx::mbar_wait(ptx::smem_u32(&kv_empty[s]), ((j / kST) & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(ptx::smem_u32(&kv_full[s]), 2 * NSUB * kTile);
-        load_tile<NSUB>(&a.m.k, ptx::smem_u32(k_s + s * NSUB * kTile), ptx::smem_u32(&kv_full[s]), g, row0 + j * kBM);
-        load_tile<NSUB>(&a.m.v, ptx::smem_u32(v_s + s * NSUB * kTile), ptx::smem_u32(&kv_full[s]), g, row0 + j * kBM);
+        const int s = j % kKS;
+        ptx::mbar_wait(ptx::smem_u32(&k_empty[s]), ((j / kKS) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(ptx::smem_u32(&k_full[s]), NSUB * kTile);
+        load_tile<NSUB>(&a.m.k, kst(j), ptx::smem_u32(&k_full[s]), g, row0 + j * kBM);
       }
     }
-  } else if (warp == 1 && (a.bwd_order & 2)) {
-    // dS(j) goes over S(j)'s buffer (the exp pass has read it into registers),
-    // so dP(j+1) needs only the dS pass of j to be done, not dQ(j):
-    //   S(0) dP(0) S(1) | per j: [dS(j)] dQ(j), dP(j+1), S(j+2) once dQ(j) has read dS(j)
+  } else if (warp == 3) {  // the V ring
     if (lane == 0) {
-      const uint32_t idesc = ptx::idesc_bf16(128, 64 * NSUB, 0, 1);
-      ptx::mbar_wait(ptx::smem_u32(qdo_full), 0);
-      auto s_mma = [&](int j) {  // S(j) = Q K_j^T into buffer j & 1
-        const int s = j % kST;
-        ptx::mbar_wait(ptx::smem_u32(&kv_full[s]), (j / kST) & 1);
-        ptx::tc_fence_after();
-        mma_tile(tS2[j & 1], ptx::smem_u32(q_s), ptx::smem_u32(k_s + s * NSUB * kTile), NSUB, 128, false, false);
-        ptx::umma_commit_cg1(ptx::smem_u32(&s_full[j & 1]));
-      };
-      auto dp_mma = [&](int j) {  // dP(j) = dO V_j^T (K/V(j) landed: S(j) waited for them)
-        mma_tile(tDP, ptx::smem_u32(do_s), ptx::smem_u32(v_s + (j % kST) * NSUB * kTile), NSUB, 128, false, false);
-        ptx::umma_commit_cg1(ptx::smem_u32(dp_full));
-      };
-      s_mma(0);
-      dp_mma(0);
-      if (nblk > 1) s_mma(1);
       for (int j = 0; j < nblk; ++j) {
-        const int s = j % kST;
-        const uint32_t ks = ptx::smem_u32(k_s + s * NSUB * kTile);
-        ptx::mbar_wait(ptx::smem_u32(ds_full), j & 1);
-        ptx::tc_fence_after();
-#pragma unroll
-        for (int k = 0; k < 8; ++k)  // dQ += dS K (dS from TMEM over S(j), K MN-major)
-          ptx::umma_bf16_tmem_a_cg1(tDQ, pk(tS2[j & 1], k), mdesc(ks + k * 2048), idesc, (j > 0 || k) ? 1u : 0u);
-        ptx::umma_commit_cg1(ptx::smem_u32(&kv_empty[s]));
-        ptx::umma_commit_cg1(ptx::smem_u32(ds_free));
-        if (j + 1 < nblk) dp_mma(j + 1);  // the dS pass of j has read dP(j)
-        if (j + 2 < nblk) {
-          if (!a.inorder) ptx::mbar_wait(ptx::smem_u32(ds_free), j & 1);  // dQ(j) read dS(j)
-          s_mma(j + 2);
-        }
+        const int s = j % kVS;
+        ptx::mbar_wait(ptx::smem_u32(&v_empty[s]), ((j / kVS) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(ptx::smem_u32(&v_full[s]), NSUB * kTile);
+        load_tile<NSUB>(&a.m.v, vst(j), ptx::smem_u32(&v_full[s]), g, row0 + j * kBM);
       }
     }
   } else if (warp == 1) {
+    // order bit 1: dS(j) goes over S(j)'s buffer (the exp pass has read it into
+    // registers), so dP(j+1) needs only the dS pass of j to be done, not dQ(j):
+    //   S(0) dP(0) S(1) | per j: [dS(j)] dQ(j), dP(j+1), S(j+2) once dQ(j) has read dS(j)
+    // otherwise dS(j) goes over dP(j):
+    //   S(0) | per j: dP(j) once dQ(j-1) has read dS(j-1), S(j+1) | [dS(j)] dQ(j)
     if (lane == 0) {
       const uint32_t idesc = ptx::idesc_bf16(128, 64 * NSUB, 0, 1);
+      const bool ds_over_s = (a.bwd_order & 2) != 0;
       ptx::mbar_wait(ptx::smem_u32(qdo_full), 0);
       auto s_mma = [&](int j) {  // S(j) = Q K_j^T into buffer j & 1
-        const int s = j % kST;
-        ptx::mbar_wait(ptx::smem_u32(&kv_full[s]), (j / kST) & 1);
+        ptx::mbar_wait(ptx::smem_u32(&k_full[j % kKS]), (j / kKS) & 1);
         ptx::tc_fence_after();
-        mma_tile(tS2[j & 1], ptx::smem_u32(q_s), ptx::smem_u32(k_s + s * NSUB * kTile), NSUB, 128, false, false);
+        mma_tile(tS2[j & 1], ptx::smem_u32(q_s), kst(j), NSUB, 128, false, false);
         ptx::umma_commit_cg1(ptx::smem_u32(&s_full[j & 1]));
       };
-      s_mma(0);
-      for (int j = 0; j < nblk; ++j) {
-        const int s = j % kST;
-        const uint32_t ks = ptx::smem_u32(k_s + s * NSUB * kTile);
-        if (j > 0 && !a.inorder) ptx::mbar_wait(ptx::smem_u32(ds_free), (j - 1) & 1);  // dQ(j-1) read dS
-        mma_tile(tDP, ptx::smem_u32(do_s), ptx::smem_u32(v_s + s * NSUB * kTile), NSUB, 128, false, false);  // dP
+      auto dp_mma = [&](int j) {  // dP(j) = dO V_j^T
+        ptx::mbar_wait(ptx::smem_u32(&v_full[j % kVS]), (j / kVS) & 1);
+        ptx::tc_fence_after();
+        mma_tile(tDP, ptx::smem_u32(do_s), vst(j), NSUB, 128, false, false);
         ptx::umma_commit_cg1(ptx::smem_u32(dp_full));
-        if (j + 1 < nblk) s_mma(j + 1);  // the next scores under this tile's dS pass
+        ptx::umma_commit_cg1(ptx::smem_u32(&v_empty[j % kVS]));
+      };
+      auto dq_mma = [&](int j, uint32_t ds) {  // dQ += dS K (dS from TMEM, K MN-major)
         ptx::mbar_wait(ptx::smem_u32(ds_full), j & 1);
         ptx::tc_fence_after();
+        const uint32_t ks = kst(j);
 #pragma unroll
-        for (int k = 0; k < 8; ++k)  // dQ += dS K (dS from TMEM, K MN-major)
-          ptx::umma_bf16_tmem_a_cg1(tDQ, pk(tDP, k), mdesc(ks + k * 2048), idesc, (j > 0 || k) ? 1u : 0u);
-        ptx::umma_commit_cg1(ptx::smem_u32(&kv_empty[s]));
+        for (int k = 0; k < 8; ++k)
+          ptx::umma_bf16_tmem_a_cg1(tDQ, pk(ds, k), mdesc(ks + k * 2048), idesc, (j > 0 || k) ? 1u : 0u);
+        ptx::umma_commit_cg1(ptx::smem_u32(&k_empty[j % kKS]));
         ptx::umma_commit_cg1(ptx::smem_u32(ds_free));
+      };
+      if (ds_over_s) {
+        s_mma(0);
+        dp_mma(0);
+        if (nblk > 1) s_mma(1);
+        for (int j = 0; j < nblk; ++j) {
+          dq_mma(j, tS2[j & 1]);
+          if (j + 1 < nblk) dp_mma(j + 1);  // the dS pass of j has read dP(j)
+          if (j + 2 < nblk) {
+            if (!a.inorder) ptx::mbar_wait(ptx::smem_u32(ds_free), j & 1);  // dQ(j) read dS(j)
+            s_mma(j + 2);
+          }
+        }
+      } else {
+        s_mma(0);
+        for (int j = 0; j < nblk; ++j) {
+          if (j > 0 && !a.inorder) ptx::mbar_wait(ptx::smem_u32(ds_free), (j - 1) & 1);  // dQ(j-1) read dS
+          dp_mma(j);
+          if (j + 1 < nblk) s_mma(j + 1);  // the next scores under this tile's dS pass
+          dq_mma(j, tDP);
+        }
       }
     }
   }
@@ -1341,8 +1349,8 @@ constexpr int dkv2_smem() {
   return 1024 + 2 * NSUB * kTile + 2 * (2 * NSUB * kTile + 1024) + 256;  // bars: 11 x 8 B + TMEM slot
 }
 template <int NSUB>
-constexpr int dq2_smem() {
-  return 1024 + 2 * NSUB * kTile + 4 * NSUB * kTile + 256;
+constexpr int dq2_smem() {  // Q, dO, 3 K stages, 2 V stages, bars
+  return 1024 + 2 * NSUB * kTile + 5 * NSUB * kTile + 256;
 }
 template <int NSUB>
 constexpr int dkv_smem() {
