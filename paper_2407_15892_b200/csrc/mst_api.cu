@@ -706,11 +706,10 @@ __global__ void finalize_loss_kernel(float* stats, int m, int mode, unsigned int
 
 // Per-chunk dlogits scale: grad_loss / valid_global (token-weighted) or
 // grad_loss / (M * valid_chunk) (paper-mean).
-// The global count is exact: the caller's fp64 device scalar `gvalid`
-// (sequence-parallel: an integer count summed over ranks, exact
-// to 2^53 tokens), else the SPEC-op stats pair `gstats[1]`, else the sum of
-// this call's per-chunk counts formed in fp64 (each chunk count is an exact
-// fp32 integer, < 2^24 rows per chunk).
+// The global count is exact: a device fp64 integer (`gvalid`: the caller's
+// all-reduced count, or this call's total from
+// sum_valid_kernel / valid_total_kernel), else the SPEC-op stats pair
+// `gstats[1]` of mst_lmhead_backward.
 __global__ void grad_scale_kernel(const double* gvalid, const float* gstats, const float* local_stats, int m,
                                   int mode, float grad_loss, float* scales) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -720,18 +719,19 @@ __global__ void grad_scale_kernel(const double* gvalid, const float* gstats, con
     const float cv = local_stats[4 + m + c];
     sc = cv > 0 ? grad_loss / (float(m) * cv) : 0.f;
   } else {
-    double gv;
-    if (gvalid) {
-      gv = *gvalid;
-    } else if (gstats) {
-      gv = gstats[1];
-    } else {
-      gv = 0;
-      for (int k = 0; k < m; ++k) gv += local_stats[4 + m + k];
-    }
+    const double gv = gvalid ? *gvalid : static_cast<double>(gstats[1]);
     sc = gv > 0 ? (float)((double)grad_loss / gv) : 0.f;
   }
   scales[c] = sc;
+}
+
+// Total of the per-chunk valid counts (exact fp32 integers, < 2^24 rows per
+// chunk) summed in fp64: one thread, O(M).
+__global__ void valid_total_kernel(const float* __restrict__ stats, int m, double* __restrict__ tot) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double t = 0;
+  for (int c = 0; c < m; ++c) t += stats[4 + m + c];
+  *tot = t;
 }
 
 // dst[c, r] = src[r, c] for a rows x cols bf16 block (row strides ld_src /
@@ -885,11 +885,13 @@ __global__ void count_valid_kernel(const int32_t* __restrict__ labels, int64_t n
   }
 }
 
-__global__ void sum_valid_kernel(float* stats, int m) {
+// stats[1] (the reported count) and the exact fp64 total in *tot.
+__global__ void sum_valid_kernel(float* stats, int m, double* tot) {
   if (threadIdx.x != 0) return;
   double t = 0;
   for (int c = 0; c < m; ++c) t += stats[4 + m + c];
   stats[1] = (float)t;
+  *tot = t;
 }
 
 // In place: e (bf16 softmax numerator, tile max m_tile in part[].x) ->
@@ -1795,9 +1797,11 @@ int mst_lmhead_backward(mst_ctx* c, void* stream, const mst_lmhead_saved* s, con
   const int64_t ldt = ld_t(n, m);
   const std::vector<int64_t> b = plan_bounds(n, m);
   const int nch = (int)b.size() - 1;
-  grad_scale_kernel<<<(nch + 255) / 256, 256, 0, st>>>(nullptr, global_stats, s->stats, nch, s->loss_mode,
-                                                           grad_loss, scales);
-  c->launches += 1;
+  double* tot = reinterpret_cast<double*>(c->scratch_dev + 64);  // context scratch (calls are serialised)
+  if (!global_stats) valid_total_kernel<<<1, 32, 0, st>>>(s->stats, nch, tot);
+  grad_scale_kernel<<<(nch + 255) / 256, 256, 0, st>>>(global_stats ? nullptr : tot, global_stats, s->stats, nch,
+                                                           s->loss_mode, grad_loss, scales);
+  c->launches += global_stats ? 1 : 2;
   WeightScope ws_(c, wout);
   for (int j = 0; j < nch; ++j) {
     const int64_t r0 = b[j], rows = b[j + 1] - b[j];
@@ -1857,9 +1861,10 @@ int mst_lmhead_fused(mst_ctx* c, void* stream, const void* x, const int32_t* lab
   // total (or the caller's global count), dlogits scale per chunk.
   MST_CUDA(cudaMemsetAsync(stats, 0, sizeof(float) * MST_STATS_LEN(nch), st));
   chunk_valid_kernel<<<nch, 256, 0, st>>>(labels, n, nch, (int)v, stats);
-  sum_valid_kernel<<<1, 32, 0, st>>>(stats, nch);
-  grad_scale_kernel<<<(nch + 255) / 256, 256, 0, st>>>(global_valid, nullptr, stats, nch, loss_mode, grad_loss,
-                                                      scales);
+  double* tot = reinterpret_cast<double*>(c->scratch_dev + 64);  // context scratch (calls are serialised)
+  sum_valid_kernel<<<1, 32, 0, st>>>(stats, nch, tot);
+  grad_scale_kernel<<<(nch + 255) / 256, 256, 0, st>>>(global_valid ? global_valid : tot, nullptr, stats, nch,
+                                                      loss_mode, grad_loss, scales);
   c->launches += 3;
   WeightScope ws_(c, wout);
   for (int j = 0; j < nch; ++j) {
@@ -2067,10 +2072,11 @@ static int block_step_chunked(mst_ctx* c, cudaStream_t st, const void* x, const 
   // dlogits scales depend only on the labels: compute them up front.
   MST_CUDA(cudaMemsetAsync(stats, 0, sizeof(float) * MST_STATS_LEN(nch_h), st));
   chunk_valid_kernel<<<nch_h, 256, 0, st>>>(labels, n, nch_h, (int)v, stats);
-  sum_valid_kernel<<<1, 32, 0, st>>>(stats, nch_h);
+  double* tot = reinterpret_cast<double*>(c->scratch_dev + 64);  // context scratch (calls are serialised)
+  sum_valid_kernel<<<1, 32, 0, st>>>(stats, nch_h, tot);
   // a sequence-parallel caller's global_valid is the all-reduced token count
-  grad_scale_kernel<<<(nch_h + 255) / 256, 256, 0, st>>>(global_valid, nullptr, stats, nch_h, loss_mode, grad_loss,
-                                                        scales);
+  grad_scale_kernel<<<(nch_h + 255) / 256, 256, 0, st>>>(global_valid ? global_valid : tot, nullptr, stats, nch_h,
+                                                        loss_mode, grad_loss, scales);
   c->launches += 3;
   WeightScope ws_(c, wg, wu, wd, wout);
   const uint64_t act_bytes = (uint64_t)max_chunk(n, m) * h * 2;  // one chunk of O, two of dO
