@@ -339,7 +339,8 @@ __global__ void __launch_bounds__(384, 1) attn_fwd2_kernel(const __grid_constant
   uint64_t* s_full = kv_empty + kST;            // [2 tiles]
   uint64_t* p_full = s_full + 2;                // [2 tiles]
   uint64_t* pv_done = p_full + 2;               // [2 tiles]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
+  uint64_t* o_done = pv_done + 2;               // [2 tiles] the tile's last PV has completed (one phase)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int hb = a.heads * a.B;
@@ -365,6 +366,7 @@ __global__ void __launch_bounds__(384, 1) attn_fwd2_kernel(const __grid_constant
       ptx::mbar_init(ptx::smem_u32(&s_full[t]), 1);
       ptx::mbar_init(ptx::smem_u32(&p_full[t]), 4);
       ptx::mbar_init(ptx::smem_u32(&pv_done[t]), 1);
+      ptx::mbar_init(ptx::smem_u32(&o_done[t]), 1);
     }
     ptx::fence_mbarrier_init();
   }
@@ -428,7 +430,10 @@ __global__ void __launch_bounds__(384, 1) attn_fwd2_kernel(const __grid_constant
           for (int k = 0; k < 8; ++k)
             ptx::umma_bf16_tmem_a_cg1(tmem + 256 * t + 128, tmem + 256 * t + 8 * k, mdesc(vb + k * 2048), pv_idesc,
                                       (j > 0 || k) ? 1u : 0u);
-          ptx::umma_commit_cg1(ptx::smem_u32(&pv_done[t]));
+          // pv_done phases only where the issuer waits for them (every phase
+          // observed before the next completes); o_done ends the tile
+          if (j + 1 < nt[t] && !a.inorder) ptx::umma_commit_cg1(ptx::smem_u32(&pv_done[t]));
+          if (j + 1 == nt[t]) ptx::umma_commit_cg1(ptx::smem_u32(&o_done[t]));
           if (j + 1 < nt[t]) {
             if (!a.inorder) ptx::mbar_wait(ptx::smem_u32(&pv_done[t]), j & 1);  // P_t consumed before S_t is overwritten
             qk(t, j + 1);
@@ -531,7 +536,7 @@ __global__ void __launch_bounds__(384, 1) attn_fwd2_kernel(const __grid_constant
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_local(ptx::smem_u32(&p_full[t]));
       }
-      ptx::mbar_wait(ptx::smem_u32(&pv_done[t]), (nt[t] - 1) & 1);
+      ptx::mbar_wait(ptx::smem_u32(&o_done[t]), 0);
       ptx::tc_fence_after();
       const bool ok = q < a.S;
       store_acc_row(tO, NSUB, 1.f / l, a.o + (static_cast<int64_t>(row0) + q) * a.ldo + h * a.hd, a.hd, ok);
@@ -901,7 +906,8 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_dkv2_kernel(const __grid_co
   uint64_t* dp_full = bars + 8;  // dP^T in TMEM
   uint64_t* p_full = bars + 9;   // P^T written (math -> MMA)
   uint64_t* dv_done = bars + 10; // dV(t) has read P^T(t) (bwd_order 1)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
+  uint64_t* acc_done = bars + 11; // the last dK / dV MMA has completed (one phase)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gb = a.kvh * a.B;
@@ -918,7 +924,9 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_dkv2_kernel(const __grid_co
     ptx::mbar_init(ptx::smem_u32(kv_full), 1);
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(ptx::smem_u32(&qdo_full[i]), 1);
-      ptx::mbar_init(ptx::smem_u32(&qdo_empty[i]), 1);
+      // the MMA commit after dK(t) + the 8 math warps once they are done with
+      // the stage's lse2 / D (the bulk copy of t+2 overwrites them)
+      ptx::mbar_init(ptx::smem_u32(&qdo_empty[i]), 9);
     }
     ptx::mbar_init(ptx::smem_u32(s_full), 1);
     ptx::mbar_init(ptx::smem_u32(ps_full), 8);
@@ -926,6 +934,7 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_dkv2_kernel(const __grid_co
     ptx::mbar_init(ptx::smem_u32(dp_full), 1);
     ptx::mbar_init(ptx::smem_u32(p_full), 8);
     ptx::mbar_init(ptx::smem_u32(dv_done), 1);
+    ptx::mbar_init(ptx::smem_u32(acc_done), 1);
     ptx::fence_mbarrier_init();
   }
   if (warp == 2) ptx::tmem_alloc_cg1(ptx::smem_u32(tmem_slot), 512);
@@ -1006,7 +1015,10 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_dkv2_kernel(const __grid_co
         for (int k = 0; k < 8; ++k)  // dK += dS^T Q (under the next exp pass)
           ptx::umma_bf16_tmem_a_cg1(tDK, pk(tDP, k), mdesc(qs + k * 2048), idesc, (t > 0 || k) ? 1u : 0u);
         ptx::umma_commit_cg1(ptx::smem_u32(&qdo_empty[st]));
-        ptx::umma_commit_cg1(ptx::smem_u32(ps_free));
+        // ps_free phases are committed only where they are waited for (each
+        // phase observed before the next completes); acc_done ends the tile
+        if (more && !a.inorder) ptx::umma_commit_cg1(ptx::smem_u32(ps_free));
+        if (!more) ptx::umma_commit_cg1(ptx::smem_u32(acc_done));
         if (more) {
           if (!a.inorder) ptx::mbar_wait(ptx::smem_u32(ps_free), t & 1);  // dK(t) read dS^T(t)
           ptx::tc_fence_after();
@@ -1040,7 +1052,8 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_dkv2_kernel(const __grid_co
         for (int k = 0; k < 8; ++k)  // dK += dS^T Q
           ptx::umma_bf16_tmem_a_cg1(tDK, pk(tDP, k), mdesc(qs + k * 2048), idesc, (t > 0 || k) ? 1u : 0u);
         ptx::umma_commit_cg1(ptx::smem_u32(&qdo_empty[st]));
-        ptx::umma_commit_cg1(ptx::smem_u32(ps_free));
+        if (t + 1 < iters && !a.inorder) ptx::umma_commit_cg1(ptx::smem_u32(ps_free));
+        if (t + 1 == iters) ptx::umma_commit_cg1(ptx::smem_u32(acc_done));
       }
     }
   }
@@ -1108,9 +1121,15 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_dkv2_kernel(const __grid_co
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_local(ptx::smem_u32(ps_full));
+      if (lane == 0) {
+        ptx::mbar_arrive_local(ptx::smem_u32(ps_full));
+        // lse2 / D of this stage read (generic proxy) before the producer's
+        // bulk copy (async proxy) of t + 2 overwrites them
+        ptx::fence_proxy_async_smem();
+        ptx::mbar_arrive_local(ptx::smem_u32(&qdo_empty[st]));
+      }
     }
-    ptx::mbar_wait(ptx::smem_u32(ps_free), (iters - 1) & 1);
+    ptx::mbar_wait(ptx::smem_u32(acc_done), 0);
     ptx::tc_fence_after();
     const bool ok = kv < a.S;
     const int64_t row = static_cast<int64_t>(row0) + kv;
@@ -1153,7 +1172,8 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_dq2_kernel(const __grid_con
   uint64_t* ds_full = s_full + 2;
   uint64_t* ds_free = ds_full + 1;
   uint64_t* dp_full = ds_free + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dp_full + 1);
+  uint64_t* acc_done = dp_full + 1;  // the last dQ MMA has completed (one phase)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int hb = a.heads * a.B;
@@ -1180,6 +1200,7 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_dq2_kernel(const __grid_con
     ptx::mbar_init(ptx::smem_u32(ds_full), 8);
     ptx::mbar_init(ptx::smem_u32(ds_free), 1);
     ptx::mbar_init(ptx::smem_u32(dp_full), 1);
+    ptx::mbar_init(ptx::smem_u32(acc_done), 1);
     ptx::fence_mbarrier_init();
   }
   if (warp == 2) ptx::tmem_alloc_cg1(ptx::smem_u32(tmem_slot), 512);
@@ -1240,7 +1261,10 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_dq2_kernel(const __grid_con
         ptx::umma_commit_cg1(ptx::smem_u32(dp_full));
         ptx::umma_commit_cg1(ptx::smem_u32(&v_empty[j % kVS]));
       };
-      auto dq_mma = [&](int j, uint32_t ds) {  // dQ += dS K (dS from TMEM, K MN-major)
+      // dQ += dS K (dS from TMEM, K MN-major).  ds_free phases are committed
+      // only where the issuer waits for them (`free_waited`), so every phase
+      // is observed before the next completes; acc_done ends the tile.
+      auto dq_mma = [&](int j, uint32_t ds, bool free_waited) {
         ptx::mbar_wait(ptx::smem_u32(ds_full), j & 1);
         ptx::tc_fence_after();
         const uint32_t ks = kst(j);
@@ -1248,14 +1272,15 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_dq2_kernel(const __grid_con
         for (int k = 0; k < 8; ++k)
           ptx::umma_bf16_tmem_a_cg1(tDQ, pk(ds, k), mdesc(ks + k * 2048), idesc, (j > 0 || k) ? 1u : 0u);
         ptx::umma_commit_cg1(ptx::smem_u32(&k_empty[j % kKS]));
-        ptx::umma_commit_cg1(ptx::smem_u32(ds_free));
+        if (free_waited && !a.inorder) ptx::umma_commit_cg1(ptx::smem_u32(ds_free));
+        if (j + 1 == nblk) ptx::umma_commit_cg1(ptx::smem_u32(acc_done));
       };
       if (ds_over_s) {
         s_mma(0);
         dp_mma(0);
         if (nblk > 1) s_mma(1);
         for (int j = 0; j < nblk; ++j) {
-          dq_mma(j, tS2[j & 1]);
+          dq_mma(j, tS2[j & 1], j + 2 < nblk);
           if (j + 1 < nblk) dp_mma(j + 1);  // the dS pass of j has read dP(j)
           if (j + 2 < nblk) {
             if (!a.inorder) ptx::mbar_wait(ptx::smem_u32(ds_free), j & 1);  // dQ(j) read dS(j)
@@ -1268,7 +1293,7 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_dq2_kernel(const __grid_con
           if (j > 0 && !a.inorder) ptx::mbar_wait(ptx::smem_u32(ds_free), (j - 1) & 1);  // dQ(j-1) read dS
           dp_mma(j);
           if (j + 1 < nblk) s_mma(j + 1);  // the next scores under this tile's dS pass
-          dq_mma(j, tDP);
+          dq_mma(j, tDP, j + 1 < nblk);
         }
       }
     }
@@ -1320,7 +1345,7 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_dq2_kernel(const __grid_con
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_local(ptx::smem_u32(ds_full));
     }
-    ptx::mbar_wait(ptx::smem_u32(ds_free), (nblk - 1) & 1);
+    ptx::mbar_wait(ptx::smem_u32(acc_done), 0);
     ptx::tc_fence_after();
     // dQ columns [64 hf, 64 hf + 64) of this row
     if (cb < a.hd)
@@ -1346,7 +1371,7 @@ constexpr int fwd2_smem() {
 }
 template <int NSUB>
 constexpr int dkv2_smem() {
-  return 1024 + 2 * NSUB * kTile + 2 * (2 * NSUB * kTile + 1024) + 256;  // bars: 11 x 8 B + TMEM slot
+  return 1024 + 2 * NSUB * kTile + 2 * (2 * NSUB * kTile + 1024) + 256;  // bars: 12 x 8 B + TMEM slot
 }
 template <int NSUB>
 constexpr int dq2_smem() {  // Q, dO, 3 K stages, 2 V stages, bars

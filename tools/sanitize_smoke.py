@@ -39,5 +39,19 @@ m = mdl.Model(cfg)
 opt = optim.AdamW(m.w.named(), optim.OptimConfig())
 tok = torch.randint(0, 512, (1, 128), device="cuda", dtype=torch.int32)
 m.train_step(tok, tok, opt)
+# attention kernels over several kv / q tiles (dK/dV ring, 3-stage K ring of the dQ kernel),
+# every backward issue order, head dims 128 and 64, GQA 2
+from paper_2407_15892_b200 import attention as A  # noqa: E402
+for hd in (128, 64):
+    Sa, Ha, KVa = 700, 4, 2
+    q = torch.randn(Sa, Ha * hd, device="cuda").bfloat16()
+    k = torch.randn(Sa, KVa * hd, device="cuda").bfloat16()
+    v = torch.randn(Sa, KVa * hd, device="cuda").bfloat16()
+    do = torch.randn(Sa, Ha * hd, device="cuda").bfloat16()
+    o, lse = A.attention_forward(q, k, v, 1, Sa, Ha, KVa)
+    for order in (3, 0):
+        ctx.set_tuning("attn_bwd_order", order)
+        A.attention_backward(q, k, v, o, do, lse, 1, Sa, Ha, KVa)
+ctx.set_tuning("attn_bwd_order", 3)
 torch.cuda.synchronize()
 print("sanitize smoke done", float(st[2]))
