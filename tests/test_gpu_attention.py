@@ -120,3 +120,35 @@ def test_attention_rejects_bad_arguments():
     q = torch.randn(128, 64, device="cuda").bfloat16()
     with pytest.raises(ms.ConfigError):  # heads not a multiple of kv_heads
         A.attention_forward(q, q[:, :48].contiguous(), q[:, :48].contiguous(), 1, 128, 4, 3)
+
+
+@pytest.mark.parametrize("hd", [128, 64, 96])
+def test_backward_issue_orders_bitwise_equal(hd):
+    """Every backward issue order (tuning attn_bwd_order: dK/dV next scores
+    under the dS pass, dQ's dS over S) and the MMA completion-wait knob only
+    move when GEMMs are issued, not what they accumulate: dq / dk / dv are
+    bitwise equal to order 0 over several kv / q tiles (ring wrap-around,
+    GQA 4)."""
+    from paper_2407_15892_b200 import miniseq as ms
+
+    ctx = ms.Context.get(0)
+    torch.manual_seed(11)
+    S, H, KV = 900, 8, 2
+    q = torch.randn(S, H * hd, device="cuda").bfloat16()
+    k = torch.randn(S, KV * hd, device="cuda").bfloat16()
+    v = torch.randn(S, KV * hd, device="cuda").bfloat16()
+    do = torch.randn(S, H * hd, device="cuda").bfloat16()
+    o, lse = A.attention_forward(q, k, v, 1, S, H, KV)
+    try:
+        ctx.set_tuning("attn_bwd_order", 0)
+        ref = [t.clone() for t in A.attention_backward(q, k, v, o, do, lse, 1, S, H, KV)]
+        for order in (1, 2, 3):
+            for inorder in (0, 1):
+                ctx.set_tuning("attn_bwd_order", order)
+                ctx.set_tuning("attn_inorder", inorder)
+                got = A.attention_backward(q, k, v, o, do, lse, 1, S, H, KV)
+                for name, a, b in zip(("dq", "dk", "dv"), got, ref):
+                    assert torch.equal(a, b), (order, inorder, name)
+    finally:
+        ctx.set_tuning("attn_bwd_order", 3)
+        ctx.set_tuning("attn_inorder", 0)
