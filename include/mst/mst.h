@@ -139,7 +139,7 @@ MST_API int mst_ctx_set_profile_buffer(mst_ctx* ctx, void* dev_counters);
  *   "dynamic": 1 (default) CTA pairs pull tiles from the global LPT order
  *              through an atomic counter (a scheduler thread per pair claims
  *              up to 8 tiles ahead); 0 static per-pair LPT lists;
- *   "tma3d":   MN-major operands as 3-D tensor maps (process-wide, default 1);
+ *   "tma3d":   MN-major operands as 3-D tensor maps (default 1);
  *   "fused_head": 1 (default) block_step runs mst_lmhead_fused, 0 runs the
  *              separate forward + backward (logits recomputed);
  *   "chunked_block": 1 (default) block_step with M_mlp == M_head runs the
@@ -149,8 +149,15 @@ MST_API int mst_ctx_set_profile_buffer(mst_ctx* ctx, void* dev_counters);
  *   "wide", "wide_mask": wide tiles (two N blocks per CTA-pair tile) per GEMM
  *              of the chunk-wise block (default off); "debug_nblk" for
  *              mst_debug_gemm / mst_gemm;
- *   "pairs":   run the GEMMs on fewer CTA pairs (diagnostics).
- * Unknown keys are MST_ERR_CONFIG.  Changing a knob clears the schedule cache. */
+ *   "pairs":   run the GEMMs on fewer CTA pairs (diagnostics);
+ *   "pair_dw", "dl_rowscale", "k9_in_k1": chunk-wise schedule variants
+ *              (defaults 1, 1, 0);
+ *   "attn_fwd", "attn_bwd": attention kernel versions (default 2, 2);
+ *   "attn_bwd_order": backward issue orders, bit 0 dK/dV, bit 1 dQ (default 3);
+ *   "attn_inorder": 1 = no completion wait between dependent MMAs (default 0);
+ *   "attn_poly": forward exp2 pairs (of 4) on the FMA pipe, 0..3 (default 0).
+ * Every knob belongs to the context.  Unknown keys are MST_ERR_CONFIG.
+ * Changing a knob clears the schedule cache. */
 MST_API int mst_ctx_set_tuning(mst_ctx* ctx, const char* key, int value);
 
 /* ---------------------------------------------------------------- memtrack

@@ -63,9 +63,9 @@ struct Args {
   float scale2;        // softmax scale * log2(e)
   float scale;         // softmax scale
   int nqb;             // q (= kv) tiles per sequence
-  int inorder;         // g_mma_inorder
-  int poly;            // g_poly_exp: exp2 pairs (of every 4) on the FMA pipe in the forward softmax
-  int bwd_order;       // g_bwd_order: backward GEMM issue orders (bit 0 dK/dV, bit 1 dQ)
+  int inorder;         // AttnTuning::mma_inorder
+  int poly;            // AttnTuning::poly_exp: exp2 pairs (of every 4) on the FMA pipe in the forward softmax
+  int bwd_order;       // AttnTuning::bwd_order: backward GEMM issue orders (bit 0 dK/dV, bit 1 dQ)
 };
 
 // 2^x on the FMA / integer pipes (FlashAttention-4's split of the softmax
@@ -1391,18 +1391,6 @@ static_assert(fwd_smem<2>() <= 232448 && fwd2_smem<2>() <= 232448 && dkv_smem<2>
 
 static_assert(dkv2_smem<2>() <= 232448 && dq2_smem<2>() <= 232448, "shared memory");
 
-int g_fwd_version = 2;  // attn_fwd2_kernel (ping-pong) by default; 1 = one q tile per CTA
-int g_bwd_version = 2;  // attn_dkv2 / attn_dq2 (TMEM A operands, 2-stage ring) by default; 1 = the first kernels
-// 1: rely on tcgen05.mma executing in issue order (an MMA that overwrites TMEM
-// columns an earlier MMA of the same thread reads as its A operand is issued
-// without waiting for that MMA's completion); 0: wait for the commit first.
-int g_mma_inorder = 0;
-// Backward issue orders (tuning "attn_bwd_order", bit mask): bit 0 = dK/dV
-// kernel issues the next tile's scores under the dS pass; bit 1 = dQ kernel
-// writes dS over S so dP(j+1) does not wait for dQ(j).  0 = round-2 orders.
-int g_bwd_order = 3;
-int g_poly_exp = 0;  // forward softmax exp2 pairs (of 4) on the FMA pipe (tuning "attn_poly" 0..3; measured slower: off)
-
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -1438,7 +1426,7 @@ static cudaError_t set_attrs() {
   return e;
 }
 
-int forward(void* enc, cudaStream_t st, const AttnShape& s, const void* q, int64_t ldq, const void* k, int64_t ldk,
+int forward(void* enc, cudaStream_t st, const AttnTuning& tune, const AttnShape& s, const void* q, int64_t ldq, const void* k, int64_t ldk,
             const void* v, int64_t ldv, void* o, int64_t ldo, float* lse, const char** err) {
   Args a;
   std::memset(&a, 0, sizeof(a));
@@ -1459,21 +1447,21 @@ int forward(void* enc, cudaStream_t st, const AttnShape& s, const void* q, int64
   a.scale = 1.f / sqrtf(static_cast<float>(s.hd));
   a.scale2 = a.scale * kLog2e;
   a.nqb = (s.S + kBM - 1) / kBM;
-  a.inorder = g_mma_inorder;
-  a.poly = g_poly_exp;
+  a.inorder = tune.mma_inorder;
+  a.poly = tune.poly_exp;
   const dim3 grid(static_cast<unsigned>(a.nqb * s.heads * s.B));
   const dim3 grid2(static_cast<unsigned>((a.nqb + 1) / 2 * s.heads * s.B));
   cudaError_t e;
   static char msg[256];
   if (s.hd <= 64) {
     if ((e = set_attrs<1>()) != cudaSuccess) return *err = cudaGetErrorString(e), 2;
-    if (g_fwd_version == 2)
+    if (tune.fwd_version == 2)
       attn_fwd2_kernel<1><<<grid2, 384, fwd2_smem<1>(), st>>>(a);
     else
       attn_fwd_kernel<1><<<grid, kThreads, fwd_smem<1>(), st>>>(a);
   } else {
     if ((e = set_attrs<2>()) != cudaSuccess) return *err = cudaGetErrorString(e), 2;
-    if (g_fwd_version == 2)
+    if (tune.fwd_version == 2)
       attn_fwd2_kernel<2><<<grid2, 384, fwd2_smem<2>(), st>>>(a);
     else
       attn_fwd_kernel<2><<<grid, kThreads, fwd_smem<2>(), st>>>(a);
@@ -1483,7 +1471,7 @@ int forward(void* enc, cudaStream_t st, const AttnShape& s, const void* q, int64
     cudaFuncAttributes fa;
     cudaFuncGetAttributes(&fa, s.hd <= 64 ? (const void*)attn_fwd2_kernel<1> : (const void*)attn_fwd2_kernel<2>);
     snprintf(msg, sizeof(msg), "%s (fwd v%d: %d regs, max %d threads, %zu B static smem, %zu B local)",
-             cudaGetErrorString(e), g_fwd_version, fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes,
+             cudaGetErrorString(e), tune.fwd_version, fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes,
              fa.localSizeBytes);
     *err = msg;
     return 2;
@@ -1491,7 +1479,7 @@ int forward(void* enc, cudaStream_t st, const AttnShape& s, const void* q, int64
   return 0;
 }
 
-int backward(void* enc, cudaStream_t st, const AttnShape& s, const void* q, int64_t ldq, const void* k, int64_t ldk,
+int backward(void* enc, cudaStream_t st, const AttnTuning& tune, const AttnShape& s, const void* q, int64_t ldq, const void* k, int64_t ldk,
              const void* v, int64_t ldv, const void* o, int64_t ldo, const void* dout, int64_t lddo, const float* lse,
              void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv, int64_t lddv, float* delta, const char** err) {
   Args a;
@@ -1518,12 +1506,12 @@ int backward(void* enc, cudaStream_t st, const AttnShape& s, const void* q, int6
   a.scale = 1.f / sqrtf(static_cast<float>(s.hd));
   a.scale2 = a.scale * kLog2e;
   a.nqb = (s.S + kBM - 1) / kBM;
-  a.inorder = g_mma_inorder;
-  a.bwd_order = g_bwd_order;
+  a.inorder = tune.mma_inorder;
+  a.bwd_order = tune.bwd_order;
   const int64_t nrow = static_cast<int64_t>(s.B) * s.heads * s.S;
   const dim3 gkv(static_cast<unsigned>(a.nqb * s.kvh * s.B)), gq(static_cast<unsigned>(a.nqb * s.heads * s.B));
   cudaError_t e;
-  if (g_bwd_version == 2) {
+  if (tune.bwd_version == 2) {
     // workspace: delta [B*heads*S] | lse2p [B*heads*spad] | deltap [B*heads*spad]
     const int spad = a.nqb * kBM;
     float* lse2p = delta + ((nrow + 63) / 64) * 64;

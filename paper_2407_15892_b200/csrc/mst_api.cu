@@ -119,6 +119,7 @@ struct mst_ctx {
   // Which GEMMs of the chunk-wise block use wide tiles (bit mask, tuning key
   // "wide_mask"): 1 K3', 2 K5, 4 K2, 8 K9, 16 K7a, 32 K1.
   int wide_mask = 0;
+  mst_attn::AttnTuning attn;  // attention kernel knobs ("attn_*" tuning keys)
   // Chunk-wise block: K8 / K10 of chunks (2k, 2k+1) as one K = 2n accumulation
   // (one fp32 dW read-modify-write per two chunks; a second dG / dU / h^T /
   // X^T chunk set stays live through the next chunk's head), and K9(j) in
@@ -1316,20 +1317,20 @@ int mst_ctx_set_tuning(mst_ctx* c, const char* key, int value) {
   } else if (std::strcmp(key, "pairs") == 0) {  // diagnostics: run GEMMs on fewer CTA pairs
     if (value < 1 || value > c->max_pairs) return fail(MST_ERR_CONFIG, "pairs must be 1..%d", c->max_pairs);
     c->num_pairs = value;
-  } else if (std::strcmp(key, "attn_fwd") == 0) {  // attention forward kernel version (process-wide)
+  } else if (std::strcmp(key, "attn_fwd") == 0) {  // attention forward kernel version (per context)
     if (value != 1 && value != 2) return fail(MST_ERR_CONFIG, "attn_fwd must be 1 or 2");
-    mst_attn::g_fwd_version = value;
-  } else if (std::strcmp(key, "attn_poly") == 0) {  // forward softmax exp2 pairs of 4 on the FMA pipe (process-wide)
+    c->attn.fwd_version = value;
+  } else if (std::strcmp(key, "attn_poly") == 0) {  // forward softmax exp2 pairs of 4 on the FMA pipe (per context)
     if (value < 0 || value > 3) return fail(MST_ERR_CONFIG, "attn_poly must be 0..3");
-    mst_attn::g_poly_exp = value;
-  } else if (std::strcmp(key, "attn_bwd_order") == 0) {  // dK/dV GEMM issue order (process-wide)
+    c->attn.poly_exp = value;
+  } else if (std::strcmp(key, "attn_bwd_order") == 0) {  // dK/dV GEMM issue order (per context)
     if (value < 0 || value > 3) return fail(MST_ERR_CONFIG, "attn_bwd_order must be 0..3 (bit 0 dK/dV, bit 1 dQ)");
-    mst_attn::g_bwd_order = value;
+    c->attn.bwd_order = value;
   } else if (std::strcmp(key, "attn_inorder") == 0) {
-    mst_attn::g_mma_inorder = value != 0;
-  } else if (std::strcmp(key, "attn_bwd") == 0) {  // attention backward kernel version (process-wide)
+    c->attn.mma_inorder = value != 0;
+  } else if (std::strcmp(key, "attn_bwd") == 0) {  // attention backward kernel version (per context)
     if (value != 1 && value != 2) return fail(MST_ERR_CONFIG, "attn_bwd must be 1 or 2");
-    mst_attn::g_bwd_version = value;
+    c->attn.bwd_version = value;
   } else if (std::strcmp(key, "tma3d") == 0) {
     c->tma3d = value != 0;
   } else {
@@ -2600,7 +2601,7 @@ int mst_attention_forward(mst_ctx* c, void* stream, const void* q, int64_t ldq, 
     return fail(MST_ERR_SHAPE, "row stride smaller than heads * head_dim");
   const mst_attn::AttnShape sh{(int)batch, (int)seq, (int)heads, (int)kv_heads, (int)head_dim};
   const char* err = "";
-  const int r = mst_attn::forward(reinterpret_cast<void*>(c->encode), static_cast<cudaStream_t>(stream), sh, q, ldq, k,
+  const int r = mst_attn::forward(reinterpret_cast<void*>(c->encode), static_cast<cudaStream_t>(stream), c->attn, sh, q, ldq, k,
                                   ldk, v, ldv, o, ldo, lse, &err);
   if (r) return fail(r == 1 ? MST_ERR_CUDA : MST_ERR_CUDA, "attention forward: %s", err);
   c->launches++;
@@ -2633,7 +2634,7 @@ int mst_attention_backward(mst_ctx* c, void* stream, const void* q, int64_t ldq,
   if (!ws || ws_bytes < need) return fail(MST_ERR_CONFIG, "workspace too small (%zu < %zu)", ws_bytes, need);
   const mst_attn::AttnShape sh{(int)batch, (int)seq, (int)heads, (int)kv_heads, (int)head_dim};
   const char* err = "";
-  const int r = mst_attn::backward(reinterpret_cast<void*>(c->encode), static_cast<cudaStream_t>(stream), sh, q, ldq,
+  const int r = mst_attn::backward(reinterpret_cast<void*>(c->encode), static_cast<cudaStream_t>(stream), c->attn, sh, q, ldq,
                                    k, ldk, v, ldv, o, ldo, dout, lddo, lse, dq, lddq, dk, lddk, dv, lddv,
                                    static_cast<float*>(ws), &err);
   if (r) return fail(MST_ERR_CUDA, "attention backward: %s", err);
