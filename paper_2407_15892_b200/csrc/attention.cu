@@ -1409,8 +1409,6 @@ static int encode(void* enc, CUtensorMap* m, const void* base, int64_t ld, int64
 
 template <int NSUB>
 static cudaError_t set_attrs() {
-  static bool done = false;
-  if (done) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<NSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem<NSUB>());
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(attn_fwd2_kernel<NSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd2_smem<NSUB>());
@@ -1422,8 +1420,15 @@ static cudaError_t set_attrs() {
     e = cudaFuncSetAttribute(attn_dkv2_kernel<NSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, dkv2_smem<NSUB>());
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(attn_dq2_kernel<NSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, dq2_smem<NSUB>());
-  done = e == cudaSuccess;
   return e;
+}
+
+// Shared-memory limits of every attention kernel on the current device: once
+// per context (mst_ctx_create), like the GEMM engine's, since a function
+// attribute is per device.
+cudaError_t init_device() {
+  cudaError_t e = set_attrs<1>();
+  return e == cudaSuccess ? set_attrs<2>() : e;
 }
 
 int forward(void* enc, cudaStream_t st, const AttnTuning& tune, const AttnShape& s, const void* q, int64_t ldq, const void* k, int64_t ldk,
@@ -1452,15 +1457,13 @@ int forward(void* enc, cudaStream_t st, const AttnTuning& tune, const AttnShape&
   const dim3 grid(static_cast<unsigned>(a.nqb * s.heads * s.B));
   const dim3 grid2(static_cast<unsigned>((a.nqb + 1) / 2 * s.heads * s.B));
   cudaError_t e;
-  static char msg[256];
+  thread_local char msg[256];
   if (s.hd <= 64) {
-    if ((e = set_attrs<1>()) != cudaSuccess) return *err = cudaGetErrorString(e), 2;
     if (tune.fwd_version == 2)
       attn_fwd2_kernel<1><<<grid2, 384, fwd2_smem<1>(), st>>>(a);
     else
       attn_fwd_kernel<1><<<grid, kThreads, fwd_smem<1>(), st>>>(a);
   } else {
-    if ((e = set_attrs<2>()) != cudaSuccess) return *err = cudaGetErrorString(e), 2;
     if (tune.fwd_version == 2)
       attn_fwd2_kernel<2><<<grid2, 384, fwd2_smem<2>(), st>>>(a);
     else
@@ -1523,11 +1526,9 @@ int backward(void* enc, cudaStream_t st, const AttnTuning& tune, const AttnShape
         static_cast<const uint16_t*>(o), ldo, static_cast<const uint16_t*>(dout), lddo, lse, lse2p, deltap, s.B, s.S,
         s.heads, s.hd, spad);
     if (s.hd <= 64) {
-      if ((e = set_attrs<1>()) != cudaSuccess) return *err = cudaGetErrorString(e), 2;
       attn_dkv2_kernel<1><<<gkv, kThreads2, dkv2_smem<1>(), st>>>(a);
       attn_dq2_kernel<1><<<gq, kThreads2, dq2_smem<1>(), st>>>(a);
     } else {
-      if ((e = set_attrs<2>()) != cudaSuccess) return *err = cudaGetErrorString(e), 2;
       attn_dkv2_kernel<2><<<gkv, kThreads2, dkv2_smem<2>(), st>>>(a);
       attn_dq2_kernel<2><<<gq, kThreads2, dq2_smem<2>(), st>>>(a);
     }
@@ -1535,11 +1536,9 @@ int backward(void* enc, cudaStream_t st, const AttnTuning& tune, const AttnShape
     attn_delta_kernel<<<static_cast<unsigned>((nrow + 255) / 256), 256, 0, st>>>(
         static_cast<const uint16_t*>(o), ldo, static_cast<const uint16_t*>(dout), lddo, delta, s.B, s.S, s.heads, s.hd);
     if (s.hd <= 64) {
-      if ((e = set_attrs<1>()) != cudaSuccess) return *err = cudaGetErrorString(e), 2;
       attn_dkv_kernel<1><<<gkv, kThreads, dkv_smem<1>(), st>>>(a);
       attn_dq_kernel<1><<<gq, kThreads, dq_smem<1>(), st>>>(a);
     } else {
-      if ((e = set_attrs<2>()) != cudaSuccess) return *err = cudaGetErrorString(e), 2;
       attn_dkv_kernel<2><<<gkv, kThreads, dkv_smem<2>(), st>>>(a);
       attn_dq_kernel<2><<<gq, kThreads, dq_smem<2>(), st>>>(a);
     }

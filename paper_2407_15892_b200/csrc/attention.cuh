@@ -27,6 +27,9 @@ struct AttnShape {
   int B, S, heads, kvh, hd;
 };
 
+// Kernel attributes on the current device (called once per context).
+cudaError_t init_device();
+
 // Return 0 on success; otherwise *err names the failure (1: tensor map, 2: CUDA).
 int forward(void* encode_fn, cudaStream_t st, const AttnTuning& tune, const AttnShape& s, const void* q, int64_t ldq, const void* k,
             int64_t ldk, const void* v, int64_t ldv, void* o, int64_t ldo, float* lse, const char** err);

@@ -1188,6 +1188,7 @@ int mst_ctx_create(int device, mst_ctx** out) {
   if (const char* dy = getenv("MST_DYNAMIC")) c->dynamic = atoi(dy) != 0;
   e = cudaFuncSetAttribute(mst::mst_grouped_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            mst::kSmemBytes);
+  if (e == cudaSuccess) e = mst_attn::init_device();
   if (e != cudaSuccess) {
     delete c;
     return fail(MST_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
